@@ -1,0 +1,201 @@
+/*
+ * glr_b200.h — C ABI of the B200-native GLR hot path (libglr_b200.so).
+ *
+ * This is the drop-in boundary for the data-parallel core of the reference
+ * package `glr` (/root/reference/pkg/src/glr). The reference has no native
+ * code of its own: every entry point below replaces a numpy/scipy call site
+ * of the reference, cited as file:line. The Python package
+ * `paper_2301_03047_b200` (the reference-facing host layer) is the only
+ * in-tree caller; INTEGRATION.md shows the ctypes binding a maintainer of the
+ * reference would add.
+ *
+ * Conventions
+ *  - Every pointer argument named *_d is a DEVICE pointer owned by the caller.
+ *    The library never allocates in a hot call; scratch comes from the caller
+ *    through an explicit workspace pointer sized by the matching *_workspace
+ *    query.
+ *  - `stream` is a cudaStream_t passed as void*; all work is stream-ordered.
+ *  - Images are (H, W, C) row-major, channels last, float64 — the reference
+ *    layout (glr/__init__.py:3-4). Anchors/positions are int32 (row, col)
+ *    pairs of patch top-left corners (glr/patches.py:5-6).
+ *  - Return value: GLR_OK or an error code; glr_last_error() gives a
+ *    thread-local message. Validation happens before any launch.
+ */
+#ifndef GLR_B200_H
+#define GLR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  GLR_OK = 0,
+  GLR_ERR_INVALID = 1,     /* bad shape / argument (reference raises ValueError) */
+  GLR_ERR_BOUNDS = 2,      /* anchor out of bounds (glr/patches.py:36-40)        */
+  GLR_ERR_NONFINITE = 3,   /* non-finite group entries (glr/lowrank.py:54-55)     */
+  GLR_ERR_CUDA = 4,        /* CUDA runtime / driver failure                        */
+  GLR_ERR_UNSUPPORTED = 5, /* shape outside what the kernels support               */
+  GLR_ERR_WORKSPACE = 6    /* workspace too small                                  */
+};
+
+/* ---- library ------------------------------------------------------------ */
+
+const char* glr_last_error(void);
+int glr_version(void);
+/* Number of SMs and compute capability of the current device (sanity probe). */
+int glr_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---- (1) edges: glr/edges.py:53-85 ---------------------------------------
+ * glr_sobel: per-channel 3x3 Sobel correlation with edge-replicate borders,
+ * fp64 with scipy.ndimage.correlate's accumulation order (edges.py:53-64).
+ * x_d (H,W,C) -> gh_d, gv_d (H,W,C).                                         */
+int glr_sobel(const double* x_d, int H, int W, int C, double* gh_d, double* gv_d, void* stream);
+
+/* glr_edge_stack: sign-split thresholding (edges.py:67-85) of gh/gv into
+ *  - maps_d  (optional, may be NULL): u8 {0,1} (4,H,W,C) in the order
+ *            h_pos, h_neg, v_pos, v_neg (EdgeMaps.as_tuple, edges.py:33-34);
+ *  - stack_d (optional): the u8 im2col-friendly "expanded" stack used by the
+ *            heat-map GEMM, (H,W,e*4C) with stack[r][c][p*4C+m*C+ch] =
+ *            map_m[r+p][c][ch] for p<e (0 past the last row).
+ * th is relative to max|g| when relative != 0 (edges.py:79-80).
+ * ws_d: 2 doubles of scratch (the two maxima).                              */
+int glr_edge_stack(const double* gh_d, const double* gv_d, int H, int W, int C, double th,
+                   int relative, int expand, uint8_t* maps_d, uint8_t* stack_d, double* ws_d,
+                   void* stream);
+
+/* glr_stack_from_maps: same expanded stack from caller-provided binary maps
+ * (4,H,W,C) u8 — the similarity_heatmap(EdgeMaps, ...) entry (matching.py:140). */
+int glr_stack_from_maps(const uint8_t* maps_d, int H, int W, int C, int expand, uint8_t* stack_d,
+                        void* stream);
+
+/* ---- (1) exemplars: glr/edges.py:88-162, solvers.py:154-167 ---------------
+ * glr_corner_response: channel-mean gradient magnitude -> Shi-Tomasi
+ * min-eigenvalue response (edges.py:88-97, 110-112), bitwise equal to the
+ * reference's fp64 evaluation order. resp_d (H,W). ws: glr_corner_workspace. */
+size_t glr_corner_workspace(int H, int W, int C);
+int glr_corner_response(const double* x_d, int H, int W, int C, double* resp_d, void* ws_d,
+                        void* stream);
+
+/* glr_corners: threshold >= quality*max, order (score desc, row, col), greedy
+ * Chebyshev NMS, at most max_n picks (edges.py:113-128).
+ * out_rc_d: 2*max_n int32; out_n_d: 1 int32. ws: glr_nms_workspace.          */
+size_t glr_nms_workspace(int H, int W);
+int glr_corners(const double* resp_d, int H, int W, int max_n, int nms_radius, double quality,
+                int32_t* out_rc_d, int32_t* out_n_d, void* ws_d, size_t ws_bytes, void* stream);
+
+/* glr_select_anchors: corners -> clamped top-left anchors, deduplicated in
+ * order, then the row-major uniform grid if grid_interval > 0
+ * (edges.py:131-162). anchors_d: 2*max_anchors int32; tags_d: u8 per anchor
+ * (0 corner, 1 uniform); n_d: 1 int32. ws: glr_anchor_workspace.            */
+size_t glr_anchor_workspace(int H, int W);
+int glr_select_anchors(const int32_t* corners_rc_d, const int32_t* n_corners_d, int max_corners,
+                       int H, int W, int P, int grid_interval, int max_anchors,
+                       int32_t* anchors_d, uint8_t* tags_d, int32_t* n_d, void* ws_d,
+                       void* stream);
+
+/* ---- (2) global similarity heat map: glr/matching.py:140-167 ---------------
+ * heat[n][u*ow+v] = sum_{p,q,ch<4C} E[u+p][v+q][ch] * E[r_n+p][c_n+q][ch],
+ * exact integer overlap counts on tcgen05 tensor cores (kind::i8, s32 accum).
+ * Exemplar-major u16 output, positions flattened row-major (oh = H-P+1,
+ * ow = W-P+1). n_dev_d (optional) caps the exemplar count on device.
+ * ws: glr_heat_workspace (the packed exemplar operand).                     */
+int glr_heat_expand_factor(int C, int P);
+size_t glr_heat_workspace(int C, int P, int n_max);
+int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, int expand,
+                 const int32_t* anchors_d, int n_max, const int32_t* n_dev_d, uint16_t* heat_d,
+                 void* ws_d, size_t ws_bytes, void* stream);
+
+/* ---- (3) top-K selection: glr/matching.py:170-231 ---------------------------
+ * Exact tie-ordered greedy selection per exemplar: slot 0 = anchor, then
+ * (score desc, flat index asc) skipping Chebyshev <= sep of any chosen,
+ * relaxed to sep = 0, then padded with the anchor.
+ * positions_d: n*K*2 int32; padded_d: n int32.                              */
+size_t glr_topk_workspace(int n_max, int K, int sep);
+int glr_topk(const uint16_t* heat_d, int n_max, const int32_t* n_dev_d, int oh, int ow,
+             int max_score, const int32_t* anchors_d, int K, int sep, int32_t* positions_d,
+             int32_t* padded_d, void* ws_d, size_t ws_bytes, void* stream);
+
+/* ---- (3) gather: glr/patches.py:43-54 ---------------------------------------
+ * groups_d: (G, K, m) fp64, column j of group g = x[r:r+P, c:c+P, :].ravel()
+ * (m = P*P*C).                                                              */
+int glr_gather(const double* x_d, int H, int W, int C, int P, const int32_t* positions_d, int G,
+               int K, double* groups_d, void* stream);
+
+/* ---- (4) WNNM: glr/lowrank.py:46-65 ------------------------------------------
+ * Batched weighted singular-value shrinkage of G groups (K columns of m
+ * rows each, column-major per group) via an fp64 Gram matrix, a one-sided
+ * cyclic Jacobi eigensolver and out = M * V diag(f(s)/s) V^T.
+ * sigma: noise level (WnnmParams.noise_sigma); uniform_weight < 0 = unused.
+ * nonfinite_d (optional): set to 1 when a group holds a non-finite value.   */
+size_t glr_wnnm_workspace(int G, int K);
+int glr_wnnm(const double* groups_d, int G, int m, int K, double sigma, double c_weight,
+             double eps, double uniform_weight, double* out_d, int32_t* nonfinite_d, void* ws_d,
+             size_t ws_bytes, void* stream);
+
+/* ---- (4)+(5) fused regularizer: glr/lowrank.py:68-87 + patches.py:57-70 ----
+ * For every group g < n: gather from x, WNNM, and scatter-add the denoised
+ * patches into acc_d, an int64 fixed-point numerator (value * 2^frac_bits),
+ * so aggregation is deterministic and rank-count invariant.               */
+int glr_wnnm_scatter(const double* x_d, int H, int W, int C, int P, const int32_t* positions_d,
+                     int n_max, const int32_t* n_dev_d, int K, double sigma, double c_weight,
+                     double eps, int frac_bits, int64_t* acc_d, void* ws_d, size_t ws_bytes,
+                     void* stream);
+
+/* glr_scatter_count: cnt[r][c] += 1 for every pixel covered by every patch
+ * (channel-invariant form of scatter_group's counter, patches.py:70).      */
+int glr_scatter_count(const int32_t* positions_d, int n_max, const int32_t* n_dev_d, int K,
+                      int P, int H, int W, int32_t* cnt_d, void* stream);
+
+/* glr_scatter_add_f64: exact-API scatter_group (patches.py:57-70) of fp64
+ * groups into fp64 acc/cnt, deterministic (one thread per output pixel).  */
+int glr_scatter_add_f64(const double* groups_d, const int32_t* positions_d, int G, int K, int P,
+                        int H, int W, int C, double* acc_d, double* cnt_d, void* stream);
+
+/* glr_normalize: z = acc/cnt where cnt > 0 else x (lowrank.py:84-87).       */
+int glr_normalize(const int64_t* acc_d, const int32_t* cnt_d, const double* x_d, int H, int W,
+                  int C, int frac_bits, double* z_d, void* stream);
+
+/* ---- (6) sensing operators + GAP update: glr/operators.py, solvers.py:298-301
+ * Mask-sum family (CACTI operators.py:35-59, MSFA operators.py:160-185):
+ *   A x = sum_t M_t x_t,  A^T y = M_t y,  gram = sum_t M_t^2.
+ * glr_gap_masksum fuses normalize + z + A^T(safe_div(y - A z, gram)),
+ * clip [lo, hi], and the per-block partial residual ||y - A x||^2.
+ * acc_d/cnt_d may be NULL (then z = x_in). x_out may alias x_in.
+ * resid_d: 1 double (deterministic reduction).                              */
+int glr_masksum_forward(const double* x_d, const double* masks_d, int H, int W, int T,
+                        double* y_d, void* stream);
+int glr_masksum_adjoint(const double* y_d, const double* masks_d, int H, int W, int T,
+                        double* x_d, void* stream);
+size_t glr_gap_workspace(int H, int W);
+int glr_gap_masksum(const int64_t* acc_d, const int32_t* cnt_d, int frac_bits,
+                    const double* x_in_d, const double* masks_d, const double* y_d,
+                    const double* gram_d, int H, int W, int T, double lo, double hi,
+                    double* x_out_d, double* resid_d, void* ws_d, void* stream);
+
+/* Masked unitary 2-D DFT (operators.py:65-89): real (C=1, adjoint keeps the
+ * real part) or complex (C=2, (re,im) channels) images. y is complex128
+ * interleaved (H,W,2). glr_gap_fourier fuses normalize + projection + clip
+ * + residual like glr_gap_masksum. ws: glr_fft_workspace.                  */
+size_t glr_fft_workspace(int H, int W);
+int glr_fourier_forward(const double* x_d, const double* mask_d, int H, int W, int C,
+                        double* y_d, void* ws_d, void* stream);
+int glr_fourier_adjoint(const double* y_d, const double* mask_d, int H, int W, int C,
+                        double* x_d, void* ws_d, void* stream);
+int glr_gap_fourier(const int64_t* acc_d, const int32_t* cnt_d, int frac_bits,
+                    const double* x_in_d, const double* mask_d, const double* y_d, int H, int W,
+                    int C, int clip, double lo, double hi, double* x_out_d, double* resid_d,
+                    void* ws_d, void* stream);
+
+/* Squared-error sum vs a reference for PSNR (metrics.py:26-37), of
+ * clip(x, 0, peak), deterministic. out_d: 1 double.                         */
+int glr_sq_err(const double* x_d, const double* ref_d, int n, double peak, double* out_d,
+               void* ws_d, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GLR_B200_H */

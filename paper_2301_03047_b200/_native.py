@@ -1,0 +1,148 @@
+"""ctypes binding of libglr_b200.so (include/glr_b200.h).
+
+The product path has no CPU fallback: importing a compute entry point
+without the built library, or calling it without a CUDA device, raises
+``NativeUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_LIB_PATH = Path(__file__).resolve().parent / "libglr_b200.so"
+
+GLR_OK = 0
+GLR_ERR_INVALID = 1
+GLR_ERR_BOUNDS = 2
+GLR_ERR_NONFINITE = 3
+GLR_ERR_CUDA = 4
+GLR_ERR_UNSUPPORTED = 5
+GLR_ERR_WORKSPACE = 6
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA extension is missing or no CUDA device is visible."""
+
+
+class GlrCudaError(RuntimeError):
+    """A CUDA launch or runtime call inside libglr_b200 failed."""
+
+
+vp = C.c_void_p
+i32 = C.c_int
+i64 = C.c_int64
+f64 = C.c_double
+sz = C.c_size_t
+
+# name -> (restype, argtypes); mirrors include/glr_b200.h
+SIGNATURES: dict[str, tuple] = {
+    "glr_last_error": (C.c_char_p, []),
+    "glr_version": (i32, []),
+    "glr_device_info": (i32, [vp, vp, vp]),
+    "glr_sobel": (i32, [vp, i32, i32, i32, vp, vp, vp]),
+    "glr_edge_stack": (i32, [vp, vp, i32, i32, i32, f64, i32, i32, vp, vp, vp, vp]),
+    "glr_stack_from_maps": (i32, [vp, i32, i32, i32, i32, vp, vp]),
+    "glr_corner_workspace": (sz, [i32, i32, i32]),
+    "glr_corner_response": (i32, [vp, i32, i32, i32, vp, vp, vp]),
+    "glr_nms_workspace": (sz, [i32, i32]),
+    "glr_corners": (i32, [vp, i32, i32, i32, i32, f64, vp, vp, vp, sz, vp]),
+    "glr_anchor_workspace": (sz, [i32, i32]),
+    "glr_select_anchors": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp]),
+    "glr_heat_expand_factor": (i32, [i32, i32]),
+    "glr_heat_workspace": (sz, [i32, i32, i32]),
+    "glr_heat_map": (i32, [vp, i32, i32, i32, i32, i32, vp, i32, vp, vp, vp, sz, vp]),
+    "glr_topk_workspace": (sz, [i32, i32, i32]),
+    "glr_topk": (i32, [vp, i32, vp, i32, i32, i32, vp, i32, i32, vp, vp, vp, sz, vp]),
+    "glr_gather": (i32, [vp, i32, i32, i32, i32, vp, i32, i32, vp, vp]),
+    "glr_wnnm_workspace": (sz, [i32, i32]),
+    "glr_wnnm": (i32, [vp, i32, i32, i32, f64, f64, f64, f64, vp, vp, vp, sz, vp]),
+    "glr_wnnm_scatter": (i32, [vp, i32, i32, i32, i32, vp, i32, vp, i32, f64, f64, f64, i32, vp,
+                               vp, sz, vp]),
+    "glr_scatter_count": (i32, [vp, i32, vp, i32, i32, i32, i32, vp, vp]),
+    "glr_scatter_add_f64": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, vp, vp, vp]),
+    "glr_normalize": (i32, [vp, vp, vp, i32, i32, i32, i32, vp, vp]),
+    "glr_masksum_forward": (i32, [vp, vp, i32, i32, i32, vp, vp]),
+    "glr_masksum_adjoint": (i32, [vp, vp, i32, i32, i32, vp, vp]),
+    "glr_gap_workspace": (sz, [i32, i32]),
+    "glr_gap_masksum": (i32, [vp, vp, i32, vp, vp, vp, vp, i32, i32, i32, f64, f64, vp, vp, vp,
+                              vp]),
+    "glr_fft_workspace": (sz, [i32, i32]),
+    "glr_fourier_forward": (i32, [vp, vp, i32, i32, i32, vp, vp, vp]),
+    "glr_fourier_adjoint": (i32, [vp, vp, i32, i32, i32, vp, vp, vp]),
+    "glr_gap_fourier": (i32, [vp, vp, i32, vp, vp, vp, i32, i32, i32, i32, f64, f64, vp, vp, vp,
+                              vp]),
+    "glr_sq_err": (i32, [vp, vp, i32, f64, vp, vp, vp]),
+}
+
+_lib = None
+
+
+def lib_path() -> Path:
+    return _LIB_PATH
+
+
+def load(require_gpu: bool = False):
+    """Load the shared library (once). ``require_gpu`` also checks for a CUDA
+    device, which every compute entry point needs."""
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            raise NativeUnavailable(
+                f"{_LIB_PATH.name} is not built; run `python -c \"import __graft_entry__ as g; "
+                f"g.build()\"` (no CPU fallback exists)")
+        lib = C.CDLL(str(_LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    if require_gpu:
+        import torch
+        if not torch.cuda.is_available():
+            raise NativeUnavailable("no CUDA device visible: the GLR B200 path has no CPU fallback")
+    return _lib
+
+
+def last_error() -> str:
+    return load().glr_last_error().decode(errors="replace")
+
+
+def check(status: int, what: str = "") -> None:
+    """Map a C status code onto the reference's exception types."""
+    if status == GLR_OK:
+        return
+    msg = last_error()
+    if what:
+        msg = f"{what}: {msg}"
+    if status in (GLR_ERR_INVALID, GLR_ERR_BOUNDS, GLR_ERR_NONFINITE):
+        raise ValueError(msg)
+    if status == GLR_ERR_CUDA:
+        raise GlrCudaError(msg)
+    raise RuntimeError(f"glr status {status}: {msg}")
+
+
+def call(name: str, *args) -> int:
+    lib = load(require_gpu=True)
+    st = getattr(lib, name)(*args)
+    check(st, name)
+    return st
+
+
+def query(name: str, *args):
+    """Host-only size / geometry queries (no device needed)."""
+    return getattr(load(), name)(*args)
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None passes NULL)."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream

@@ -1,0 +1,316 @@
+// (2) Global similarity heat map as an implicit GEMM on tcgen05 tensor cores.
+//
+// Reference: glr/matching.py:140-167 (similarity_heatmap, im2col branch
+// :145-156): heat[u,v,n] = sum over the P x P x 4C window of the product of
+// the binary edge stack at position (u,v) and at exemplar anchor n. The
+// reference runs this as an OpenBLAS sgemm on an explicit im2col copy; here
+// the im2col is never materialised:
+//
+//   * The edge stack is stored u8 {0,1} as (H, W, Ce) with Ce = e*4C ("e-row
+//     expanded": channel p*4C+k of pixel (r,c) holds map_k(r+p, c)). For a
+//     fixed output row u and slab s, the K-run of position v is the
+//     contiguous byte range stack[u+s*e][v .. v+P-1][0..Ce-1] of length
+//     L = P*Ce, and consecutive v are Ce bytes apart. A 3-D TMA map with
+//     dims {L, ow, H} and strides {Ce, W*Ce} therefore addresses the
+//     overlapping im2col rows directly; one TMA box = 128 positions x 128 K.
+//   * The exemplar operand B (Npad x Kp, K-major, zero-padded) is gathered
+//     once per refresh from the same stack (exemplar_pack_kernel).
+//   * u8 x u8 -> s32 on tcgen05.mma kind::i8 is exact for every count
+//     (max 4*C*P^2); the accumulator lives in TMEM (128 lanes x 256 cols).
+//   * Output: exemplar-major u16 heat[n][u*ow+v] (flat index = the
+//     reference's row-major slice index, matching.py:177-178).
+//
+// Warp roles (128 threads): warp0.lane0 = TMA producer, warp1.lane0 = MMA
+// issuer, warp1 owns the TMEM allocation, all four warps run the epilogue.
+#include <cstdio>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace glr {
+
+namespace heat {
+constexpr int BM = 128;      // positions per tile (UMMA M)
+constexpr int BN = 256;      // exemplars per tile (UMMA N)
+constexpr int BK = 128;      // bytes of K per stage (one 128B swizzle row)
+constexpr int UK = 32;       // K per tcgen05.mma kind::i8
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK;
+constexpr int B_BYTES = BN * BK;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr uint32_t TMEM_COLS = 256;
+}  // namespace heat
+
+struct HeatGeom {
+  int H, W, C4, P, e, Ce, S, L, kchunks, Kp, oh, ow;
+};
+
+static HeatGeom heat_geom(int H, int W, int C, int P, int e) {
+  HeatGeom g;
+  g.H = H;
+  g.W = W;
+  g.C4 = 4 * C;
+  g.P = P;
+  g.e = e;
+  g.Ce = e * 4 * C;
+  g.S = (int)cdiv(P, e);
+  g.L = P * g.Ce;
+  g.kchunks = (int)cdiv(g.L, heat::BK);
+  g.Kp = g.S * g.kchunks * heat::BK;
+  g.oh = H - P + 1;
+  g.ow = W - P + 1;
+  return g;
+}
+
+struct HeatParams {
+  int oh, ow, M, n_max, n_tiles, m_tiles_per_row, S, kchunks, e;
+  const int32_t* n_dev;
+  uint16_t* heat;
+};
+
+__global__ void __launch_bounds__(128, 1)
+    heat_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                     const __grid_constant__ CUtensorMap tmB, HeatParams p) {
+  using namespace heat;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* done = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int n_tile = blockIdx.x % p.n_tiles;
+  const int m_tile = blockIdx.x / p.n_tiles;
+  const int n0 = n_tile * BN;
+  const int N = p.n_dev ? min(*p.n_dev, p.n_max) : p.n_max;
+  if (n0 >= N) return;  // block-uniform, before any barrier
+  const int u = m_tile / p.m_tiles_per_row;
+  const int v0 = (m_tile % p.m_tiles_per_row) * BM;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+  }
+  if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int num_k = p.S * p.kchunks;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer ----
+    for (int kb = 0; kb < num_k; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (kb / STAGES) & 1;
+      if (kb >= STAGES) mbar_wait(&empty[s], ph ^ 1);
+      mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+      const int slab = kb / p.kchunks;
+      const int kc = kb - slab * p.kchunks;
+      tma_load_3d(sA + s * A_BYTES, &tmA, &full[s], kc * BK, v0, u + slab * p.e);
+      tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, n0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer ----
+    constexpr uint32_t idesc = idesc_u8_s32(BM, BN);
+    for (int kb = 0; kb < num_k; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (kb / STAGES) & 1;
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      const uint64_t ad = smem_desc_k_sw128(sA + s * A_BYTES);
+      const uint64_t bd = smem_desc_k_sw128(sB + s * B_BYTES);
+#pragma unroll
+      for (int k = 0; k < BK / UK; ++k) {
+        // advance the start address by k*32 bytes inside the 128B swizzle atom
+        umma_i8(tmem, ad + (uint64_t)((k * UK) >> 4), bd + (uint64_t)((k * UK) >> 4), idesc,
+                (kb | k) != 0);
+      }
+      umma_commit(&empty[s]);
+    }
+    umma_commit(done);
+  }
+  __syncwarp();
+
+  // ---- epilogue: TMEM -> registers -> u16 exemplar-major rows ----
+  mbar_wait(done, 0);
+  tc_fence_after();
+  const int v = v0 + warp * 32 + lane;
+  const bool v_ok = v < p.ow;
+  uint16_t* out = p.heat + (size_t)u * p.ow + v;
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * 32), r);
+    tmem_ld_wait();
+    const int nb = n0 + c * 32;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int n = nb + j;
+      if (v_ok && n < N) out[(size_t)n * p.M] = (uint16_t)r[j];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
+}
+
+// B operand: bmat[n][s*kchunks*BK + k'] = stack[r_n + s*e][c_n + k'/Ce][k' % Ce] for
+// k' < L, zero for the K padding, for the padded exemplars and past row H.
+__global__ void exemplar_pack_kernel(const uint8_t* __restrict__ stack, HeatGeom g,
+                                     const int32_t* __restrict__ anchors, int n_max,
+                                     const int32_t* n_dev, int n_pad, uint8_t* __restrict__ bmat) {
+  const int N = n_dev ? min(*n_dev, n_max) : n_max;
+  const int row_bytes = g.Kp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)n_pad * row_bytes;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(i / row_bytes);
+    const int k = (int)(i - (int64_t)n * row_bytes);
+    const int slab = k / (g.kchunks * heat::BK);
+    const int kk = k - slab * g.kchunks * heat::BK;
+    uint8_t val = 0;
+    if (n < N && kk < g.L) {
+      const int ch = kk % g.Ce;
+      // expanded channel ch holds map row (anchor row + slab*e + ch / 4C); rows
+      // at or past P belong to no patch and stay zero
+      if (slab * g.e + ch / g.C4 < g.P) {
+        const int r = anchors[2 * n] + slab * g.e;
+        const int c = anchors[2 * n + 1] + kk / g.Ce;
+        val = stack[((size_t)r * g.W + c) * g.Ce + ch];
+      }
+    }
+    bmat[i] = val;
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+}  // namespace glr
+
+using namespace glr;
+
+extern "C" int glr_heat_expand_factor(int C, int P) {
+  // Smallest padded K (then the smallest expansion) among e in [1, max(P,4)]
+  // whose pixel stride e*4C is a multiple of 16 bytes (TMA stride rule);
+  // e = 4 always qualifies. Expanded rows at or past P are zero in B.
+  int best_e = -1;
+  int64_t best_k = 0;
+  for (int e = 1; e <= (P > 4 ? P : 4); ++e) {
+    if ((4 * C * e) % 16 != 0) continue;
+    HeatGeom g = heat_geom(P, P, C, P, e);
+    if (best_e < 0 || g.Kp < best_k) {
+      best_e = e;
+      best_k = g.Kp;
+    }
+  }
+  return best_e;
+}
+
+extern "C" size_t glr_heat_workspace(int C, int P, int n_max) {
+  int e = glr_heat_expand_factor(C, P);
+  if (e < 1) return 0;
+  HeatGeom g = heat_geom(P, P, C, P, e);
+  size_t n_pad = (size_t)cdiv(n_max, heat::BN) * heat::BN;
+  return n_pad * (size_t)g.Kp + 256;
+}
+
+extern "C" int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, int expand,
+                            const int32_t* anchors_d, int n_max, const int32_t* n_dev_d,
+                            uint16_t* heat_d, void* ws_d, size_t ws_bytes, void* stream) {
+  GLR_REQUIRE(P >= 1 && P <= H && P <= W && C >= 1, GLR_ERR_INVALID,
+              "heat_map: bad shape H=%d W=%d C=%d P=%d", H, W, C, P);
+  GLR_REQUIRE(expand >= 1 && expand <= (P > 4 ? P : 4) && (4 * C * expand) % 16 == 0,
+              GLR_ERR_INVALID,
+              "heat_map: expand factor %d invalid for C=%d", expand, C);
+  if (n_max <= 0) return GLR_OK;
+  HeatGeom g = heat_geom(H, W, C, P, expand);
+  GLR_REQUIRE(4 * C * P * P <= 65535, GLR_ERR_UNSUPPORTED,
+              "heat_map: max score %d does not fit u16", 4 * C * P * P);
+  const int n_pad = (int)cdiv(n_max, heat::BN) * heat::BN;
+  GLR_REQUIRE(ws_bytes >= (size_t)n_pad * g.Kp, GLR_ERR_WORKSPACE,
+              "heat_map: workspace %zu < %zu", ws_bytes, (size_t)n_pad * g.Kp);
+  auto encode = get_encode_fn();
+  GLR_REQUIRE(encode != nullptr, GLR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* bmat = reinterpret_cast<uint8_t*>(ws_d);
+
+  {
+    int64_t total = (int64_t)n_pad * g.Kp;
+    int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
+    exemplar_pack_kernel<<<blocks, 256, 0, st>>>(stack_d, g, anchors_d, n_max, n_dev_d, n_pad,
+                                                 bmat);
+    GLR_CUDA(cudaGetLastError());
+  }
+
+  CUtensorMap tmA, tmB;
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)g.L, (cuuint64_t)g.ow, (cuuint64_t)H};
+    cuuint64_t strides[2] = {(cuuint64_t)g.Ce, (cuuint64_t)W * g.Ce};
+    cuuint32_t box[3] = {heat::BK, heat::BM, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode(&tmA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)stack_d, dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    GLR_REQUIRE(r == CUDA_SUCCESS, GLR_ERR_CUDA, "cuTensorMapEncodeTiled(A) failed: %d", (int)r);
+  }
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)g.Kp, (cuuint64_t)n_pad};
+    cuuint64_t strides[1] = {(cuuint64_t)g.Kp};
+    cuuint32_t box[2] = {heat::BK, heat::BN};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)bmat, dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    GLR_REQUIRE(r == CUDA_SUCCESS, GLR_ERR_CUDA, "cuTensorMapEncodeTiled(B) failed: %d", (int)r);
+  }
+
+  HeatParams hp;
+  hp.oh = g.oh;
+  hp.ow = g.ow;
+  hp.M = g.oh * g.ow;
+  hp.n_max = n_max;
+  hp.n_tiles = n_pad / heat::BN;
+  hp.m_tiles_per_row = (int)cdiv(g.ow, heat::BM);
+  hp.S = g.S;
+  hp.kchunks = g.kchunks;
+  hp.e = g.e;
+  hp.n_dev = n_dev_d;
+  hp.heat = heat_d;
+  static bool attr_set = false;
+  if (!attr_set) {
+    GLR_CUDA(cudaFuncSetAttribute(heat_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  heat::SMEM_BYTES));
+    attr_set = true;
+  }
+  int64_t grid = (int64_t)g.oh * hp.m_tiles_per_row * hp.n_tiles;
+  GLR_REQUIRE(grid < (1ll << 31), GLR_ERR_UNSUPPORTED, "heat_map: grid too large");
+  heat_gemm_kernel<<<(unsigned)grid, 128, heat::SMEM_BYTES, st>>>(tmA, tmB, hp);
+  GLR_CUDA(cudaGetLastError());
+  return GLR_OK;
+}

@@ -1,0 +1,231 @@
+"""Generate golden fixtures by running the REFERENCE package itself.
+
+Run in the build container (the reference lives at /root/reference and does
+not exist on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Writes small .npz files next to this script. Every array is produced by the
+reference's own public functions (glr.*), so the oracle (oracle/glr_oracle.py)
+and the CUDA path are pinned to the reference, not to each other.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF_SRC = os.environ.get("GLR_REFERENCE_SRC", "/root/reference/pkg/src")
+sys.path.insert(0, REF_SRC)
+
+import glr  # noqa: E402  (the reference)
+import glr.solvers as ref_solvers  # noqa: E402
+from glr.edges import EdgeMaps, ExemplarSet  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+
+def f32(a):
+    """Inputs are rounded once to fp32 and fed as float64 to both sides."""
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def blob_texture(rng, h, w, c):
+    yy, xx = np.mgrid[0:h, 0:w]
+    base = np.zeros((h, w))
+    for _ in range(6):
+        cy, cx = rng.uniform(0, h), rng.uniform(0, w)
+        sy, sx = rng.uniform(2, h / 4), rng.uniform(2, w / 4)
+        base += rng.uniform(0.2, 1.0) * np.exp(-((yy - cy) / sy) ** 2 - ((xx - cx) / sx) ** 2)
+    tex = rng.random((8, 8))
+    base += 0.3 * np.tile(tex, (h // 8 + 1, w // 8 + 1))[:h, :w]
+    x = np.stack([np.roll(base, k, axis=1) for k in range(c)], axis=2)
+    x = (x - x.min()) / (x.max() - x.min())
+    return f32(x)
+
+
+def random_maps(rng, h, w, c, density):
+    m = lambda: (rng.random((h, w, c)) < density).astype(np.float64)  # noqa: E731
+    hp, vp = m(), m()
+    return EdgeMaps(h_pos=hp, h_neg=m() * (1 - hp), v_pos=vp, v_neg=m() * (1 - vp))
+
+
+def gen_edges():
+    rng = np.random.default_rng(101)
+    cases = {}
+    shapes = [(24, 31, 1), (32, 32, 3), (40, 36, 8), (29, 27, 9), (48, 40, 16), (20, 22, 24)]
+    for i, (h, w, c) in enumerate(shapes):
+        x = blob_texture(rng, h, w, c) if i % 2 == 0 else f32(rng.random((h, w, c)))
+        gh, gv = glr.sobel_gradients(x)
+        em = glr.binarize_gradients(gh, gv, 0.2)
+        maps = np.stack([m.astype(np.uint8) for m in em.as_tuple()])
+        from glr.edges import _shi_tomasi_response
+        mag = np.sqrt(gh ** 2 + gv ** 2).mean(axis=2)
+        resp = _shi_tomasi_response(mag)
+        corners = glr.detect_corners(x, max_n=40, nms_radius=3)
+        ex = glr.select_exemplars(corners, (h, w), 6, uniform_interval=7)
+        cases.update({
+            f"x{i}": x, f"gh{i}": gh, f"gv{i}": gv, f"maps{i}": maps, f"resp{i}": resp,
+            f"corners{i}": np.array(corners, dtype=np.int32).reshape(-1, 2),
+            f"anchors{i}": np.array(ex.anchors, dtype=np.int32).reshape(-1, 2),
+            f"tags{i}": np.array([t == "uniform" for t in ex.tags], dtype=np.uint8),
+        })
+    cases["n"] = np.array(len(shapes))
+    np.savez_compressed(OUT / "edges.npz", **cases)
+
+
+def gen_heat_topk():
+    """similarity_heatmap + global_match on random edge maps (acceptance #1
+    style) and blob images; positions and padding from the reference."""
+    rng = np.random.default_rng(202)
+    cases = {}
+    specs = [(20, 18, 2, 6, 3, 5, None), (33, 41, 1, 8, 6, 16, None), (28, 30, 3, 4, 5, 9, 1),
+             (45, 40, 4, 8, 7, 24, None), (16, 16, 1, 8, 3, 40, None), (12, 11, 2, 3, 4, 30, 1)]
+    for i, (h, w, c, p, n, k, sep) in enumerate(specs):
+        edge = random_maps(rng, h, w, c, float(rng.uniform(0.1, 0.5)))
+        anchors = [(int(rng.integers(0, h - p + 1)), int(rng.integers(0, w - p + 1)))
+                   for _ in range(n)]
+        ex = ExemplarSet(anchors=anchors, tags=["corner"] * n, patch_size=p)
+        hm = glr.matching.similarity_heatmap(edge, ex)
+        cfg = glr.MatchConfig(patch_size=p, group_size=k, min_separation=sep)
+        x = f32(rng.random((h, w, c)))
+        groups = glr.global_match(x, ex, cfg, edge)
+        cases.update({
+            f"maps{i}": np.stack([m.astype(np.uint8) for m in edge.as_tuple()]),
+            f"anchors{i}": np.array(anchors, dtype=np.int32),
+            f"heat{i}": hm.values.astype(np.int32),
+            f"x{i}": x,
+            f"positions{i}": np.array([g.positions for g in groups], dtype=np.int32),
+            f"padded{i}": np.array([g.padded for g in groups], dtype=np.int32),
+            f"matrix{i}": np.stack([g.matrix for g in groups]),
+            f"meta{i}": np.array([h, w, c, p, n, k, cfg.sep]),
+        })
+    cases["n"] = np.array(len(specs))
+    np.savez_compressed(OUT / "heat_topk.npz", **cases)
+
+
+def gen_topk_slices():
+    """top_k_positions on random integer slices (test_matching.py:134-143 style)."""
+    rng = np.random.default_rng(303)
+    cases = {}
+    n = 60
+    for i in range(n):
+        oh, ow = int(rng.integers(2, 40)), int(rng.integers(2, 40))
+        s = rng.integers(0, int(rng.choice([2, 6, 50])), size=(oh, ow)).astype(np.float64)
+        anchor = (int(rng.integers(0, oh)), int(rng.integers(0, ow)))
+        k = int(rng.integers(1, 40))
+        sep = int(rng.integers(0, 4))
+        pos, pad = glr.matching.top_k_positions(s, anchor, k, sep)
+        cases.update({f"s{i}": s, f"meta{i}": np.array([anchor[0], anchor[1], k, sep, pad]),
+                      f"pos{i}": np.array(pos, dtype=np.int32)})
+    cases["n"] = np.array(n)
+    np.savez_compressed(OUT / "topk_slices.npz", **cases)
+
+
+def gen_wnnm():
+    rng = np.random.default_rng(404)
+    cases = {}
+    shapes = [(64, 64), (128, 48), (12, 8), (5, 20), (64, 10), (512, 64), (2, 2), (33, 17)]
+    for i, (m, k) in enumerate(shapes):
+        a = rng.standard_normal((m, k)) if i % 2 else f32(rng.random((m, k)))
+        sigma = float(rng.uniform(0.01, 0.5))
+        out = glr.wnnm_prox(a, glr.WnnmParams(noise_sigma=sigma))
+        uw = glr.wnnm_prox(a, glr.WnnmParams(uniform_weight=0.3))
+        cases.update({f"m{i}": a, f"sigma{i}": np.array(sigma), f"out{i}": out, f"uw{i}": uw})
+    cases["n"] = np.array(len(shapes))
+    # glr_regularize on gathered groups (lowrank.py:68-87)
+    x = blob_texture(rng, 30, 28, 3)
+    pos = [[(int(rng.integers(0, 25)), int(rng.integers(0, 23))) for _ in range(6)]
+           for _ in range(9)]
+    groups = [glr.gather_group(x, q, 4) for q in pos]
+    z = glr.glr_regularize(x, groups, glr.WnnmParams(noise_sigma=0.05))
+    cases.update({"reg_x": x, "reg_pos": np.array(pos, dtype=np.int32), "reg_z": z})
+    np.savez_compressed(OUT / "wnnm.npz", **cases)
+
+
+def gen_operators():
+    rng = np.random.default_rng(505)
+    x8 = f32(rng.random((16, 20, 8)))
+    masks = glr.bernoulli_masks(16, 20, 8, seed=3)
+    cop = glr.cacti_operator(masks)
+    y = cop.forward(x8)
+    mm = glr.msfa_pattern("periodic-4x4", 16, 16, 20)
+    mop = glr.msfa_operator(mm)
+    x16 = f32(rng.random((16, 20, 16)))
+    fmask = glr.radial_mask(16, 16, 5)
+    fop = glr.fourier_operator(fmask)
+    xf = f32(rng.random((16, 16, 1)))
+    yf = fop.forward(xf)
+    np.savez_compressed(
+        OUT / "operators.npz",
+        cacti_x=x8, cacti_masks=masks, cacti_y=y, cacti_adj=cop.adjoint(y), cacti_gram=cop.gram_diag,
+        msfa_x=x16, msfa_masks=mm, msfa_y=mop.forward(x16), msfa_adj=mop.adjoint(mop.forward(x16)),
+        four_x=xf, four_mask=fmask, four_y=yf, four_adj=fop.adjoint(yf),
+        bern_seed7=glr.bernoulli_masks(9, 7, 3, seed=7),
+    )
+
+
+def gen_solves():
+    """Small end-to-end gap_solve runs; the per-refresh anchors/positions are
+    captured by wrapping the reference's own global_match."""
+    rng = np.random.default_rng(606)
+    captured = []
+    orig = ref_solvers.global_match
+
+    def spy(x, exemplars, cfg, edge):
+        groups = orig(x, exemplars, cfg, edge)
+        captured.append((list(exemplars.anchors), [g.positions for g in groups]))
+        return groups
+
+    ref_solvers.global_match = spy
+    try:
+        cases = {}
+        runs = [
+            ("cacti", (32, 32, 4), dict(patch_size=4, group_size=8, max_corners=24,
+                                        exemplar_stride=4), 8),
+            ("msfa", (32, 32, 4), dict(patch_size=4, group_size=8, max_corners=24,
+                                       exemplar_stride=4), 6),
+            ("cacti", (40, 36, 8), dict(patch_size=8, group_size=16, max_corners=30,
+                                        exemplar_stride=6), 6),
+        ]
+        for i, (kind, (h, w, c), mc, iters) in enumerate(runs):
+            scene = blob_texture(rng, h, w, c)
+            if kind == "cacti":
+                masks = glr.bernoulli_masks(h, w, c, seed=10 + i)
+                op = glr.cacti_operator(masks)
+            else:
+                masks = glr.msfa_pattern("bayer-like-2x2", 4, h, w)
+                op = glr.msfa_operator(masks)
+            y = op.forward(scene)
+            cfg = glr.SolverConfig(regularizer="glr", max_iters=iters, match=glr.MatchConfig(**mc))
+            captured.clear()
+            xr, rep = glr.gap_solve(op, y, cfg, ref=scene)
+            cases.update({
+                f"kind{i}": np.array(kind), f"scene{i}": scene, f"masks{i}": masks, f"y{i}": y,
+                f"out{i}": xr, f"resid{i}": np.array([r["residual"] for r in rep.rows]),
+                f"psnr{i}": np.array([r["psnr_db"] for r in rep.rows]),
+                f"mc{i}": np.array([mc["patch_size"], mc["group_size"], mc["max_corners"],
+                                    mc["exemplar_stride"], iters]),
+                f"nref{i}": np.array(len(captured)),
+            })
+            for j, (anc, pos) in enumerate(captured):
+                cases[f"anchors{i}_{j}"] = np.array(anc, dtype=np.int32)
+                cases[f"positions{i}_{j}"] = np.array(pos, dtype=np.int32)
+        cases["n"] = np.array(len(runs))
+        np.savez_compressed(OUT / "solves.npz", **cases)
+    finally:
+        ref_solvers.global_match = orig
+
+
+if __name__ == "__main__":
+    gen_edges()
+    gen_heat_topk()
+    gen_topk_slices()
+    gen_wnnm()
+    gen_operators()
+    gen_solves()
+    for f in sorted(OUT.glob("*.npz")):
+        print(f.name, f.stat().st_size)

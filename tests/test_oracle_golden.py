@@ -1,0 +1,107 @@
+"""Pin the CPU oracle (oracle/glr_oracle.py) to golden vectors produced by
+running the reference itself (tests/golden/make_golden.py)."""
+
+import numpy as np
+import pytest
+
+import glr_oracle as O
+from conftest import load_golden
+
+
+def test_edges_bitwise():
+    g = load_golden("edges")
+    for i in range(int(g["n"])):
+        x = g[f"x{i}"]
+        gh, gv = O.sobel_gradients(x)
+        assert np.array_equal(gh, g[f"gh{i}"]) and np.array_equal(gv, g[f"gv{i}"]), i
+        maps = np.stack(O.binarize_gradients(gh, gv, 0.2))
+        assert np.array_equal(maps, g[f"maps{i}"]), i
+        assert np.array_equal(O.corner_response(x), g[f"resp{i}"]), i
+        corners = O.detect_corners(x, max_n=40, nms_radius=3)
+        assert np.array_equal(np.array(corners, dtype=np.int32).reshape(-1, 2), g[f"corners{i}"])
+        anchors, tags = O.select_exemplars(corners, x.shape[:2], 6, uniform_interval=7)
+        assert np.array_equal(np.array(anchors, dtype=np.int32).reshape(-1, 2), g[f"anchors{i}"])
+        assert np.array_equal(np.array([t == "uniform" for t in tags], dtype=np.uint8),
+                              g[f"tags{i}"])
+
+
+def test_heat_and_topk_bitwise():
+    g = load_golden("heat_topk")
+    for i in range(int(g["n"])):
+        h, w, c, p, n, k, sep = (int(v) for v in g[f"meta{i}"])
+        maps = list(g[f"maps{i}"])
+        anchors = [tuple(a) for a in g[f"anchors{i}"].tolist()]
+        heat = O.similarity_heatmap(maps, anchors, p)
+        assert np.array_equal(heat, g[f"heat{i}"]), i
+        pos, pads = O.match_positions(heat, anchors, k, sep)
+        assert np.array_equal(np.array(pos, dtype=np.int32), g[f"positions{i}"]), i
+        assert np.array_equal(np.array(pads), g[f"padded{i}"]), i
+        for j, q in enumerate(pos):
+            assert np.array_equal(O.gather_group(g[f"x{i}"], q, p), g[f"matrix{i}"][j])
+
+
+def test_topk_slices_bitwise():
+    g = load_golden("topk_slices")
+    for i in range(int(g["n"])):
+        ar, ac, k, sep, pad = (int(v) for v in g[f"meta{i}"])
+        pos, padded = O.top_k_positions(g[f"s{i}"], (ar, ac), k, sep)
+        assert padded == pad, i
+        assert np.array_equal(np.array(pos, dtype=np.int32), g[f"pos{i}"]), i
+
+
+def test_wnnm_and_regularize():
+    g = load_golden("wnnm")
+    for i in range(int(g["n"])):
+        m = g[f"m{i}"]
+        out = O.wnnm_prox(m, float(g[f"sigma{i}"]))
+        np.testing.assert_allclose(out, g[f"out{i}"], atol=1e-12, rtol=0)
+        uw = O.wnnm_prox(m, 0.0, uniform_weight=0.3)
+        np.testing.assert_allclose(uw, g[f"uw{i}"], atol=1e-12, rtol=0)
+    pos = [[tuple(p) for p in grp] for grp in g["reg_pos"].tolist()]
+    z = O.glr_regularize(g["reg_x"], pos, 4, 0.05)
+    np.testing.assert_allclose(z, g["reg_z"], atol=1e-12, rtol=0)
+
+
+def test_operators():
+    g = load_golden("operators")
+    np.testing.assert_array_equal(O.bernoulli_masks(9, 7, 3, seed=7), g["bern_seed7"])
+    op = O.Operator("cacti", masks=g["cacti_masks"])
+    np.testing.assert_allclose(op.forward(g["cacti_x"]), g["cacti_y"], atol=1e-13)
+    np.testing.assert_allclose(op.adjoint(g["cacti_y"]), g["cacti_adj"], atol=1e-13)
+    np.testing.assert_allclose(op.gram, g["cacti_gram"], atol=0)
+    np.testing.assert_array_equal(O.msfa_pattern_periodic(4, 16, 20), g["msfa_masks"])
+    op = O.Operator("msfa", masks=g["msfa_masks"])
+    np.testing.assert_allclose(op.forward(g["msfa_x"]), g["msfa_y"], atol=1e-13)
+    np.testing.assert_allclose(op.adjoint(g["msfa_y"]), g["msfa_adj"], atol=1e-13)
+    op = O.Operator("fourier", mask=g["four_mask"], channels=1)
+    np.testing.assert_allclose(op.forward(g["four_x"]), g["four_y"], atol=1e-13)
+    np.testing.assert_allclose(op.adjoint(g["four_y"]), g["four_adj"], atol=1e-13)
+
+
+def test_complex_fourier_adjoint_identity(rng):
+    mask = (rng.random((16, 12)) < 0.4).astype(float)
+    op = O.Operator("fourier", mask=mask, channels=2)
+    for _ in range(20):
+        x = rng.standard_normal((16, 12, 2))
+        y = rng.standard_normal((16, 12)) + 1j * rng.standard_normal((16, 12))
+        lhs = np.vdot(op.forward(x), y).real
+        rhs = np.vdot(x, op.adjoint(y)).real
+        assert abs(lhs - rhs) <= 1e-12 * max(1.0, abs(lhs))
+
+
+@pytest.mark.parametrize("i", [0, 1, 2])
+def test_gap_solve_matches_reference_run(i):
+    g = load_golden("solves")
+    kind = str(g[f"kind{i}"])
+    p, k, mc, stride, iters = (int(v) for v in g[f"mc{i}"])
+    op = O.Operator(kind, masks=g[f"masks{i}"])
+    trace = []
+    x, res, ps = O.gap_solve(op, g[f"y{i}"], iters, patch_size=p, group_size=k, max_corners=mc,
+                             exemplar_stride=stride, ref=g[f"scene{i}"], trace=trace)
+    assert len(trace) == int(g[f"nref{i}"])
+    for j, (anc, pos) in enumerate(trace):
+        assert np.array_equal(np.array(anc, dtype=np.int32), g[f"anchors{i}_{j}"])
+        assert np.array_equal(np.array(pos, dtype=np.int32), g[f"positions{i}_{j}"])
+    np.testing.assert_allclose(x, g[f"out{i}"], atol=1e-10, rtol=0)
+    np.testing.assert_allclose(res, g[f"resid{i}"], rtol=1e-9)
+    np.testing.assert_allclose(ps, g[f"psnr{i}"], atol=1e-8)

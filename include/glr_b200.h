@@ -99,10 +99,12 @@ int glr_select_anchors(const int32_t* corners_rc_d, const int32_t* n_corners_d, 
 /* ---- (2) global similarity heat map: glr/matching.py:140-167 ---------------
  * heat[n][u*ow+v] = sum_{p,q,ch<4C} E[u+p][v+q][ch] * E[r_n+p][c_n+q][ch],
  * exact integer overlap counts on tcgen05 tensor cores (kind::i8, s32 accum).
- * Exemplar-major u16 output, positions flattened row-major (oh = H-P+1,
- * ow = W-P+1). n_dev_d (optional) caps the exemplar count on device.
+ * Exemplar-major u16 output heat[n*stride + u*ow + v], stride =
+ * glr_heat_stride(H,W,P) (oh = H-P+1, ow = W-P+1). n_dev_d (optional) caps the exemplar count on device.
  * ws: glr_heat_workspace (the packed exemplar operand).                     */
 int glr_heat_expand_factor(int C, int P);
+/* Row stride (entries) of the heat map: (H-P+1)*(W-P+1) rounded up to 8.  */
+int64_t glr_heat_stride(int H, int W, int P);
 size_t glr_heat_workspace(int C, int P, int n_max);
 int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, int expand,
                  const int32_t* anchors_d, int n_max, const int32_t* n_dev_d, uint16_t* heat_d,
@@ -154,6 +156,11 @@ int glr_scatter_count(const int32_t* positions_d, int n_max, const int32_t* n_de
 int glr_scatter_add_f64(const double* groups_d, const int32_t* positions_d, int G, int K, int P,
                         int H, int W, int C, double* acc_d, double* cnt_d, void* stream);
 
+/* glr_scatter_fixed: fixed-point scatter-add of explicit fp64 groups (G,K,m)
+ * into acc_d (the glr_regularize(x, groups, params) entry, lowrank.py:80-83). */
+int glr_scatter_fixed(const double* groups_d, const int32_t* positions_d, int G, int K, int P,
+                      int H, int W, int C, int frac_bits, int64_t* acc_d, void* stream);
+
 /* glr_normalize: z = acc/cnt where cnt > 0 else x (lowrank.py:84-87).       */
 int glr_normalize(const int64_t* acc_d, const int32_t* cnt_d, const double* x_d, int H, int W,
                   int C, int frac_bits, double* z_d, void* stream);
@@ -190,7 +197,7 @@ int glr_gap_fourier(const int64_t* acc_d, const int32_t* cnt_d, int frac_bits,
                     void* ws_d, void* stream);
 
 /* Squared-error sum vs a reference for PSNR (metrics.py:26-37), of
- * clip(x, 0, peak), deterministic. out_d: 1 double.                         */
+ * clip(x, 0, peak) (no clip when peak <= 0), deterministic. out_d: 1 double. */
 int glr_sq_err(const double* x_d, const double* ref_d, int n, double peak, double* out_d,
                void* ws_d, void* stream);
 

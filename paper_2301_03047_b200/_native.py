@@ -62,6 +62,8 @@ SIGNATURES: dict[str, tuple] = {
                                vp, sz, vp]),
     "glr_scatter_count": (i32, [vp, i32, vp, i32, i32, i32, i32, vp, vp]),
     "glr_scatter_add_f64": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, vp, vp, vp]),
+    "glr_scatter_fixed": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, vp]),
+    "glr_heat_stride": (i64, [i32, i32, i32]),
     "glr_normalize": (i32, [vp, vp, vp, i32, i32, i32, i32, vp, vp]),
     "glr_masksum_forward": (i32, [vp, vp, i32, i32, i32, vp, vp]),
     "glr_masksum_adjoint": (i32, [vp, vp, i32, i32, i32, vp, vp]),

@@ -35,6 +35,32 @@ constexpr int kNumSMs = 148;
 
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Block-wide exclusive scan of one int per thread (blockDim a multiple of 32,
+// <= 1024). warp_tot: 32 ints of shared scratch. Returns the exclusive prefix;
+// *total (shared) receives the block sum. Contains __syncthreads().
+__device__ __forceinline__ int block_excl_scan_1024(int v, int* warp_tot, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = (lane < (int)(blockDim.x >> 5)) ? warp_tot[lane] : 0;
+    int s = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    warp_tot[lane] = s - w;
+    if (lane == 31) *total = s;
+  }
+  __syncthreads();
+  return warp_tot[warp] + x - v;
+}
+
 // ---------------------------------------------------------------------------
 // PTX wrappers (sm_100a)
 

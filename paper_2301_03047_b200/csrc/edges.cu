@@ -332,30 +332,6 @@ __global__ void cand_keys_kernel(const double* __restrict__ resp, int64_t n, dou
   }
 }
 
-__device__ __forceinline__ int block_excl_scan_1024(int v, int* warp_tot, int* total) {
-  // 1024-thread exclusive scan of per-thread counts
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int x = v;
-  for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) warp_tot[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    int w = (lane < (int)(blockDim.x >> 5)) ? warp_tot[lane] : 0;
-    int s = w;
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += y;
-    }
-    warp_tot[lane] = s - w;
-    if (lane == 31) *total = s;
-  }
-  __syncthreads();
-  return warp_tot[warp] + x - v;
-}
-
 __global__ void __launch_bounds__(1024) nms_kernel(const uint64_t* __restrict__ keys,
                                                    const int32_t* __restrict__ idx, int64_t total,
                                                    int H, int W, int max_n, int R,

@@ -18,7 +18,8 @@
 //   * u8 x u8 -> s32 on tcgen05.mma kind::i8 is exact for every count
 //     (max 4*C*P^2); the accumulator lives in TMEM (128 lanes x 256 cols).
 //   * Output: exemplar-major u16 heat[n][u*ow+v] (flat index = the
-//     reference's row-major slice index, matching.py:177-178).
+//     reference's row-major slice index, matching.py:177-178), rows padded
+//     to a multiple of 8 entries (glr_heat_stride) for 16-byte loads.
 //
 // Warp roles (128 threads): warp0.lane0 = TMA producer, warp1.lane0 = MMA
 // issuer, warp1 owns the TMEM allocation, all four warps run the epilogue.
@@ -64,7 +65,7 @@ static HeatGeom heat_geom(int H, int W, int C, int P, int e) {
 }
 
 struct HeatParams {
-  int oh, ow, M, n_max, n_tiles, m_tiles_per_row, S, kchunks, e;
+  int oh, ow, Mpad, n_max, n_tiles, m_tiles_per_row, S, kchunks, e;
   const int32_t* n_dev;
   uint16_t* heat;
 };
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int n = nb + j;
-      if (v_ok && n < N) out[(size_t)n * p.M] = (uint16_t)r[j];
+      if (v_ok && n < N) out[(size_t)n * p.Mpad] = (uint16_t)r[j];
     }
   }
   tc_fence_before();
@@ -232,6 +233,10 @@ extern "C" int glr_heat_expand_factor(int C, int P) {
   return best_e;
 }
 
+extern "C" int64_t glr_heat_stride(int H, int W, int P) {
+  return cdiv((int64_t)(H - P + 1) * (W - P + 1), 8) * 8;
+}
+
 extern "C" size_t glr_heat_workspace(int C, int P, int n_max) {
   int e = glr_heat_expand_factor(C, P);
   if (e < 1) return 0;
@@ -293,7 +298,7 @@ extern "C" int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, 
   HeatParams hp;
   hp.oh = g.oh;
   hp.ow = g.ow;
-  hp.M = g.oh * g.ow;
+  hp.Mpad = (int)glr_heat_stride(H, W, P);
   hp.n_max = n_max;
   hp.n_tiles = n_pad / heat::BN;
   hp.m_tiles_per_row = (int)cdiv(g.ow, heat::BM);

@@ -1,0 +1,215 @@
+// (6) Sensing operators and the fused GAP projection.
+//
+// Reference: glr/operators.py (CACTI :35-59, masked Fourier :65-89, MSFA
+// :160-185) and glr/solvers.py:284-308 (gap_solve projection
+// x = clip(z + A^T(safe_div(y - A z, gram)), -p/2, 3p/2), residual
+// ||y - A x||, _safe_div :220-226).
+//
+// The mask-sum family (CACTI and MSFA share A x = sum_t M_t x_t) is one
+// pixel-local kernel that fuses: count-normalisation of the aggregated
+// numerator (lowrank.py:84-87), the projection, the clip, and a
+// deterministic per-block partial of the squared residual of the NEW
+// iterate. Channel sums use numpy's pairwise order (operators.py:39 sums
+// over axis 2) so A x matches the reference to the last bit for T <= 128.
+//
+// The Fourier family uses a hand-written fp64 complex FFT (fft.cu).
+#include "common.cuh"
+#include "fft.cuh"
+
+namespace glr {
+
+namespace gap {
+constexpr int THREADS = 256;
+constexpr int TMAX = 128;
+}  // namespace gap
+
+// numpy pairwise sum over a small register/local array
+__device__ __forceinline__ double pw_sum(const double* a, int n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+  return res;
+}
+
+__global__ void masksum_forward_kernel(const double* __restrict__ x, const double* __restrict__ mk,
+                                       int64_t npix, int T, double* __restrict__ y) {
+  double prod[gap::TMAX];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npix;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    for (int t = 0; t < T; ++t) prod[t] = __dmul_rn(mk[i * T + t], x[i * T + t]);
+    y[i] = pw_sum(prod, T);
+  }
+}
+
+__global__ void masksum_adjoint_kernel(const double* __restrict__ y, const double* __restrict__ mk,
+                                       int64_t npix, int T, double* __restrict__ x) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npix * T;
+       i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = __dmul_rn(mk[i], y[i / T]);
+}
+
+// deterministic block partial sums -> out[blockIdx.x]
+__device__ __forceinline__ void block_sum_store(double v, double* out) {
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s = __dadd_rn(s, red[w]);
+    out[blockIdx.x] = s;
+  }
+}
+
+__global__ void final_sum_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+  __shared__ double red[32];
+  double v = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) v = __dadd_rn(v, part[i]);
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s = __dadd_rn(s, red[w]);
+    *out = s;
+  }
+}
+
+struct GapArgs {
+  const int64_t* acc;
+  const int32_t* cnt;
+  double inv_scale;
+  const double* x_in;
+  const double* mk;
+  const double* y;
+  const double* gram;
+  int64_t npix;
+  int T;
+  double lo, hi;
+  double* x_out;
+  double* part;
+};
+
+__global__ void __launch_bounds__(gap::THREADS) gap_masksum_kernel(GapArgs a) {
+  double z[gap::TMAX], prod[gap::TMAX];
+  double acc_sq = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.npix;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int T = a.T;
+    const int n = a.cnt ? a.cnt[i] : 0;
+    for (int t = 0; t < T; ++t) {
+      const int64_t k = i * T + t;
+      z[t] = n > 0 ? ((double)a.acc[k] * a.inv_scale) / (double)n : a.x_in[k];
+    }
+    double gram;
+    if (a.gram) {
+      gram = a.gram[i];
+    } else {
+      for (int t = 0; t < T; ++t) {
+        const double m = a.mk[i * T + t];
+        prod[t] = __dmul_rn(m, m);
+      }
+      gram = pw_sum(prod, T);
+    }
+    for (int t = 0; t < T; ++t) prod[t] = __dmul_rn(a.mk[i * T + t], z[t]);
+    const double az = pw_sum(prod, T);
+    const double yi = a.y[i];
+    const double r = gram != 0.0 ? __ddiv_rn(__dsub_rn(yi, az), gram) : 0.0;
+    for (int t = 0; t < T; ++t) {
+      const double m = a.mk[i * T + t];
+      double v = __dadd_rn(z[t], __dmul_rn(m, r));
+      v = fmin(fmax(v, a.lo), a.hi);
+      z[t] = v;
+      a.x_out[i * T + t] = v;
+      prod[t] = __dmul_rn(m, v);
+    }
+    const double d = __dsub_rn(yi, pw_sum(prod, T));
+    acc_sq = fma(d, d, acc_sq);
+  }
+  block_sum_store(acc_sq, a.part);
+}
+
+__global__ void sq_err_kernel(const double* __restrict__ x, const double* __restrict__ ref,
+                              int64_t n, double peak, double* __restrict__ part) {
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = peak > 0.0 ? fmin(fmax(x[i], 0.0), peak) : x[i];
+    const double d = ref[i] - v;
+    s = fma(d, d, s);
+  }
+  block_sum_store(s, part);
+}
+
+constexpr int kGapBlocks = 2 * kNumSMs;
+
+}  // namespace glr
+
+using namespace glr;
+
+extern "C" int glr_masksum_forward(const double* x_d, const double* masks_d, int H, int W, int T,
+                                   double* y_d, void* stream) {
+  GLR_REQUIRE(T >= 1 && T <= gap::TMAX, GLR_ERR_UNSUPPORTED, "masksum: T=%d", T);
+  const int64_t npix = (int64_t)H * W;
+  masksum_forward_kernel<<<kGapBlocks, gap::THREADS, 0, (cudaStream_t)stream>>>(x_d, masks_d,
+                                                                               npix, T, y_d);
+  return check_launch("masksum_forward_kernel");
+}
+
+extern "C" int glr_masksum_adjoint(const double* y_d, const double* masks_d, int H, int W, int T,
+                                   double* x_d, void* stream) {
+  const int64_t npix = (int64_t)H * W;
+  masksum_adjoint_kernel<<<kGapBlocks * 4, gap::THREADS, 0, (cudaStream_t)stream>>>(
+      y_d, masks_d, npix, T, x_d);
+  return check_launch("masksum_adjoint_kernel");
+}
+
+extern "C" size_t glr_gap_workspace(int H, int W) { return (kGapBlocks + 8) * sizeof(double); }
+
+extern "C" int glr_gap_masksum(const int64_t* acc_d, const int32_t* cnt_d, int frac_bits,
+                               const double* x_in_d, const double* masks_d, const double* y_d,
+                               const double* gram_d, int H, int W, int T, double lo, double hi,
+                               double* x_out_d, double* resid_d, void* ws_d, void* stream) {
+  GLR_REQUIRE(T >= 1 && T <= gap::TMAX, GLR_ERR_UNSUPPORTED, "gap_masksum: T=%d", T);
+  cudaStream_t st = (cudaStream_t)stream;
+  GapArgs a;
+  a.acc = acc_d;
+  a.cnt = acc_d ? cnt_d : nullptr;
+  a.inv_scale = ldexp(1.0, -frac_bits);
+  a.x_in = x_in_d;
+  a.mk = masks_d;
+  a.y = y_d;
+  a.gram = gram_d;
+  a.npix = (int64_t)H * W;
+  a.T = T;
+  a.lo = lo;
+  a.hi = hi;
+  a.x_out = x_out_d;
+  a.part = reinterpret_cast<double*>(ws_d);
+  gap_masksum_kernel<<<kGapBlocks, gap::THREADS, 0, st>>>(a);
+  GLR_CUDA(cudaGetLastError());
+  final_sum_kernel<<<1, 256, 0, st>>>(a.part, kGapBlocks, resid_d);
+  return check_launch("final_sum_kernel");
+}
+
+extern "C" int glr_sq_err(const double* x_d, const double* ref_d, int n, double peak,
+                          double* out_d, void* ws_d, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  double* part = reinterpret_cast<double*>(ws_d);
+  sq_err_kernel<<<kGapBlocks, 256, 0, st>>>(x_d, ref_d, n, peak, part);
+  GLR_CUDA(cudaGetLastError());
+  final_sum_kernel<<<1, 256, 0, st>>>(part, kGapBlocks, out_d);
+  return check_launch("sq_err");
+}

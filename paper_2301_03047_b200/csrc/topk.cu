@@ -1,0 +1,302 @@
+// (3) Exact tie-ordered top-K selection per exemplar + patch gather.
+//
+// Reference: glr/matching.py:170-231 (top_k_positions) and :240-252
+// (global_match loop), glr/patches.py:43-54 (gather_group).
+//
+// Semantics reproduced exactly (integer decisions, no tolerance):
+//   slot 0 = the exemplar's anchor; remaining slots walk positions in
+//   (score desc, flat row-major index asc) order, skipping any position within
+//   Chebyshev distance <= sep of an already-chosen one; if the walk runs out,
+//   a second walk with sep = 0; missing slots repeat the anchor ("padded").
+//
+// One CTA per exemplar over its u16 heat-map row:
+//   1. shared-memory histogram of the integer scores;
+//   2. the cut T = largest score with count(>= T) >= need, need = min(pool, M)
+//      where pool = K(2 sep + 1)^2 + 1 (the reference's bound: the first pool
+//      entries of the ordered walk always fill the group, matching.py:219-225);
+//   3. one ordered pass compacting A = {score > T} (all, < need entries) and
+//      the first need-|A| entries of B = {score == T} in index order — this
+//      is exactly the first `need` entries of the reference's ordered walk;
+//   4. bitonic sort of A by (score desc, index asc) in shared memory;
+//   5. one warp runs the greedy walk, 32 candidates per step: lanes test
+//      their candidate against the chosen set in parallel, then accepted
+//      candidates are committed in lane order with an in-warp re-check.
+#include "common.cuh"
+
+namespace glr {
+
+namespace topk {
+constexpr int THREADS = 512;
+constexpr int VEC = 8;  // u16 scores per 16-byte load
+constexpr int MAX_BINS = 12288;
+}  // namespace topk
+
+struct TopkParams {
+  const uint16_t* heat;
+  int64_t stride;  // heat row stride (entries)
+  int n_max;
+  const int32_t* n_dev;
+  int oh, ow;
+  int64_t M;
+  int bins;  // max_score + 1
+  const int32_t* anchors;
+  int K, sep, pool, a_cap;  // a_cap: power of two >= pool
+  int32_t* positions;
+  int32_t* padded;
+};
+
+__device__ __forceinline__ int cheb(int r0, int c0, int r1, int c1) {
+  return max(abs(r0 - r1), abs(c0 - c1));
+}
+
+__global__ void __launch_bounds__(topk::THREADS) topk_kernel(TopkParams p) {
+  using namespace topk;
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* sA = reinterpret_cast<uint64_t*>(smem);                   // a_cap
+  int32_t* sB = reinterpret_cast<int32_t*>(sA + p.a_cap);              // pool
+  int32_t* hist = sB + p.pool;                                         // bins
+  int32_t* chosen = hist + p.bins;                                     // 2*K
+  __shared__ int warp_tot[32];
+  __shared__ int s_total, s_T, s_cntA, s_baseA, s_baseB;
+
+  const int n = blockIdx.x;
+  const int N = p.n_dev ? min(*p.n_dev, p.n_max) : p.n_max;
+  if (n >= N) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint16_t* row = p.heat + (size_t)n * p.stride;
+  const int64_t M = p.M;
+  const int need = (int)(M < (int64_t)p.pool ? M : (int64_t)p.pool);
+
+  // 1. histogram
+  for (int b = tid; b < p.bins; b += THREADS) hist[b] = 0;
+  __syncthreads();
+  for (int64_t base = (int64_t)tid * VEC; base < M; base += (int64_t)THREADS * VEC) {
+    const uint4 v = *reinterpret_cast<const uint4*>(row + base);
+    const uint16_t* s = reinterpret_cast<const uint16_t*>(&v);
+#pragma unroll
+    for (int j = 0; j < VEC; ++j)
+      if (base + j < M) atomicAdd(&hist[min((int)s[j], p.bins - 1)], 1);
+  }
+  __syncthreads();
+
+  // 2. cut score T: walk bins from the top, 32 at a time
+  if (warp == 0) {
+    int running = 0;
+    int T = 0, cntA = 0;
+    bool found = false;
+    for (int top = p.bins - 1; top >= 0 && !found; top -= 32) {
+      const int b = top - lane;
+      const int c = b >= 0 ? hist[b] : 0;
+      int incl = c;  // inclusive prefix from the top (lane 0 = highest bin)
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const unsigned hit = __ballot_sync(0xffffffffu, b >= 0 && running + incl >= need);
+      if (hit) {
+        const int l = __ffs(hit) - 1;
+        T = top - l;
+        cntA = running + __shfl_sync(0xffffffffu, incl - c, l);
+        found = true;
+      }
+      running += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) {
+      s_T = T;
+      s_cntA = cntA;
+      s_baseA = 0;
+      s_baseB = 0;
+    }
+  }
+  __syncthreads();
+  const int T = s_T, cntA = s_cntA, capB = need - cntA;
+
+  // 3. ordered compaction of A (score > T) and the first capB of B (score == T)
+  for (int64_t tile = 0; tile < M; tile += (int64_t)THREADS * VEC) {
+    if (s_baseA >= cntA && s_baseB >= capB) break;  // block-uniform
+    const int64_t base = tile + (int64_t)tid * VEC;
+    uint16_t s[VEC];
+    int a = 0, b = 0;
+    if (base < M) {
+      const uint4 v = *reinterpret_cast<const uint4*>(row + base);
+      const uint16_t* sv = reinterpret_cast<const uint16_t*>(&v);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        s[j] = (base + j < M) ? sv[j] : 0;
+        const bool valid = base + j < M;
+        a += valid && s[j] > T;
+        b += valid && s[j] == T;
+      }
+    }
+    const int pre = block_excl_scan_1024(a | (b << 16), warp_tot, &s_total);
+    int ia = s_baseA + (pre & 0xFFFF);
+    int ib = s_baseB + (pre >> 16);
+    if (a | b) {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        if (base + j >= M) break;
+        if (s[j] > T) {
+          sA[ia++] = ((uint64_t)(65535 - s[j]) << 32) | (uint32_t)(base + j);
+        } else if (s[j] == T) {
+          if (ib < capB) sB[ib] = (int32_t)(base + j);
+          ++ib;
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      s_baseA += s_total & 0xFFFF;
+      s_baseB += s_total >> 16;
+    }
+    __syncthreads();
+  }
+
+  // 4. bitonic sort of A (padded to the next power of two >= cntA)
+  int sz = 1;
+  while (sz < cntA) sz <<= 1;
+  for (int i = cntA + tid; i < sz; i += THREADS) sA[i] = ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= sz; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < sz; i += THREADS) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const uint64_t x = sA[i], y = sA[ixj];
+          const bool up = (i & k) == 0;
+          if ((x > y) == up) {
+            sA[i] = y;
+            sA[ixj] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // 5. greedy walk (warp 0)
+  if (warp == 0) {
+    const int ar = p.anchors[2 * n], ac = p.anchors[2 * n + 1];
+    if (lane == 0) {
+      chosen[0] = ar;
+      chosen[1] = ac;
+    }
+    __syncwarp();
+    int nch = 1;
+    const int L = need;
+    const bool full_walk = (int64_t)need == M;  // the list is the whole ordered slice
+    for (int pass = 0; pass < (full_walk ? 2 : 1) && nch < p.K; ++pass) {
+      const int sep = pass == 0 ? p.sep : 0;
+      for (int base = 0; base < L && nch < p.K; base += 32) {
+        const int j = base + lane;
+        int idx = -1;
+        if (j < L) idx = j < cntA ? (int)(uint32_t)(sA[j] & 0xFFFFFFFFull) : sB[j - cntA];
+        const int r = idx >= 0 ? idx / p.ow : 0;
+        const int c = idx >= 0 ? idx - r * p.ow : 0;
+        bool blocked = idx < 0;
+        for (int t = 0; t < nch && !blocked; ++t)
+          if (cheb(r, c, chosen[2 * t], chosen[2 * t + 1]) <= sep) blocked = true;
+        unsigned mask = __ballot_sync(0xffffffffu, !blocked);
+        while (mask && nch < p.K) {
+          const int l0 = __ffs(mask) - 1;
+          const int pr = __shfl_sync(0xffffffffu, r, l0);
+          const int pc = __shfl_sync(0xffffffffu, c, l0);
+          if (lane == 0) {
+            chosen[2 * nch] = pr;
+            chosen[2 * nch + 1] = pc;
+          }
+          ++nch;
+          if (lane <= l0 || cheb(r, c, pr, pc) <= sep) blocked = true;
+          mask = __ballot_sync(0xffffffffu, !blocked);
+        }
+        __syncwarp();
+      }
+    }
+    __syncwarp();
+    int32_t* out = p.positions + (size_t)n * p.K * 2;
+    for (int t = lane; t < p.K; t += 32) {
+      out[2 * t] = t < nch ? chosen[2 * t] : ar;
+      out[2 * t + 1] = t < nch ? chosen[2 * t + 1] : ac;
+    }
+    if (lane == 0) p.padded[n] = p.K - nch;
+  }
+}
+
+// gather_group (patches.py:43-54): groups[g][j][i], i = (dr*P + dc)*C + ch
+__global__ void gather_kernel(const double* __restrict__ x, int H, int W, int C, int P,
+                              const int32_t* __restrict__ pos, int G, int K,
+                              double* __restrict__ groups) {
+  const int m = P * P * C;
+  const int64_t total = (int64_t)G * K * m;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t col = i / m;
+    const int e = (int)(i - col * m);
+    const int r = pos[2 * col] + e / (P * C);
+    const int c = pos[2 * col + 1] + (e / C) % P;
+    groups[i] = x[((int64_t)r * W + c) * C + (e % C)];
+  }
+}
+
+static int topk_pool(int K, int sep) { return K * (2 * sep + 1) * (2 * sep + 1) + 1; }
+
+static size_t topk_smem(int pool, int bins, int K) {
+  int a_cap = 1;
+  while (a_cap < pool) a_cap <<= 1;
+  return (size_t)a_cap * 8 + (size_t)pool * 4 + (size_t)bins * 4 + (size_t)K * 8 + 16;
+}
+
+}  // namespace glr
+
+using namespace glr;
+
+extern "C" size_t glr_topk_workspace(int n_max, int K, int sep) { return 0; }
+
+extern "C" int glr_topk(const uint16_t* heat_d, int n_max, const int32_t* n_dev_d, int oh, int ow,
+                        int max_score, const int32_t* anchors_d, int K, int sep,
+                        int32_t* positions_d, int32_t* padded_d, void* ws_d, size_t ws_bytes,
+                        void* stream) {
+  GLR_REQUIRE(K >= 1, GLR_ERR_INVALID, "group_size must be >= 1");
+  GLR_REQUIRE(sep >= 0, GLR_ERR_INVALID, "min_separation must be >= 0");
+  GLR_REQUIRE(oh >= 1 && ow >= 1, GLR_ERR_INVALID, "topk: empty slice");
+  GLR_REQUIRE(max_score >= 0 && max_score < topk::MAX_BINS, GLR_ERR_UNSUPPORTED,
+              "topk: max score %d above %d", max_score, topk::MAX_BINS - 1);
+  if (n_max <= 0) return GLR_OK;
+  const int64_t M = (int64_t)oh * ow;
+  const int pool = (int)std::min<int64_t>(topk_pool(K, sep), M);
+  const int bins = max_score + 1;
+  const size_t smem = topk_smem(pool, bins, K);
+  GLR_REQUIRE(smem <= 200 * 1024, GLR_ERR_UNSUPPORTED,
+              "topk: K=%d sep=%d needs %zu bytes of shared memory", K, sep, smem);
+  TopkParams p;
+  p.heat = heat_d;
+  p.stride = cdiv(M, 8) * 8;
+  p.n_max = n_max;
+  p.n_dev = n_dev_d;
+  p.oh = oh;
+  p.ow = ow;
+  p.M = M;
+  p.bins = bins;
+  p.anchors = anchors_d;
+  p.K = K;
+  p.sep = sep;
+  p.pool = pool;
+  p.a_cap = 1;
+  while (p.a_cap < pool) p.a_cap <<= 1;
+  p.positions = positions_d;
+  p.padded = padded_d;
+  GLR_CUDA(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  topk_kernel<<<n_max, topk::THREADS, smem, (cudaStream_t)stream>>>(p);
+  return check_launch("topk_kernel");
+}
+
+extern "C" int glr_gather(const double* x_d, int H, int W, int C, int P, const int32_t* positions_d,
+                          int G, int K, double* groups_d, void* stream) {
+  GLR_REQUIRE(P >= 1 && P <= H && P <= W, GLR_ERR_INVALID, "gather: bad patch size");
+  int64_t total = (int64_t)G * K * P * P * C;
+  if (total == 0) return GLR_OK;
+  int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 32);
+  gather_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(x_d, H, W, C, P, positions_d, G, K,
+                                                         groups_d);
+  return check_launch("gather_kernel");
+}

@@ -1,0 +1,241 @@
+"""Device-resident GLR iteration engine behind gap_solve / regularize_dispatch.
+
+Everything the reference's hot loop touches (glr/solvers.py:170-308) stays
+on the GPU between iterations: the iterate x (fp64, (H, W, C)), the
+measurement, the masks, the edge stack, the heat map, the match positions,
+the int64 fixed-point aggregation numerator and the int32 counter. One
+iteration is a fixed sequence of libglr_b200 launches on one stream:
+
+  refresh (every match_refresh_interval iterations, solvers.py:185-203)
+      corner response -> NMS corners -> anchors (+ uniform grid)
+      Sobel -> sign-split edge stack
+      heat map (tcgen05) -> exact top-K positions       [per exemplar shard]
+      counter of covered pixels                         [+ all-reduce]
+  every iteration (solvers.py:204-210, 298-301)
+      fused gather + WNNM + fixed-point scatter          [per exemplar shard]
+      all-reduce of the numerator (multi-GPU only)
+      fused normalise + GAP projection + clip + residual
+
+Exemplars shard across ranks as contiguous anchor blocks; the
+integer all-reduce makes every rank count bitwise identical.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _device as D
+from . import _native as N
+from .lowrank import KMAX, frac_bits_for
+
+
+def shard_bounds(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous anchor block [lo, hi) of ``rank`` out of ``world``."""
+    return (n * rank) // world, (n * (rank + 1)) // world
+
+
+class DeviceOperator:
+    """Device copy of a SensingOperator, rebuilt from kind + meta
+    (operators.py plug point; the Python lambdas are never called)."""
+
+    def __init__(self, op, clip_policy: bool | None = None):
+        t = D.torch()
+        self.kind = op.kind
+        h, w, c = op.x_shape
+        self.shape = (h, w, c)
+        if op.kind in ("cacti", "msfa"):
+            masks = np.asarray(op.meta["masks"], dtype=np.float64)
+            self.masks = D.f64(masks)
+            gram = np.asarray(op.gram_diag, dtype=np.float64).reshape(h, w)
+            self.gram = D.f64(gram)
+            self.y_shape = (h, w, 1)
+        elif op.kind == "fourier":
+            self.mask = D.f64(np.asarray(op.meta["mask"], dtype=np.float64))
+            self.y_shape = (h, w)
+            self.fft_ws = D.empty((N.query("glr_fft_workspace", h, w),), t.uint8)
+        else:
+            raise ValueError(f"unsupported operator kind {op.kind!r}")
+        # complex (re, im) images are not clipped
+        self.clip = (c != 2) if clip_policy is None else bool(clip_policy)
+
+    def upload_y(self, y: np.ndarray):
+        y = np.asarray(y)
+        if self.kind == "fourier":
+            yc = np.stack([y.real, y.imag], axis=2) if np.iscomplexobj(y) else \
+                np.stack([y, np.zeros_like(y)], axis=2)
+            return D.f64(yc)
+        return D.f64(np.asarray(y, dtype=np.float64).reshape(self.shape[0], self.shape[1]))
+
+    def adjoint(self, y_d, x_d):
+        h, w, c = self.shape
+        if self.kind == "fourier":
+            N.call("glr_fourier_adjoint", y_d.data_ptr(), self.mask.data_ptr(), h, w, c,
+                   x_d.data_ptr(), self.fft_ws.data_ptr(), D.stream())
+        else:
+            N.call("glr_masksum_adjoint", y_d.data_ptr(), self.masks.data_ptr(), h, w, c,
+                   x_d.data_ptr(), D.stream())
+
+    def gap_update(self, acc, cnt, frac, x_in, y_d, lo, hi, x_out, resid_out, ws):
+        """x_out = clip(z + A^T safe_div(y - A z, gram)); resid_out = ||y - A x_out||^2,
+        z = acc/cnt where covered else x_in (acc None: z = x_in)."""
+        h, w, c = self.shape
+        ap = acc.data_ptr() if acc is not None else None
+        cp = cnt.data_ptr() if cnt is not None else None
+        if self.kind == "fourier":
+            N.call("glr_gap_fourier", ap, cp, frac, x_in.data_ptr(), self.mask.data_ptr(),
+                   y_d.data_ptr(), h, w, c, 1 if self.clip else 0, lo, hi, x_out.data_ptr(),
+                   resid_out.data_ptr(), self.fft_ws.data_ptr(), D.stream())
+        else:
+            N.call("glr_gap_masksum", ap, cp, frac, x_in.data_ptr(), self.masks.data_ptr(),
+                   y_d.data_ptr(), self.gram.data_ptr(), h, w, c, lo, hi, x_out.data_ptr(),
+                   resid_out.data_ptr(), ws.data_ptr(), D.stream())
+
+
+class GlrEngine:
+    """Device state of one GLR reconstruction (one rank of a sharded run)."""
+
+    def __init__(self, shape, match, peak: float = 1.0, c_weight: float = 2.0 * np.sqrt(2.0),
+                 eps: float = 1e-16, process_group=None, heat_budget_bytes: int = 24 << 30):
+        t = D.torch()
+        h, w, c = shape
+        self.shape = (h, w, c)
+        self.mc = match
+        self.p = match.patch_size
+        self.k = match.group_size
+        if self.k > KMAX:
+            raise ValueError(f"group_size {self.k} exceeds the B200 WNNM kernel's {KMAX}")
+        if self.p > min(h, w):
+            raise ValueError(f"patch size {self.p} exceeds image {h}x{w}")
+        self.c_weight = c_weight
+        self.eps = eps
+        self.frac = frac_bits_for(peak)
+        self.pg = process_group
+        self.rank, self.world = 0, 1
+        if process_group is not None:
+            import torch.distributed as dist
+            self.rank = dist.get_rank(process_group)
+            self.world = dist.get_world_size(process_group)
+        p = self.p
+        self.oh, self.ow = h - p + 1, w - p + 1
+        self.grid_interval = 3 * match.exemplar_stride
+        g = self.grid_interval
+        self.max_anchors = match.max_corners + ((h - p) // g + 1) * ((w - p) // g + 1)
+        self.expand = N.query("glr_heat_expand_factor", c, p)
+        self.max_score = 4 * c * p * p
+        self.stride = N.query("glr_heat_stride", h, w, p)
+        # buffers
+        self.resp = D.empty((h, w), t.float64)
+        self.gh = D.empty((h, w, c), t.float64)
+        self.gv = D.empty((h, w, c), t.float64)
+        self.stack = D.empty((h * w * 4 * c * self.expand,), t.uint8)
+        self.corners = D.empty((match.max_corners, 2), t.int32)
+        self.n_corners = D.zeros((1,), t.int32)
+        self.anchors = D.empty((self.max_anchors, 2), t.int32)
+        self.tags = D.empty((self.max_anchors,), t.uint8)
+        self.n_anchors = D.zeros((1,), t.int32)
+        self.positions = D.empty((self.max_anchors, self.k, 2), t.int32)
+        self.padded = D.empty((self.max_anchors,), t.int32)
+        self.acc = D.zeros((h, w, c), t.int64)
+        self.cnt = D.zeros((h, w), t.int32)
+        self.gap_ws = D.empty((N.query("glr_gap_workspace", h, w),), t.uint8)
+        self.ws_corner = D.empty((N.query("glr_corner_workspace", h, w, c),), t.uint8)
+        self.ws_nms = D.empty((N.query("glr_nms_workspace", h, w),), t.uint8)
+        self.ws_anchor = D.empty((N.query("glr_anchor_workspace", h, w),), t.uint8)
+        self.ws_edge = D.empty((64,), t.uint8)
+        # heat map chunking over exemplars (the heat map is never communicated)
+        self.heat_chunk = max(1, min(self.max_anchors, heat_budget_bytes // (2 * self.stride)))
+        self.heat = D.empty((self.heat_chunk, self.stride), t.int16)
+        self.ws_heat = D.empty((N.query("glr_heat_workspace", c, p, self.heat_chunk),), t.uint8)
+        self.n = 0          # anchors in the current match state (all ranks)
+        self.lo = self.hi = 0
+        self.has_positions = False
+
+    # -- refresh: solvers.py:154-167 + 187-203 ---------------------------------
+    def refresh(self, x_d) -> int:
+        """Exemplars, edge stack, heat map and top-K for this rank's shard.
+        Returns the total anchor count."""
+        h, w, c = self.shape
+        mc = self.mc
+        s = D.stream()
+        N.call("glr_corner_response", x_d.data_ptr(), h, w, c, self.resp.data_ptr(),
+               self.ws_corner.data_ptr(), s)
+        N.call("glr_corners", self.resp.data_ptr(), h, w, mc.max_corners, mc.nms,
+               float(mc.corner_quality), self.corners.data_ptr(), self.n_corners.data_ptr(),
+               self.ws_nms.data_ptr(), self.ws_nms.numel(), s)
+        N.call("glr_select_anchors", self.corners.data_ptr(), self.n_corners.data_ptr(),
+               mc.max_corners, h, w, self.p, self.grid_interval, self.max_anchors,
+               self.anchors.data_ptr(), self.tags.data_ptr(), self.n_anchors.data_ptr(),
+               self.ws_anchor.data_ptr(), s)
+        n = int(self.n_anchors.item())  # one host sync per refresh
+        self.n = n
+        self.lo, self.hi = shard_bounds(n, self.rank, self.world)
+        self.has_positions = True
+        if n == 0:
+            return 0
+        N.call("glr_sobel", x_d.data_ptr(), h, w, c, self.gh.data_ptr(), self.gv.data_ptr(), s)
+        N.call("glr_edge_stack", self.gh.data_ptr(), self.gv.data_ptr(), h, w, c,
+               float(mc.edge_threshold), 1, self.expand, None, self.stack.data_ptr(),
+               self.ws_edge.data_ptr(), s)
+        self.match_shard()
+        self.count()
+        return n
+
+    def match_shard(self):
+        h, w, c = self.shape
+        s = D.stream()
+        for a in range(self.lo, self.hi, self.heat_chunk):
+            b = min(self.hi, a + self.heat_chunk)
+            nb = b - a
+            anc = self.anchors[a:b]
+            N.call("glr_heat_map", self.stack.data_ptr(), h, w, c, self.p, self.expand,
+                   anc.data_ptr(), nb, None, self.heat.data_ptr(), self.ws_heat.data_ptr(),
+                   self.ws_heat.numel(), s)
+            N.call("glr_topk", self.heat.data_ptr(), nb, None, self.oh, self.ow, self.max_score,
+                   anc.data_ptr(), self.k, self.mc.sep, self.positions[a:b].data_ptr(),
+                   self.padded[a:b].data_ptr(), None, 0, s)
+
+    def count(self):
+        h, w, c = self.shape
+        self.cnt.zero_()
+        nloc = self.hi - self.lo
+        if nloc > 0:
+            N.call("glr_scatter_count", self.positions[self.lo:self.hi].data_ptr(), nloc, None,
+                   self.k, self.p, h, w, self.cnt.data_ptr(), D.stream())
+        self._all_reduce(self.cnt)
+
+    def set_positions(self, anchors: np.ndarray, positions: np.ndarray):
+        """Inject a match state (positions-locked parity)."""
+        n = len(anchors)
+        self.n = n
+        self.lo, self.hi = shard_bounds(n, self.rank, self.world)
+        self.has_positions = True
+        if n:
+            self.anchors[:n].copy_(D.i32(np.asarray(anchors).reshape(n, 2)))
+            self.positions[:n].copy_(D.i32(np.asarray(positions).reshape(n, self.k, 2)))
+        self.count()
+
+    # -- every iteration: lowrank.py:68-87 --------------------------------------
+    def regularize(self, x_d, sigma: float) -> bool:
+        """acc <- fixed-point sum of WNNM-denoised patches of this shard (all-
+        reduced). Returns False when there are no groups (z = x)."""
+        if self.n == 0:
+            return False
+        h, w, c = self.shape
+        self.acc.zero_()
+        nloc = self.hi - self.lo
+        if nloc > 0:
+            N.call("glr_wnnm_scatter", x_d.data_ptr(), h, w, c, self.p,
+                   self.positions[self.lo:self.hi].data_ptr(), nloc, None, self.k, float(sigma),
+                   float(self.c_weight), float(self.eps), self.frac, self.acc.data_ptr(), None, 0,
+                   D.stream())
+        self._all_reduce(self.acc)
+        return True
+
+    def _all_reduce(self, t):
+        if self.pg is not None and self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.pg)
+
+    def positions_host(self):
+        n = self.n
+        return D.host(self.anchors[:n]), D.host(self.positions[:n]), D.host(self.padded[:n])

@@ -1,0 +1,299 @@
+"""GAP reconstruction loop with the global low-rank regularizer, on device
+(reference: glr/solvers.py:35-354).
+
+``gap_solve(op, y, cfg, ref=None)`` keeps the reference signature and
+returns (x, ReconReport) as numpy float64. The iterate never leaves the GPU
+inside the loop (engine.GlrEngine); the report's residuals, PSNRs and phase
+times are gathered once at the end. ``process_group`` (extra keyword) shards
+exemplars over the ranks of a torch.distributed group (one GPU per rank).
+"""
+
+from __future__ import annotations
+
+import csv
+import io
+import json
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _device as D
+from . import _native as N
+from .engine import DeviceOperator, GlrEngine
+from .lowrank import WnnmParams
+from .matching import MatchConfig
+from .metrics import PSNR_CAP_DB, ssim
+
+REGULARIZERS = ("glr", "nlr-bm", "nlr-corner-bm", "nlr-corner-uniform-bm", "tv")
+ALGORITHMS = ("gap", "admm")
+
+
+class SolverDivergenceError(RuntimeError):
+    pass
+
+
+@dataclass
+class SolverConfig:
+    """solvers.py:35-69."""
+
+    algorithm: str = "gap"
+    regularizer: str = "glr"
+    max_iters: int = 200
+    match_refresh_interval: int = 5
+    sigma0: float = 0.10
+    sigma_min: float = 0.003
+    admm_rho: float = 0.01
+    tv_weight: float = 0.05
+    tv_iters: int = 20
+    peak: float = 1.0
+    init: str = "adjoint"
+    seed: int = 0
+    match: MatchConfig = field(default_factory=MatchConfig)
+    wnnm: WnnmParams = field(default_factory=WnnmParams)
+
+    def __post_init__(self):
+        if self.algorithm not in ALGORITHMS:
+            raise ValueError(f"unknown algorithm {self.algorithm!r}")
+        if self.regularizer not in REGULARIZERS:
+            raise ValueError(f"unknown regularizer {self.regularizer!r}")
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be >= 1")
+        if self.match_refresh_interval < 1:
+            raise ValueError("match_refresh_interval must be >= 1")
+        if not (self.sigma0 >= self.sigma_min > 0):
+            raise ValueError("need sigma0 >= sigma_min > 0")
+        if self.init not in ("adjoint", "zero", "interp"):
+            raise ValueError(f"unknown init {self.init!r}")
+
+    def sigma_at(self, k: int) -> float:
+        """Geometric noise-level schedule, in absolute units (solvers.py:66-69)."""
+        frac = self.sigma0 * (self.sigma_min / self.sigma0) ** (k / self.max_iters)
+        return frac * self.peak
+
+
+REPORT_COLUMNS = ["iteration", "residual", "psnr_db", "ssim",
+                  "match_ms", "lowrank_ms", "projection_ms"]
+
+
+@dataclass
+class ReconReport:
+    """solvers.py:76-98."""
+
+    rows: list[dict] = field(default_factory=list)
+    total_ms: float = 0.0
+    diverged: bool = False
+
+    def add(self, **kw) -> None:
+        self.rows.append(kw)
+
+    def to_csv(self) -> str:
+        buf = io.StringIO()
+        w = csv.DictWriter(buf, fieldnames=REPORT_COLUMNS)
+        w.writeheader()
+        for row in self.rows:
+            w.writerow({k: row.get(k, "") for k in REPORT_COLUMNS})
+        return buf.getvalue()
+
+    def to_jsonl(self) -> str:
+        return "\n".join(json.dumps(r) for r in self.rows) + "\n"
+
+    @property
+    def final_psnr(self) -> float | None:
+        return self.rows[-1].get("psnr_db") if self.rows else None
+
+
+@dataclass
+class MatchState:
+    """Group anchor positions reused between matching refreshes
+    (solvers.py:145-151); ``engine`` holds the device state."""
+
+    positions: list[list[tuple[int, int]]] | None = None
+    last_refresh: int = -1
+    last_match_ms: float = 0.0
+    engine: object = None
+
+
+def _require_glr(cfg: SolverConfig) -> None:
+    if cfg.regularizer != "glr":
+        raise NotImplementedError(
+            f"regularizer {cfg.regularizer!r} is a baseline outside the B200 hot path "
+            "(SURVEY §8f); only 'glr' runs on device")
+
+
+def _expected_y_shape(op) -> tuple:
+    h, w = op.x_shape[:2]
+    return (h, w) if op.kind == "fourier" else (h, w, 1)
+
+
+def _check_measurement(op, y: np.ndarray) -> None:
+    """solvers.py:350-354."""
+    expect = _expected_y_shape(op)
+    if y.shape != expect:
+        raise ValueError(f"measurement shape {y.shape} does not match operator output {expect}")
+
+
+def _check_divergence(residuals: list[float], y_norm: float) -> None:
+    """solvers.py:272-281 — residual 10x above its minimum for 20 iterations."""
+    if len(residuals) < 21:
+        return
+    best = max(min(residuals), 1e-6 * y_norm)
+    tail = residuals[-20:]
+    if all(r > 10.0 * best for r in tail):
+        raise SolverDivergenceError(
+            f"data residual grew 10x over its minimum ({best:.3e}) for 20 "
+            f"consecutive iterations, last {tail[-1]:.3e}")
+
+
+def _init_device(dop: DeviceOperator, y_d, cfg: SolverConfig):
+    t = D.torch()
+    x = D.zeros(dop.shape, t.float64)
+    if cfg.init == "zero":
+        return x
+    if cfg.init == "interp":
+        raise NotImplementedError("init='interp' (Gaussian inpainting start) is not on the B200 "
+                                  "path yet; use init='adjoint' (DESIGN.md)")
+    dop.adjoint(y_d, x)
+    return x
+
+
+def regularize_dispatch(x: np.ndarray, cfg: SolverConfig, state: MatchState,
+                        iteration: int = 0, sigma: float | None = None) -> np.ndarray:
+    """solvers.py:170-210 — GLR regularizer with cached match positions."""
+    _require_glr(cfg)
+    x = np.asarray(x, dtype=np.float64)
+    sigma = cfg.sigma_at(iteration) if sigma is None else sigma
+    WnnmParams(c_weight=cfg.wnnm.c_weight, eps=cfg.wnnm.eps, noise_sigma=sigma)
+    eng = state.engine
+    if eng is None or eng.shape != x.shape:
+        eng = GlrEngine(x.shape, cfg.match, cfg.peak, cfg.wnnm.c_weight, cfg.wnnm.eps)
+        state.engine = eng
+    x_d = D.f64(x)
+    refresh = (state.positions is None
+               or iteration - state.last_refresh >= cfg.match_refresh_interval)
+    if refresh:
+        t0 = time.perf_counter()
+        n = eng.refresh(x_d)
+        if n:
+            _, pos, _ = eng.positions_host()
+            state.positions = [[tuple(q) for q in g] for g in pos.tolist()]
+        else:
+            state.positions = []
+        state.last_refresh = iteration
+        D.torch().cuda.synchronize()
+        state.last_match_ms = (time.perf_counter() - t0) * 1e3
+    else:
+        state.last_match_ms = 0.0
+    if not state.positions:
+        return x.copy()
+    eng.regularize(x_d, sigma)
+    z = D.empty(x.shape, D.torch().float64)
+    h, w, c = x.shape
+    N.call("glr_normalize", eng.acc.data_ptr(), eng.cnt.data_ptr(), x_d.data_ptr(), h, w, c,
+           eng.frac, z.data_ptr(), D.stream())
+    return D.host(z)
+
+
+def gap_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = None,
+              process_group=None, positions_override=None, trace=None):
+    """solvers.py:284-308 — regularize, then project onto the measurement-
+    consistent set; everything device-resident.
+
+    Extra keywords (not in the reference): ``process_group`` shards exemplars
+    across ranks; ``positions_override`` (list of (anchors, positions) per
+    refresh) locks matching for positions-locked parity; ``trace`` (a list)
+    receives (anchors, positions) of every refresh."""
+    if cfg.algorithm != "gap":
+        raise NotImplementedError("ADMM is the 'next' row f1 (SURVEY §8f); use algorithm='gap'")
+    _require_glr(cfg)
+    y = np.asarray(y)
+    _check_measurement(op, y)
+    t = D.torch()
+    t_start = time.perf_counter()
+    report = ReconReport()
+    dop = DeviceOperator(op)
+    eng = GlrEngine(op.x_shape, cfg.match, cfg.peak, cfg.wnnm.c_weight, cfg.wnnm.eps,
+                    process_group=process_group)
+    y_d = dop.upload_y(y)
+    x = _init_device(dop, y_d, cfg)
+    x_next = D.empty(dop.shape, t.float64)
+    iters = cfg.max_iters
+    resid_sq = D.zeros((iters,), t.float64)
+    ref_d = D.f64(ref) if ref is not None else None
+    sq = D.zeros((iters,), t.float64) if ref is not None else None
+    sq_ws = D.empty((N.query("glr_gap_workspace", 1, 1),), t.uint8) if ref is not None else None
+    lo, hi = -0.5 * cfg.peak, 1.5 * cfg.peak
+    ev = [[t.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(iters)]
+    last = -1
+    refresh_no = 0
+    refreshed = []
+    ssims = []
+    for it in range(iters):
+        e0, e1, e2, e3 = ev[it]
+        e0.record()
+        sigma = cfg.sigma_at(it)
+        is_refresh = (not eng.has_positions) or it - last >= cfg.match_refresh_interval
+        if is_refresh:
+            if positions_override is not None:
+                anc, pos = positions_override[refresh_no]
+                eng.set_positions(np.asarray(anc), np.asarray(pos))
+            else:
+                eng.refresh(x)
+            if trace is not None:
+                a, pz, _ = eng.positions_host()
+                trace.append((a.tolist(), pz.tolist()))
+            last = it
+            refresh_no += 1
+        refreshed.append(is_refresh)
+        e1.record()
+        has = eng.regularize(x, sigma)
+        e2.record()
+        dop.gap_update(eng.acc if has else None, eng.cnt if has else None, eng.frac, x, y_d,
+                       lo, hi, x_next, resid_sq[it:it + 1], eng.gap_ws)
+        e3.record()
+        x, x_next = x_next, x
+        if ref_d is not None:
+            n_el = int(np.prod(dop.shape))
+            N.call("glr_sq_err", x.data_ptr(), ref_d.data_ptr(), n_el, float(cfg.peak),
+                   sq[it:it + 1].data_ptr(), sq_ws.data_ptr(), D.stream())
+            xc = np.clip(D.host(x), 0.0, cfg.peak)
+            ssims.append(ssim(ref, xc, cfg.peak))
+    t.cuda.synchronize()
+    res = np.sqrt(D.host(resid_sq)).tolist()
+    sqh = D.host(sq) if sq is not None else None
+    for it in range(iters):
+        e0, e1, e2, e3 = ev[it]
+        row = {"iteration": it, "residual": float(res[it]),
+               "match_ms": round(e0.elapsed_time(e1), 3),
+               "lowrank_ms": round(e1.elapsed_time(e2), 3),
+               "projection_ms": round(e2.elapsed_time(e3), 3)}
+        if sqh is not None:
+            mse = sqh[it] / float(np.prod(dop.shape))
+            row["psnr_db"] = PSNR_CAP_DB if mse == 0.0 else \
+                min(10.0 * np.log10(cfg.peak ** 2 / mse), PSNR_CAP_DB)
+            row["ssim"] = ssims[it]
+        report.add(**row)
+    report.total_ms = (time.perf_counter() - t_start) * 1e3
+    y_norm = float(np.linalg.norm(y.ravel()))
+    for k in range(21, iters + 1):
+        _check_divergence(res[:k], y_norm)
+    out = D.host(x)
+    if dop.clip:
+        out = np.clip(out, 0.0, cfg.peak)
+    return out, report
+
+
+def admm_solve(op, y, cfg, ref=None):
+    """solvers.py:311-341 — the 'next' row f1."""
+    raise NotImplementedError("admm_solve is the 'next' row f1 (SURVEY §8f), not yet on B200")
+
+
+def solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = None):
+    """solvers.py:344-347."""
+    fn = gap_solve if cfg.algorithm == "gap" else admm_solve
+    return fn(op, y, cfg, ref)
+
+
+def tv_denoise(x, weight, iters=20):
+    """solvers.py:121-139 — TV baseline regularizer, outside the hot path."""
+    raise NotImplementedError("tv_denoise is a baseline outside the B200 hot path (DESIGN.md)")

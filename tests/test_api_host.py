@@ -1,0 +1,136 @@
+"""Host-side logic of the reference-facing API: dataclass validation, mask
+generators and argument checks that raise before any launch (CPU tests)."""
+
+import numpy as np
+import pytest
+
+import paper_2301_03047_b200 as G
+from conftest import load_golden
+
+
+def test_match_config_validation_and_defaults():
+    with pytest.raises(ValueError, match="group_size"):
+        G.MatchConfig(group_size=0)
+    with pytest.raises(ValueError, match="patch_size"):
+        G.MatchConfig(patch_size=1)
+    with pytest.raises(ValueError, match="mode"):
+        G.MatchConfig(mode="nope")
+    with pytest.raises(ValueError, match="backend"):
+        G.MatchConfig(backend="nope")
+    with pytest.raises(ValueError, match="bm_window"):
+        G.MatchConfig(mode="bm-uniform", patch_size=8, bm_window=4)
+    cfg = G.MatchConfig(patch_size=8)
+    assert cfg.sep == 2 and cfg.nms == 4
+    cfg = G.MatchConfig(patch_size=12)
+    assert cfg.sep == 3 and cfg.nms == 6
+    cfg = G.MatchConfig(patch_size=5, min_separation=0, nms_radius=1)
+    assert cfg.sep == 0 and cfg.nms == 1
+
+
+def test_solver_config_validation_and_schedule():
+    for bad in [dict(algorithm="sgd"), dict(regularizer="deep-prior"), dict(max_iters=0),
+                dict(match_refresh_interval=0), dict(sigma0=0.001, sigma_min=0.01),
+                dict(init="oracle")]:
+        with pytest.raises(ValueError):
+            G.SolverConfig(**bad)
+    cfg = G.SolverConfig(sigma0=0.1, sigma_min=0.001, max_iters=100, peak=2.0)
+    assert cfg.sigma_at(0) == pytest.approx(0.2)
+    assert cfg.sigma_at(100) == pytest.approx(0.002)
+    assert cfg.sigma_at(50) == pytest.approx(np.sqrt(0.1 * 0.001) * 2.0)
+
+
+def test_wnnm_params_validation():
+    for bad in [dict(c_weight=0.0), dict(eps=0.0), dict(noise_sigma=-1.0)]:
+        with pytest.raises(ValueError):
+            G.WnnmParams(**bad)
+
+
+def test_mask_generators_match_reference_golden():
+    g = load_golden("operators")
+    np.testing.assert_array_equal(G.bernoulli_masks(9, 7, 3, seed=7), g["bern_seed7"])
+    np.testing.assert_array_equal(G.msfa_pattern("periodic-4x4", 16, 16, 20), g["msfa_masks"])
+    np.testing.assert_array_equal(G.radial_mask(16, 16, 5), g["four_mask"])
+    np.testing.assert_array_equal(G.bernoulli_masks(16, 20, 8, seed=3), g["cacti_masks"])
+
+
+def test_radial_mask_properties():
+    for h, w, n in ((16, 16, 1), (32, 24, 5), (64, 64, 30)):
+        m = np.fft.fftshift(G.radial_mask(h, w, n))
+        assert m[h // 2, w // 2] == 1.0
+        ys, xs = np.nonzero(m)
+        for r, c in zip(ys, xs):
+            r2, c2 = 2 * (h // 2) - r, 2 * (w // 2) - c
+            if 0 <= r2 < h and 0 <= c2 < w:
+                assert m[r2, c2] == 1.0
+    m = np.fft.fftshift(G.radial_mask(17, 17, 1))
+    assert np.array_equal(np.nonzero(m.sum(axis=1))[0], [8])
+    assert G.radial_mask(64, 64, 128).mean() >= 0.95
+    with pytest.raises(ValueError):
+        G.radial_mask(8, 8, 0)
+
+
+def test_msfa_pattern_and_partition_errors():
+    with pytest.raises(ValueError, match="requires C"):
+        G.msfa_pattern("periodic-4x4", 9, 8, 8)
+    with pytest.raises(ValueError, match="out of range"):
+        G.msfa_pattern("custom-tile", 2, 8, 8, tile=np.array([[0, 2], [1, 0]]))
+    with pytest.raises(ValueError, match="unknown"):
+        G.msfa_pattern("hexagonal", 4, 8, 8)
+    with pytest.raises(ValueError, match="tile"):
+        G.msfa_pattern("custom-tile", 4, 8, 8)
+    with pytest.raises(ValueError, match="orthogonal"):
+        G.msfa_operator(np.ones((4, 4, 2)))
+    masks = np.zeros((4, 4, 2))
+    masks[:, :, 0] = 1.0
+    masks[0, 0, 0] = 0.0
+    with pytest.raises(ValueError, match="partition"):
+        G.msfa_operator(masks)
+    for kind, c in [("bayer-like-2x2", 4), ("periodic-3x3", 9), ("periodic-4x4", 16)]:
+        m = G.msfa_pattern(kind, c, 48, 48)
+        assert np.array_equal(m.sum(axis=2), np.ones((48, 48)))
+
+
+def test_validation_before_launch():
+    with pytest.raises(ValueError, match="nonnegative"):
+        G.binarize_gradients(np.zeros((3, 3, 1)), np.zeros((3, 3, 1)), th=-0.1)
+    with pytest.raises(ValueError, match="differ"):
+        G.binarize_gradients(np.zeros((3, 3, 1)), np.zeros((3, 4, 1)))
+    with pytest.raises(ValueError, match="too small"):
+        G.sobel_gradients(np.zeros((2, 5, 1)))
+    with pytest.raises(ValueError, match="max_n"):
+        G.detect_corners(np.zeros((8, 8, 1)), max_n=0)
+    with pytest.raises(ValueError, match="exceeds"):
+        G.select_exemplars([], (6, 6), 8)
+    with pytest.raises(ValueError, match="anchor 1"):
+        G.gather_group(np.zeros((4, 4, 1)), [(0, 0), (3, 0)], 2)
+    g = G.PatchGroup(patch_size=2, positions=[(0, 0)], matrix=np.zeros((4, 1)))
+    with pytest.raises(ValueError, match="accumulator"):
+        G.scatter_group(np.zeros((4, 4, 1)), np.zeros((4, 5, 1)), g)
+    m = np.ones((3, 3))
+    m[1, 1] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        G.wnnm_prox(m, G.WnnmParams())
+    op = G.cacti_operator(G.bernoulli_masks(8, 8, 2, seed=0))
+    with pytest.raises(ValueError, match="measurement shape"):
+        G.gap_solve(op, np.zeros((8, 9, 1)), G.SolverConfig())
+    with pytest.raises(ValueError, match="mask"):
+        G.operators.cacti_forward(np.zeros((8, 8, 3)), np.zeros((8, 8, 4)))
+    with pytest.raises(ValueError, match="integer overlap counts"):
+        G.top_k_positions(np.full((4, 4), 0.5), (0, 0), 3, 1)
+    with pytest.raises(NotImplementedError):
+        G.gap_solve(op, np.zeros((8, 8, 1)), G.SolverConfig(regularizer="tv"))
+
+
+def test_report_serialization():
+    rep = G.ReconReport()
+    rep.add(iteration=0, residual=1.5, match_ms=2.0, lowrank_ms=3.0, projection_ms=0.5)
+    assert rep.to_csv().splitlines()[0].startswith("iteration,residual")
+    assert rep.to_jsonl().strip().startswith("{")
+    assert rep.final_psnr is None
+
+
+def test_divergence_guard():
+    from paper_2301_03047_b200.solvers import _check_divergence
+    with pytest.raises(G.SolverDivergenceError, match="10x"):
+        _check_divergence([1.0] + [20.0] * 20, y_norm=1.0)
+    _check_divergence([1e-15] + [1e-9] * 20, y_norm=1.0)

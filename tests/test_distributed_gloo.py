@@ -1,0 +1,94 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2): exemplar sharding and
+the int64 fixed-point aggregation all-reduce are rank-count invariant —
+the 2-rank result is bitwise the 1-rank result."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import glr_oracle as O
+from paper_2301_03047_b200.engine import shard_bounds
+from paper_2301_03047_b200.lowrank import frac_bits_for
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _fixed_point_partial(x, groups, p, sigma, frac, lo, hi):
+    """CPU model of the device numerator for anchors [lo, hi): WNNM per group
+    (oracle), values rounded to int64 fixed point, scatter-added."""
+    h, w, c = x.shape
+    acc = np.zeros((h, w, c), dtype=np.int64)
+    cnt = np.zeros((h, w), dtype=np.int32)
+    scale = 2.0 ** frac
+    for pos in groups[lo:hi]:
+        den = O.wnnm_prox(O.gather_group(x, pos, p), sigma)
+        for j, (r, cc) in enumerate(pos):
+            acc[r:r + p, cc:cc + p, :] += np.rint(den[:, j].reshape(p, p, c) * scale).astype(np.int64)
+            cnt[r:r + p, cc:cc + p] += 1
+    return acc, cnt
+
+
+def _setup_case():
+    rng = np.random.default_rng(7)
+    x = rng.random((20, 22, 3))
+    p, k = 4, 6
+    groups = [[(int(rng.integers(0, 17)), int(rng.integers(0, 19))) for _ in range(k)]
+              for _ in range(13)]
+    return x, p, groups
+
+
+def _worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    x, p, groups = _setup_case()
+    frac = frac_bits_for(1.0)
+    lo, hi = shard_bounds(len(groups), rank, world)
+    acc, cnt = _fixed_point_partial(x, groups, p, 0.05, frac, lo, hi)
+    ta, tc = torch.from_numpy(acc), torch.from_numpy(cnt)
+    dist.all_reduce(ta)
+    dist.all_reduce(tc)
+    if rank == 0:
+        np.savez(out_path, acc=ta.numpy(), cnt=tc.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_shard_bounds_cover_exactly():
+    for n in [0, 1, 7, 701, 4096, 4097]:
+        for world in [1, 2, 3, 4, 8]:
+            bounds = [shard_bounds(n, r, world) for r in range(world)]
+            assert bounds[0][0] == 0 and bounds[-1][1] == n
+            for (a, b), (c, d) in zip(bounds, bounds[1:]):
+                assert b == c and a <= b
+            sizes = [b - a for a, b in bounds]
+            assert max(sizes) - min(sizes) <= 1
+
+
+@pytest.mark.timeout(180)
+def test_two_rank_aggregation_bitwise_equals_one_rank(tmp_path):
+    out = tmp_path / "r.npz"
+    mp.spawn(_worker, args=(2, _free_port(), str(out)), nprocs=2, join=True)
+    got = np.load(out)
+    x, p, groups = _setup_case()
+    acc1, cnt1 = _fixed_point_partial(x, groups, p, 0.05, frac_bits_for(1.0), 0, len(groups))
+    assert np.array_equal(got["acc"], acc1)
+    assert np.array_equal(got["cnt"], cnt1)
+    # the fixed-point normalisation agrees with the reference's fp64 pass
+    covered = cnt1 > 0
+    z = x.copy()
+    z[covered] = (acc1[covered].astype(np.float64) / 2.0 ** frac_bits_for(1.0)) \
+        / cnt1[covered][:, None]
+    ref = O.glr_regularize(x, groups, p, 0.05)
+    np.testing.assert_allclose(z, ref, atol=1e-11, rtol=0)

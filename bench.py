@@ -1,0 +1,380 @@
+"""GLR hot-path benchmark (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config C2] [--no-cpu-baseline]
+
+A step is one full GAP-GLR reconstruction of the workload (BASELINE.json
+configs[1] = C2 by default: 1024x1024x24 CACTI, 50 iterations, 8x8 patches,
+4096 exemplars, K = 64 — refreshes every 5 iterations included). The metric
+is GLR iterations per second of the whole job:
+
+  value  device-resident: measurement and masks already in HBM, CUDA events,
+         barrier + synchronize on both sides, max over ranks;
+  e2e    the public API gap_solve(op, y, cfg) with host (pinned) numpy inputs,
+         H2D of y/masks/gram and D2H of the result inside the timed region.
+
+N > 1 (torchrun): exemplars shard over the ranks of one solve with an int64
+NCCL all-reduce of the aggregation numerator per iteration (strong scaling).
+``--impl reference`` times the CPU oracle port (oracle/glr_oracle.py — the
+reference's algorithm restated; the reference is pure Python and cannot
+travel to the box) on a bounded sample of the same workload, extrapolated to
+the full solve; only rank 0 runs it.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "GLR iters/s (C2 1024x1024x24 CACTI GAP-GLR, 50 it, 4096 exemplars, K=64)"
+UNIT = "iters/s"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md clocks line)
+
+class Clocks:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.proc = None
+        self.path = Path(os.environ.get("TMPDIR", "/tmp")) / f"glr_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self, device_index: int = 0):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9 or f[0] != str(device_index):
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = max(smax, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port on a bounded sample, extrapolated
+
+def cpu_sample(wl, n_heat=8, n_groups=64) -> dict:
+    """Times the oracle on one slice of every stage of the solve and
+    extrapolates to the full reconstruction (iters/s)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import glr_oracle as O
+    mc = wl.match
+    p, k = mc.patch_size, mc.group_size
+    sep = mc.sep
+    if wl.kind == "fourier":
+        op = O.Operator("fourier", mask=wl.masks, channels=wl.scene.shape[2])
+    else:
+        op = O.Operator(wl.kind, masks=wl.masks)
+    t0 = time.perf_counter()
+    x = op.adjoint(wl.y)
+    t_init = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    anchors = O.build_exemplars(x, p, mc.max_corners, mc.nms, mc.corner_quality,
+                                mc.exemplar_stride)
+    t_exemplars = time.perf_counter() - t0
+    n = len(anchors)
+    t0 = time.perf_counter()
+    gh, gv = O.sobel_gradients(x)
+    maps = O.binarize_gradients(gh, gv, mc.edge_threshold)
+    t_edges = time.perf_counter() - t0
+    sub = anchors[:n_heat]
+    t0 = time.perf_counter()
+    heat = O.similarity_heatmap(maps, sub, p)
+    t_heat = (time.perf_counter() - t0) / len(sub)
+    t0 = time.perf_counter()
+    positions, _ = O.match_positions(heat, sub, k, sep)
+    t_topk = (time.perf_counter() - t0) / len(sub)
+    groups = [positions[i % len(positions)] for i in range(n_groups)]
+    sigma = O.sigma_at(0, wl.max_iters)
+    t0 = time.perf_counter()
+    acc = np.zeros_like(x)
+    cnt = np.zeros_like(x)
+    for pos in groups:
+        den = O.wnnm_prox(O.gather_group(x, pos, p), sigma)
+        O.scatter_group(acc, cnt, den, pos, p)
+    t_group = (time.perf_counter() - t0) / n_groups
+    t0 = time.perf_counter()
+    z = x + op.adjoint(O.safe_div(wl.y - op.forward(x), op.gram))
+    np.linalg.norm((wl.y - op.forward(np.clip(z, -0.5, 1.5))).ravel())
+    t_proj = time.perf_counter() - t0
+    iters = wl.max_iters
+    n_refresh = -(-iters // 5)
+    total = (t_init + n_refresh * (t_exemplars + t_edges + n * (t_heat + t_topk))
+             + iters * (n * t_group + t_proj))
+    sampled = t_init + t_exemplars + t_edges + len(sub) * (t_heat + t_topk) \
+        + n_groups * t_group + t_proj
+    return {
+        "value": iters / total, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+        "sample": (f"oracle/glr_oracle.py on {wl.name}: full exemplar detection + edges, heat "
+                   f"map + top-K for {len(sub)} of {n} exemplars, gather+WNNM+scatter for "
+                   f"{n_groups} groups, one projection ({sampled:.1f} s sampled); extrapolated "
+                   f"to {n_refresh} refreshes + {iters} iterations = {total:.0f} s per solve"),
+        "stage_s": {"exemplars": t_exemplars, "edges": t_edges, "heat_per_exemplar": t_heat,
+                    "topk_per_exemplar": t_topk, "group": t_group, "projection": t_proj},
+        "n_exemplars": n,
+    }
+
+
+# ---------------------------------------------------------------------------
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    from paper_2301_03047_b200 import workloads
+    wl = workloads.make(args.config)
+    vals, details = [], None
+    for _ in range(args.warmup):
+        cpu_sample(wl, n_heat=2, n_groups=8)
+    t_start = time.perf_counter()
+    for _ in range(args.steps):
+        details = cpu_sample(wl)
+        vals.append(details["value"])
+    wall = time.perf_counter() - t_start
+    v = float(statistics.mean(vals))
+    line = {
+        "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config(args, wl, details["n_exemplars"]),
+        "cpu_baseline": {k: details[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config(args, wl, n_exemplars):
+    h, w, c = wl.shape
+    return {"workload": f"{wl.name}: {wl.kind.upper()} {h}x{w}x{c}, GAP-GLR {wl.max_iters} it, "
+                        f"P={wl.match.patch_size}, K={wl.match.group_size}, "
+                        f"max_corners={wl.match.max_corners}, "
+                        f"exemplar_stride={wl.match.exemplar_stride}",
+            "exemplars": n_exemplars, "iters_per_step": wl.max_iters,
+            "parallelism": f"exemplar-shard x{args.gpus}",
+            "l2": "inputs > L2 (x, masks 201 MB each; heat map 8.5 GB per refresh)",
+            "seed": 0}
+
+
+def run_b200(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    pg = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        pg = dist.group.WORLD
+    import paper_2301_03047_b200 as G
+    from paper_2301_03047_b200 import _device as D, _native as N, workloads
+    from paper_2301_03047_b200.solvers import GapRunner
+    wl = workloads.make(args.config)
+    h, w, c = wl.shape
+    cfg = G.SolverConfig(max_iters=wl.max_iters, match=wl.match)
+    op = workloads.operator_for(wl)
+    runner = GapRunner(op, cfg, process_group=pg)
+    y_d = runner.dop.upload_y(wl.y)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        runner.run(y_d)
+    torch.cuda.synchronize()
+    n_ex = runner.eng.n
+    # ---- timed region: device-resident solves ----
+    clocks = Clocks() if rank == 0 else None
+    runner.eng.timing = []
+    barrier()
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.start()
+    launches0 = N.launch_count
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        runner.run(y_d)
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    launches = N.launch_count - launches0
+    ck = clocks.stop(local_rank) if clocks else None
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    timing = runner.eng.timing
+    runner.eng.timing = None
+    kern = {}
+    for (name, nb), a, b in timing:
+        d = kern.setdefault(name, {"launches": 0, "ms": 0.0, "units": 0})
+        d["launches"] += 1
+        d["ms"] += a.elapsed_time(b)
+        d["units"] += nb
+    iters_total = args.steps * wl.max_iters
+    value = iters_total / (ms / 1e3)
+
+    # ---- e2e: public API with host inputs ----
+    import torch as _t
+    pin = lambda a: _t.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    y_host = pin(wl.y)
+    op_host = workloads.operator_for(wl)
+    if wl.kind != "fourier":
+        op_host.meta["masks"] = pin(op_host.meta["masks"])
+        op_host.gram_diag = pin(op_host.gram_diag)
+        h2d = y_host.nbytes + op_host.meta["masks"].nbytes + op_host.gram_diag.nbytes
+    else:
+        op_host.meta["mask"] = pin(op_host.meta["mask"])
+        h2d = 2 * y_host.nbytes + op_host.meta["mask"].nbytes
+    d2h = h * w * c * 8 + wl.max_iters * 8
+    e2e_steps = max(1, min(args.steps, 3))
+    G.gap_solve(op_host, y_host, cfg, process_group=pg)  # allocator warm
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        G.gap_solve(op_host, y_host, cfg, process_group=pg)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = e2e_steps * wl.max_iters / e2e_s
+
+    if rank == 0:
+        peaks, peak_src = _peaks()
+        mp = wl.match.patch_size
+        oh, ow = h - mp + 1, w - mp + 1
+        roof = {}
+        if "heat_map" in kern:
+            d = kern["heat_map"]
+            flops = 2.0 * oh * ow * 4 * c * mp * mp * d["units"] / d["launches"]
+            avg_s = d["ms"] / d["launches"] / 1e3
+            ach = flops / avg_s / 1e12
+            pk = 2.0 * peaks["bf16_tflops"]
+            roof["heat_map"] = {"bound": "tensor", "achieved": ach, "peak": pk,
+                                "unit": "TFLOP/s", "frac": ach / pk,
+                                "avg_ms": d["ms"] / d["launches"]}
+        if "wnnm_scatter" in kern:
+            d = kern["wnnm_scatter"]
+            m = mp * mp * c
+            k = wl.match.group_size
+            byts = 2.0 * m * k * 8 * d["units"] / d["launches"]
+            avg_s = d["ms"] / d["launches"] / 1e3
+            ach = byts / avg_s / 1e9
+            roof["wnnm_scatter"] = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
+                                    "unit": "GB/s", "frac": ach / peaks["hbm_gbs"],
+                                    "avg_ms": d["ms"] / d["launches"],
+                                    "fp64_tflops": (4.0 * m * k * k * d["units"] / d["launches"])
+                                    / avg_s / 1e12}
+        if "topk" in kern:
+            d = kern["topk"]
+            byts = 2.0 * oh * ow * 2 * d["units"] / d["launches"]
+            avg_s = d["ms"] / d["launches"] / 1e3
+            ach = byts / avg_s / 1e9
+            roof["topk"] = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
+                            "unit": "GB/s", "frac": ach / peaks["hbm_gbs"],
+                            "avg_ms": d["ms"] / d["launches"]}
+        dominant = max(kern, key=lambda n: kern[n]["ms"]) if kern else None
+        roofline = dict(roof.get(dominant, {})) if dominant else {}
+        traffic = None
+        prof = ROOT / "profiles" / "ncu_traffic.json"
+        if prof.exists() and dominant:
+            traffic = json.loads(prof.read_text()).get(dominant)
+        roofline["traffic"] = traffic
+        roofline["kernel"] = dominant
+        roofline["peak_source"] = f"{peak_src} (MEASURED_PEAKS.json)" if peak_src == "measured" \
+            else "fallback (B200_PROFILING.md)"
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64+u8",
+            "data": "synthetic (seeded generator, workloads.py)",
+            "config": _config(args, wl, n_ex),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "steps": e2e_steps},
+            "gpu_launches": int(launches),
+            "roofline": roofline,
+            "kernels": {n: {"launches": d["launches"], "ms_total": round(d["ms"], 3),
+                            "share_of_step": round(d["ms"] / ms, 4),
+                            **({k2: v for k2, v in roof[n].items()} if n in roof else {})}
+                        for n, d in kern.items()},
+            "clocks": ck,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            cb = cpu_sample(wl)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    run_b200(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -140,11 +140,14 @@ int glr_wnnm(const double* groups_d, int G, int m, int K, double sigma, double c
 /* ---- (4)+(5) fused regularizer: glr/lowrank.py:68-87 + patches.py:57-70 ----
  * For every group g < n: gather from x, WNNM, and scatter-add the denoised
  * patches into acc_d, an int64 fixed-point numerator (value * 2^frac_bits),
- * so aggregation is deterministic and rank-count invariant.               */
+ * so aggregation is deterministic and rank-count invariant.
+ * vcache_d (optional, n_max*64*64 doubles) keeps each group's eigenvectors;
+ * warm != 0 starts the Jacobi sweeps from them (valid while the group's
+ * positions are unchanged, i.e. between matching refreshes).              */
 int glr_wnnm_scatter(const double* x_d, int H, int W, int C, int P, const int32_t* positions_d,
                      int n_max, const int32_t* n_dev_d, int K, double sigma, double c_weight,
-                     double eps, int frac_bits, int64_t* acc_d, void* ws_d, size_t ws_bytes,
-                     void* stream);
+                     double eps, int frac_bits, int64_t* acc_d, double* vcache_d, int warm,
+                     void* ws_d, size_t ws_bytes, void* stream);
 
 /* glr_scatter_count: cnt[r][c] += 1 for every pixel covered by every patch
  * (channel-invariant form of scatter_group's counter, patches.py:70).      */

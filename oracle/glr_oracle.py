@@ -177,11 +177,13 @@ def build_exemplars(x, patch_size=8, max_corners=512, nms=None, quality=0.01,
 def similarity_heatmap(maps, anchors, patch_size: int, chunk: int = 256) -> np.ndarray:
     """matching.py:140-167 — (oh, ow, N) edge-overlap counts, int64.
 
-    Computed by shift-and-accumulate over the P x P window on the 4C-channel
-    stack in integer arithmetic (exact, like the reference's f32 GEMM of 0/1
-    values); exemplars in chunks to bound memory (they are independent)."""
+    Computed exactly in float32 (integers < 2^24, like the reference's f32
+    GEMM of 0/1 values) without an im2col copy: for each kernel row dr one
+    GEMM of the contiguous row block E[dr:dr+oh] against all P column taps of
+    every exemplar, then the P column-shifted partials are summed.
+    Exemplars go in chunks to bound memory (they are independent)."""
     e = np.concatenate([np.asarray(m, dtype=np.uint8) for m in maps], axis=2)  # (H,W,4C)
-    h, w, _ = e.shape
+    h, w, c4 = e.shape
     p = patch_size
     oh, ow = h - p + 1, w - p + 1
     n = len(anchors)
@@ -189,13 +191,16 @@ def similarity_heatmap(maps, anchors, patch_size: int, chunk: int = 256) -> np.n
     ef = e.astype(np.float32)
     for s in range(0, n, chunk):
         block = anchors[s:s + chunk]
+        b = len(block)
         ker = np.stack([ef[r:r + p, c:c + p, :] for r, c in block])      # (b,P,P,4C)
-        acc = np.zeros((oh, ow, len(block)), dtype=np.float32)
+        acc = np.zeros((oh, ow, b), dtype=np.float32)
         for dr in range(p):
+            rows = ef[dr:dr + oh].reshape(oh * w, c4)                    # contiguous
+            kt = ker[:, dr].transpose(2, 1, 0).reshape(c4, p * b)        # (4C, P*b)
+            part = (rows @ kt).reshape(oh, w, p, b)
             for dc in range(p):
-                win = ef[dr:dr + oh, dc:dc + ow, :]                      # (oh,ow,4C)
-                acc += win @ ker[:, dr, dc, :].T                         # exact ints < 2^24
-        out[:, :, s:s + len(block)] = acc.astype(np.int64)
+                acc += part[:, dc:dc + ow, dc, :]
+        out[:, :, s:s + b] = acc.astype(np.int64)
     return out
 
 

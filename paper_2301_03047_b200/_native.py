@@ -59,7 +59,7 @@ SIGNATURES: dict[str, tuple] = {
     "glr_wnnm_workspace": (sz, [i32, i32]),
     "glr_wnnm": (i32, [vp, i32, i32, i32, f64, f64, f64, f64, vp, vp, vp, sz, vp]),
     "glr_wnnm_scatter": (i32, [vp, i32, i32, i32, i32, vp, i32, vp, i32, f64, f64, f64, i32, vp,
-                               vp, sz, vp]),
+                               vp, i32, vp, sz, vp]),
     "glr_scatter_count": (i32, [vp, i32, vp, i32, i32, i32, i32, vp, vp]),
     "glr_scatter_add_f64": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, vp, vp, vp]),
     "glr_scatter_fixed": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, vp]),
@@ -125,10 +125,29 @@ def check(status: int, what: str = "") -> None:
     raise RuntimeError(f"glr status {status}: {msg}")
 
 
+# Own kernels launched per successful call (fixed by each entry point's body;
+# the CUB radix-sort kernels inside glr_corners are not counted). Used for the
+# bench's gpu_launches claim.
+KERNELS_PER_CALL = {
+    "glr_sobel": 1, "glr_stack_from_maps": 1, "glr_corner_response": 6, "glr_corners": 3,
+    "glr_select_anchors": 1, "glr_heat_map": 2, "glr_topk": 1, "glr_gather": 1, "glr_wnnm": 1,
+    "glr_wnnm_scatter": 1, "glr_scatter_count": 1, "glr_scatter_fixed": 1,
+    "glr_scatter_add_f64": 1, "glr_normalize": 1, "glr_masksum_forward": 1,
+    "glr_masksum_adjoint": 1, "glr_gap_masksum": 2, "glr_fourier_forward": 4,
+    "glr_fourier_adjoint": 4, "glr_gap_fourier": 11, "glr_sq_err": 2,
+}
+launch_count = 0
+
+
 def call(name: str, *args) -> int:
+    global launch_count
     lib = load(require_gpu=True)
     st = getattr(lib, name)(*args)
     check(st, name)
+    if name == "glr_edge_stack":  # relative max pass + maps and/or stack
+        launch_count += int(bool(args[6])) + int(args[8] is not None) + int(args[9] is not None)
+    else:
+        launch_count += KERNELS_PER_CALL.get(name, 0)
     return st
 
 

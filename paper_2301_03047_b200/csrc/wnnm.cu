@@ -22,8 +22,9 @@ namespace glr {
 namespace wn {
 constexpr int THREADS = 256;
 constexpr int KMAX = 64;
-constexpr int LD = KMAX + 1;  // padded leading dimension of G / V / Wm
+constexpr int LD = KMAX + 2;  // padded leading dimension of G / V / Wm (16-byte rows)
 constexpr int ROWS = 32;      // rows of M per tile
+constexpr int TS = KMAX + 2;  // row stride of the M tiles (16-byte rows, 2-way STS banks)
 constexpr int MAX_SWEEPS = 24;
 }  // namespace wn
 
@@ -42,6 +43,8 @@ struct WnnmArgs {
   int64_t* acc;
   double scale;  // 2^frac_bits
   int32_t* nonfinite;
+  double* vcache;  // optional per-group eigenvector cache (n_max x 64 x 64)
+  int warm;        // start the Jacobi sweeps from vcache
 };
 
 template <bool FROM_IMAGE>
@@ -61,24 +64,58 @@ template <bool FROM_IMAGE>
 __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
   using namespace wn;
   extern __shared__ __align__(16) double sm[];
-  double* G = sm;                 // KMAX x LD
-  double* V = G + KMAX * LD;      // KMAX x LD
+  double* G = sm;                 // KMAX x LD (Gram, then Wm)
+  double* V = G + KMAX * LD;      // KMAX x LD (eigenvectors, then row tiles)
   double* T = V + KMAX * LD;      // ROWS x KMAX tile of M
-  __shared__ double cs_c[KMAX / 2], cs_s[KMAX / 2];
-  __shared__ int pair_p[KMAX / 2], pair_q[KMAX / 2];
   __shared__ double ratio[KMAX];
-  __shared__ double red[wn::THREADS / 32][2];
-  __shared__ int s_stop, s_bad;
+  __shared__ double s_tiny;
+  __shared__ int s_flag[2], s_bad;
 
   const int g = blockIdx.x;
   const int N = a.n_dev ? min(*a.n_dev, a.n_max) : a.n_max;
   if (g >= N) return;
   const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const int K = a.K, m = a.m;
-  const int Ke = K + (K & 1);  // even size for the round-robin pairing
 
-  // ---- Gram: each thread owns a 4x4 block of G ----
-  const int bi = tid / 16, bj = tid % 16;
+  // Element (r, j) of the group matrix lives at src[cbase[j] + roff(r)]: for
+  // image groups roff(r) = (r / PC) * W*C + r % PC (patch row dr, then the
+  // contiguous (dc, ch) run of P*C values), for explicit groups roff(r) = r.
+  const double* src = FROM_IMAGE ? a.x : a.groups;
+  const int PC = FROM_IMAGE ? a.P * a.C : m;
+  const int64_t rs = FROM_IMAGE ? (int64_t)a.W * a.C : 0;
+  __shared__ long long cbase[KMAX];
+  if (tid < KMAX) {
+    long long b = 0;
+    if (tid < K) {
+      if constexpr (FROM_IMAGE) {
+        const int32_t* q = a.pos + ((size_t)g * K + tid) * 2;
+        b = ((long long)q[0] * a.W + q[1]) * a.C;
+      } else {
+        b = ((long long)g * K + tid) * m;
+      }
+    }
+    cbase[tid] = b;
+  }
+  __syncthreads();
+  // coalesced tile fill: warp w loads columns w, w+8, ..., lanes run down rows
+  auto fill = [&](double* Tt, int r0, int R, bool& bad) {
+    for (int rr = lane; rr < R; rr += 32) {
+      const int r = r0 + rr;
+      const bool rok = r < m;
+      const int64_t off = rok ? (int64_t)(r / PC) * rs + (r % PC) : 0;
+#pragma unroll 4
+      for (int j = warp; j < KMAX; j += THREADS / 32) {
+        double v = 0.0;
+        if (rok && j < K) v = src[cbase[j] + off];
+        bad |= !isfinite(v);
+        Tt[rr * TS + j] = v;
+      }
+    }
+  };
+
+  // ---- Gram G = M^T M (K padded to 64 with zero columns); 4x4 block per thread
+  const int bi = tid >> 4, bj = tid & 15;
   double acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -86,198 +123,284 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
   bool bad = false;
   for (int r0 = 0; r0 < m; r0 += ROWS) {
-    for (int t = tid; t < ROWS * KMAX; t += THREADS) {
-      const int rr = t / KMAX, j = t % KMAX;
-      double v = 0.0;
-      if (r0 + rr < m && j < K) v = load_m<FROM_IMAGE>(a, g, r0 + rr, j);
-      bad |= !isfinite(v);
-      T[t] = v;
-    }
+    fill(T, r0, ROWS, bad);
     __syncthreads();
-    if (4 * bi < K && 4 * bj < K) {
-      const int rmax = min(ROWS, m - r0);
-      for (int rr = 0; rr < rmax; ++rr) {
-        double x[4], y[4];
+    const int rmax = min(ROWS, m - r0);
+    for (int rr = 0; rr < rmax; ++rr) {
+      const double2 x01 = *reinterpret_cast<const double2*>(&T[rr * TS + 4 * bi]);
+      const double2 x23 = *reinterpret_cast<const double2*>(&T[rr * TS + 4 * bi + 2]);
+      const double2 y01 = *reinterpret_cast<const double2*>(&T[rr * TS + 4 * bj]);
+      const double2 y23 = *reinterpret_cast<const double2*>(&T[rr * TS + 4 * bj + 2]);
+      const double x[4] = {x01.x, x01.y, x23.x, x23.y};
+      const double y[4] = {y01.x, y01.y, y23.x, y23.y};
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          x[k] = T[rr * KMAX + 4 * bi + k];
-          y[k] = T[rr * KMAX + 4 * bj + k];
-        }
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fma(x[i], y[j], acc[i][j]);
-      }
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(x[i], y[j], acc[i][j]);
     }
     __syncthreads();
   }
-  if (tid == 0) s_bad = 0;
+  if (tid == 0) {
+    s_bad = 0;
+    s_flag[0] = s_flag[1] = 0;
+  }
   __syncthreads();
   if (bad) s_bad = 1;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int ii = 4 * bi + i, jj = 4 * bj + j;
-      if (ii < KMAX && jj < KMAX) G[ii * LD + jj] = (ii < K && jj < K) ? acc[i][j] : 0.0;
+    for (int j = 0; j < 4; ++j) G[(4 * bi + i) * LD + 4 * bj + j] = acc[i][j];
+  double* vc = a.vcache ? a.vcache + (size_t)g * KMAX * KMAX : nullptr;
+  if (!(vc && a.warm)) {
+    for (int t = tid; t < KMAX * KMAX; t += THREADS) {
+      const int i = t >> 6, j = t & 63;
+      V[i * LD + j] = (i == j) ? 1.0 : 0.0;
     }
-  for (int t = tid; t < KMAX * KMAX; t += THREADS) {
-    const int i = t / KMAX, j = t % KMAX;
-    V[i * LD + j] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
   if (s_bad) {
     if (tid == 0 && a.nonfinite) atomicExch(a.nonfinite, 1);
     return;
   }
+  if (vc && a.warm) {
+    // Warm start from this group's eigenvectors of the previous iteration
+    // (same positions, slightly changed pixels): G <- Vp^T G Vp, V <- Vp, so
+    // the Jacobi sweeps only have to remove a small off-diagonal residue.
+    {
+      double y[4][4];  // Y = G Vp, 4x4 block per thread, into V's buffer
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) y[i][j] = 0.0;
+      for (int k = 0; k < KMAX; ++k) {
+        const double2 v01 = *reinterpret_cast<const double2*>(vc + k * KMAX + 4 * bj);
+        const double2 v23 = *reinterpret_cast<const double2*>(vc + k * KMAX + 4 * bj + 2);
+        const double vv[4] = {v01.x, v01.y, v23.x, v23.y};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double gk = G[(4 * bi + i) * LD + k];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) y[i][j] = fma(gk, vv[j], y[i][j]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) V[(4 * bi + i) * LD + 4 * bj + j] = y[i][j];
+    }
+    __syncthreads();
+    {
+      double z[4][4];  // G' = Vp^T Y
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) z[i][j] = 0.0;
+      for (int k = 0; k < KMAX; ++k) {
+        const double2 v01 = *reinterpret_cast<const double2*>(vc + k * KMAX + 4 * bi);
+        const double2 v23 = *reinterpret_cast<const double2*>(vc + k * KMAX + 4 * bi + 2);
+        const double vv[4] = {v01.x, v01.y, v23.x, v23.y};
+        const double2 y01 = *reinterpret_cast<const double2*>(&V[k * LD + 4 * bj]);
+        const double2 y23 = *reinterpret_cast<const double2*>(&V[k * LD + 4 * bj + 2]);
+        const double yy[4] = {y01.x, y01.y, y23.x, y23.y};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) z[i][j] = fma(vv[i], yy[j], z[i][j]);
+      }
+      __syncthreads();
+      // symmetrise (the product is symmetric up to rounding) and reload Vp
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) G[(4 * bi + i) * LD + 4 * bj + j] = z[i][j];
+      for (int t = tid; t < KMAX * KMAX; t += THREADS) {
+        const int i = t >> 6, j = t & 63;
+        V[i * LD + j] = vc[t];
+      }
+    }
+    __syncthreads();
+    for (int t = tid; t < KMAX * KMAX; t += THREADS) {
+      const int i = t >> 6, j = t & 63;
+      if (i < j) {
+        const double v = 0.5 * (G[i * LD + j] + G[j * LD + i]);
+        G[i * LD + j] = v;
+        G[j * LD + i] = v;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    double tr = 0.0;
+    for (int i = 0; i < K; ++i) tr += fabs(G[i * LD + i]);
+    s_tiny = 1e-17 * tr;
+  }
+  __syncthreads();
+  const double tiny = s_tiny;
 
-  // ---- parallel cyclic Jacobi (round-robin tournament over Ke indices) ----
-  const int npairs = Ke / 2;
+  // ---- parallel cyclic Jacobi: 32 disjoint rotations per round (circle
+  // schedule over 64 indices); 8 threads per pair, 2 barriers per round.
+  // A rotation is skipped once |g_pq| is at rounding level relative to its
+  // diagonal pair (or to 1e-17 trace); stop after a sweep without rotations.
+  const int pk = tid >> 3, l = tid & 7;
   for (int sweep = 0; sweep < MAX_SWEEPS; ++sweep) {
-    for (int round = 0; round < Ke - 1; ++round) {
-      if (tid < npairs) {
-        // tournament: index 0 fixed, others rotate
-        auto slot = [&](int s) { return s == 0 ? 0 : 1 + (s - 1 + round) % (Ke - 1); };
-        int p = slot(tid), q = slot(Ke - 1 - tid);
-        if (p > q) {
-          const int t = p;
-          p = q;
-          q = t;
+    if (tid == 0) s_flag[(sweep + 1) & 1] = 0;
+    for (int round = 0; round < KMAX - 1; ++round) {
+      int p = 0, q;
+      if (pk != 0) {
+        p = 1 + (pk - 1 + round);
+        if (p > KMAX - 1) p -= KMAX - 1;
+      }
+      q = 1 + (KMAX - 2 - pk + round);
+      if (q > KMAX - 1) q -= KMAX - 1;
+      if (p > q) {
+        const int t = p;
+        p = q;
+        q = t;
+      }
+      const double app = G[p * LD + p], aqq = G[q * LD + q], apq = G[p * LD + q];
+      __syncwarp();
+      const bool rot = fabs(apq) > fmax(1e-15 * sqrt(fabs(app * aqq)), tiny);
+      double c = 1.0, s = 0.0;
+      if (rot) {
+        const double tau = (aqq - app) / (2.0 * apq);
+        const double t = fabs(tau) > 1e150
+                             ? 0.5 / tau
+                             : (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+        c = 1.0 / sqrt(1.0 + t * t);
+        s = t * c;
+        if (l == 0) s_flag[sweep & 1] = 1;
+        // rows p, q: G <- J^T G (all loads issued before any store)
+        double gp[KMAX / 8], gq[KMAX / 8];
+#pragma unroll
+        for (int i = 0; i < KMAX / 8; ++i) {
+          gp[i] = G[p * LD + l + 8 * i];
+          gq[i] = G[q * LD + l + 8 * i];
         }
-        double c = 1.0, s = 0.0;
-        if (q < K) {
-          const double app = G[p * LD + p], aqq = G[q * LD + q], apq = G[p * LD + q];
-          if (apq != 0.0) {
-            const double tau = (aqq - app) / (2.0 * apq);
-            double t;
-            if (fabs(tau) > 1e150) {
-              t = 0.5 / tau;
-            } else {
-              t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-            }
-            c = 1.0 / sqrt(1.0 + t * t);
-            s = t * c;
-          }
+#pragma unroll
+        for (int i = 0; i < KMAX / 8; ++i) {
+          G[p * LD + l + 8 * i] = c * gp[i] - s * gq[i];
+          G[q * LD + l + 8 * i] = s * gp[i] + c * gq[i];
         }
-        pair_p[tid] = p;
-        pair_q[tid] = q;
-        cs_c[tid] = c;
-        cs_s[tid] = s;
       }
       __syncthreads();
-      // rows: G <- J^T G
-      for (int t = tid; t < npairs * K; t += THREADS) {
-        const int k = t / K, j = t % K;
-        const double s = cs_s[k];
-        if (s == 0.0) continue;
-        const double c = cs_c[k];
-        const int p = pair_p[k], q = pair_q[k];
-        const double gp = G[p * LD + j], gq = G[q * LD + j];
-        G[p * LD + j] = c * gp - s * gq;
-        G[q * LD + j] = s * gp + c * gq;
-      }
-      __syncthreads();
-      // columns: G <- G J, V <- V J
-      for (int t = tid; t < 2 * npairs * K; t += THREADS) {
-        const int which = t / (npairs * K);
-        const int u = t % (npairs * K);
-        const int k = u / K, i = u % K;
-        const double s = cs_s[k];
-        if (s == 0.0) continue;
-        const double c = cs_c[k];
-        const int p = pair_p[k], q = pair_q[k];
-        double* Mx = which ? V : G;
-        const double xp = Mx[i * LD + p], xq = Mx[i * LD + q];
-        Mx[i * LD + p] = c * xp - s * xq;
-        Mx[i * LD + q] = s * xp + c * xq;
+      if (rot) {
+        // columns p, q: G <- G J, V <- V J
+        double gp[KMAX / 8], gq[KMAX / 8], vp[KMAX / 8], vq[KMAX / 8];
+#pragma unroll
+        for (int i = 0; i < KMAX / 8; ++i) {
+          const int r = l + 8 * i;
+          gp[i] = G[r * LD + p];
+          gq[i] = G[r * LD + q];
+          vp[i] = V[r * LD + p];
+          vq[i] = V[r * LD + q];
+        }
+#pragma unroll
+        for (int i = 0; i < KMAX / 8; ++i) {
+          const int r = l + 8 * i;
+          G[r * LD + p] = c * gp[i] - s * gq[i];
+          G[r * LD + q] = s * gp[i] + c * gq[i];
+          V[r * LD + p] = c * vp[i] - s * vq[i];
+          V[r * LD + q] = s * vp[i] + c * vq[i];
+        }
       }
       __syncthreads();
     }
-    // convergence: off-diagonal mass vs total
-    double off = 0.0, tot = 0.0;
-    for (int t = tid; t < K * K; t += THREADS) {
-      const int i = t / K, j = t % K;
-      const double v = G[i * LD + j];
-      tot += v * v;
-      if (i != j) off += v * v;
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      off += __shfl_xor_sync(0xffffffffu, off, o);
-      tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    }
-    if ((tid & 31) == 0) {
-      red[tid >> 5][0] = off;
-      red[tid >> 5][1] = tot;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      double o = 0.0, s = 0.0;
-      for (int w = 0; w < THREADS / 32; ++w) {
-        o += red[w][0];
-        s += red[w][1];
-      }
-      s_stop = (o <= 1e-30 * s) || s == 0.0;
-    }
-    __syncthreads();
-    if (s_stop) break;
+    if (!s_flag[sweep & 1]) break;
+  }
+
+  if (vc) {
+    for (int t = tid; t < KMAX * KMAX; t += THREADS) vc[t] = V[(t >> 6) * LD + (t & 63)];
   }
 
   // ---- shrinkage weights (lowrank.py:58-64) ----
-  if (tid < K) {
-    const double lam = G[tid * LD + tid];
-    const double s = sqrt(fmax(lam, 0.0));
-    double w;
-    if (a.uniform_weight >= 0.0) {
-      w = a.uniform_weight;
-    } else {
-      const double sig_hat = sqrt(fmax(s * s - K * a.sigma * a.sigma, 0.0));
-      w = a.c_weight * sqrt((double)K) * a.sigma * a.sigma / (sig_hat + a.eps);
+  if (tid < KMAX) {
+    double r = 0.0;
+    if (tid < K) {
+      const double lam = G[tid * LD + tid];
+      const double s = sqrt(fmax(lam, 0.0));
+      double w;
+      if (a.uniform_weight >= 0.0) {
+        w = a.uniform_weight;
+      } else {
+        const double sig_hat = sqrt(fmax(s * s - K * a.sigma * a.sigma, 0.0));
+        w = a.c_weight * sqrt((double)K) * a.sigma * a.sigma / (sig_hat + a.eps);
+      }
+      const double f = fmax(s - w, 0.0);
+      r = s > 0.0 ? f / s : 0.0;
     }
-    const double f = fmax(s - w, 0.0);
-    ratio[tid] = s > 0.0 ? f / s : 0.0;
+    ratio[tid] = r;
   }
   __syncthreads();
-  // Wm = V diag(ratio) V^T into G
-  for (int t = tid; t < K * K; t += THREADS) {
-    const int i = t / K, j = t % K;
-    double v = 0.0;
-    for (int k = 0; k < K; ++k) v = fma(V[i * LD + k] * ratio[k], V[j * LD + k], v);
-    G[i * LD + j] = v;
+  // Wm = V diag(ratio) V^T into G (4x4 block per thread)
+  {
+    double o[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[i][j] = 0.0;
+    for (int k = 0; k < KMAX; ++k) {
+      const double rk = ratio[k];
+      if (rk == 0.0) continue;
+      double x[4], y[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        x[i] = V[(4 * bi + i) * LD + k] * rk;
+        y[i] = V[(4 * bj + i) * LD + k];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[i][j] = fma(x[i], y[j], o[i][j]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) G[(4 * bi + i) * LD + 4 * bj + j] = o[i][j];
   }
   __syncthreads();
 
-  // ---- out = M Wm, row tiles; thread -> (row, 8 consecutive columns) ----
-  const int cb = tid % 8, rr = tid / 8;  // 8 column blocks x 32 rows
-  for (int r0 = 0; r0 < m; r0 += ROWS) {
-    for (int t = tid; t < ROWS * KMAX; t += THREADS) {
-      const int r2 = t / KMAX, j = t % KMAX;
-      T[t] = (r0 + r2 < m && j < K) ? load_m<FROM_IMAGE>(a, g, r0 + r2, j) : 0.0;
-    }
+  // ---- out = M Wm over 64-row tiles (in V's space); 4 rows x 4 cols / thread
+  // thread -> rows {r16 + 16u} x columns {4 cq .. 4 cq + 3}: lanes of a half
+  // warp run down consecutive rows, so the scatter atomics coalesce.
+  double* R = V;  // 64 x TS row tile
+  const int r16 = tid & 15, cq = tid >> 4;
+  for (int r0 = 0; r0 < m; r0 += 64) {
+    bool dummy = false;
+    fill(R, r0, 64, dummy);
     __syncthreads();
-    const int r = r0 + rr;
-    if (r < m) {
-      double o[8];
+    double o[4][4];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) o[k] = 0.0;
-      for (int i = 0; i < K; ++i) {
-        const double mv = T[rr * KMAX + i];
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int k = 0; k < 8; ++k) o[k] = fma(mv, G[i * LD + cb * 8 + k], o[k]);
-      }
+      for (int j = 0; j < 4; ++j) o[i][j] = 0.0;
+    for (int i = 0; i < K; ++i) {
+      double mv[4];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int j = cb * 8 + k;
+      for (int u = 0; u < 4; ++u) mv[u] = R[(r16 + 16 * u) * TS + i];
+      const double2 w01 = *reinterpret_cast<const double2*>(&G[i * LD + 4 * cq]);
+      const double2 w23 = *reinterpret_cast<const double2*>(&G[i * LD + 4 * cq + 2]);
+      const double wv[4] = {w01.x, w01.y, w23.x, w23.y};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) o[u][v] = fma(mv[u], wv[v], o[u][v]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = r0 + r16 + 16 * u;
+      if (r >= m) break;
+      const int64_t off = (int64_t)(r / PC) * rs + (r % PC);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int j = 4 * cq + v;
         if (j >= K) break;
         if constexpr (FROM_IMAGE) {
-          const int32_t* q = a.pos + ((size_t)g * K + j) * 2;
-          const int PC = a.P * a.C;
-          const int prow = q[0] + r / PC;
-          const int pcol = q[1] + (r / a.C) % a.P;
-          const int64_t idx = ((int64_t)prow * a.W + pcol) * a.C + (r % a.C);
-          const long long v = __double2ll_rn(o[k] * a.scale);
-          atomicAdd(reinterpret_cast<unsigned long long*>(a.acc + idx), (unsigned long long)v);
+          const long long val = __double2ll_rn(o[u][v] * a.scale);
+          atomicAdd(reinterpret_cast<unsigned long long*>(a.acc + cbase[j] + off),
+                    (unsigned long long)val);
         } else {
-          a.out[((size_t)g * K + j) * m + r] = o[k];
+          a.out[cbase[j] + off] = o[u][v];
         }
       }
     }
@@ -359,7 +482,7 @@ static int blocks_for(int64_t n, int threads = 256) {
 }
 
 static size_t wnnm_smem() {
-  return (size_t)(2 * wn::KMAX * wn::LD + wn::ROWS * wn::KMAX) * sizeof(double);
+  return (size_t)(2 * wn::KMAX * wn::LD + wn::ROWS * wn::TS) * sizeof(double);
 }
 
 template <bool FROM_IMAGE>
@@ -403,7 +526,8 @@ extern "C" int glr_wnnm(const double* groups_d, int G, int m, int K, double sigm
 extern "C" int glr_wnnm_scatter(const double* x_d, int H, int W, int C, int P,
                                 const int32_t* positions_d, int n_max, const int32_t* n_dev_d,
                                 int K, double sigma, double c_weight, double eps, int frac_bits,
-                                int64_t* acc_d, void* ws_d, size_t ws_bytes, void* stream) {
+                                int64_t* acc_d, double* vcache_d, int warm, void* ws_d,
+                                size_t ws_bytes, void* stream) {
   GLR_REQUIRE(K >= 1 && K <= wn::KMAX, GLR_ERR_UNSUPPORTED, "wnnm: K=%d outside [1, %d]", K,
               wn::KMAX);
   GLR_REQUIRE(P >= 1 && P <= H && P <= W, GLR_ERR_INVALID, "wnnm_scatter: bad patch size");
@@ -426,6 +550,8 @@ extern "C" int glr_wnnm_scatter(const double* x_d, int H, int W, int C, int P,
   a.uniform_weight = -1.0;
   a.acc = acc_d;
   a.scale = ldexp(1.0, frac_bits);
+  a.vcache = vcache_d;
+  a.warm = warm;
   return launch_wnnm<true>(a, n_max, (cudaStream_t)stream);
 }
 

@@ -146,9 +146,24 @@ class GlrEngine:
         self.heat_chunk = max(1, min(self.max_anchors, heat_budget_bytes // (2 * self.stride)))
         self.heat = D.empty((self.heat_chunk, self.stride), t.int16)
         self.ws_heat = D.empty((N.query("glr_heat_workspace", c, p, self.heat_chunk),), t.uint8)
+        # per-group Jacobi eigenvectors, warm start between refreshes
+        self.vcache = D.empty((self.max_anchors, KMAX, KMAX), t.float64)
+        self.warm = False
+        self.timing = None  # list of (name, start, end) CUDA events when profiling
         self.n = 0          # anchors in the current match state (all ranks)
         self.lo = self.hi = 0
         self.has_positions = False
+
+    def _ev(self):
+        if self.timing is None:
+            return None
+        e = D.torch().cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def _log(self, name, start):
+        if start is not None:
+            self.timing.append((name, start, self._ev()))
 
     # -- refresh: solvers.py:154-167 + 187-203 ---------------------------------
     def refresh(self, x_d) -> int:
@@ -170,6 +185,7 @@ class GlrEngine:
         self.n = n
         self.lo, self.hi = shard_bounds(n, self.rank, self.world)
         self.has_positions = True
+        self.warm = False
         if n == 0:
             return 0
         N.call("glr_sobel", x_d.data_ptr(), h, w, c, self.gh.data_ptr(), self.gv.data_ptr(), s)
@@ -187,12 +203,16 @@ class GlrEngine:
             b = min(self.hi, a + self.heat_chunk)
             nb = b - a
             anc = self.anchors[a:b]
+            e = self._ev()
             N.call("glr_heat_map", self.stack.data_ptr(), h, w, c, self.p, self.expand,
                    anc.data_ptr(), nb, None, self.heat.data_ptr(), self.ws_heat.data_ptr(),
                    self.ws_heat.numel(), s)
+            self._log(("heat_map", nb), e)
+            e = self._ev()
             N.call("glr_topk", self.heat.data_ptr(), nb, None, self.oh, self.ow, self.max_score,
                    anc.data_ptr(), self.k, self.mc.sep, self.positions[a:b].data_ptr(),
                    self.padded[a:b].data_ptr(), None, 0, s)
+            self._log(("topk", nb), e)
 
     def count(self):
         h, w, c = self.shape
@@ -209,6 +229,7 @@ class GlrEngine:
         self.n = n
         self.lo, self.hi = shard_bounds(n, self.rank, self.world)
         self.has_positions = True
+        self.warm = False
         if n:
             self.anchors[:n].copy_(D.i32(np.asarray(anchors).reshape(n, 2)))
             self.positions[:n].copy_(D.i32(np.asarray(positions).reshape(n, self.k, 2)))
@@ -224,10 +245,14 @@ class GlrEngine:
         self.acc.zero_()
         nloc = self.hi - self.lo
         if nloc > 0:
+            e = self._ev()
             N.call("glr_wnnm_scatter", x_d.data_ptr(), h, w, c, self.p,
                    self.positions[self.lo:self.hi].data_ptr(), nloc, None, self.k, float(sigma),
-                   float(self.c_weight), float(self.eps), self.frac, self.acc.data_ptr(), None, 0,
+                   float(self.c_weight), float(self.eps), self.frac, self.acc.data_ptr(),
+                   self.vcache[self.lo:self.hi].data_ptr(), 1 if self.warm else 0, None, 0,
                    D.stream())
+            self.warm = True
+            self._log(("wnnm_scatter", nloc), e)
         self._all_reduce(self.acc)
         return True
 

@@ -194,6 +194,80 @@ def regularize_dispatch(x: np.ndarray, cfg: SolverConfig, state: MatchState,
     return D.host(z)
 
 
+class GapRunner:
+    """A prepared device operator + GLR engine for repeated GAP solves: the
+    solver state is allocated once and a solve is `run(y_d)` on a device
+    measurement (bench.py times this; gap_solve wraps it)."""
+
+    def __init__(self, op, cfg: SolverConfig, process_group=None):
+        t = D.torch()
+        self.cfg = cfg
+        self.dop = DeviceOperator(op)
+        self.eng = GlrEngine(op.x_shape, cfg.match, cfg.peak, cfg.wnnm.c_weight, cfg.wnnm.eps,
+                             process_group=process_group)
+        self.xa = D.empty(self.dop.shape, t.float64)
+        self.xb = D.empty(self.dop.shape, t.float64)
+        self.resid_sq = D.zeros((cfg.max_iters,), t.float64)
+        self.sq = D.zeros((cfg.max_iters,), t.float64)
+        self.sq_ws = D.empty((N.query("glr_gap_workspace", 1, 1),), t.uint8)
+        self.events = None
+
+    def sq_err(self, x, ref_d, it):
+        n_el = int(np.prod(self.dop.shape))
+        N.call("glr_sq_err", x.data_ptr(), ref_d.data_ptr(), n_el, float(self.cfg.peak),
+               self.sq[it:it + 1].data_ptr(), self.sq_ws.data_ptr(), D.stream())
+
+    def run(self, y_d, positions_override=None, trace=None, on_iter=None, events=False):
+        """One full GAP-GLR solve (solvers.py:284-308) on device; returns the
+        final iterate (device tensor, before the final [0, peak] clip)."""
+        t = D.torch()
+        cfg, dop, eng = self.cfg, self.dop, self.eng
+        iters = cfg.max_iters
+        x, x_next = self.xa, self.xb
+        if cfg.init == "interp":
+            raise NotImplementedError("init='interp' (Gaussian inpainting start) is not on the "
+                                      "B200 path yet; use init='adjoint' (DESIGN.md)")
+        if cfg.init == "zero":
+            x.zero_()
+        else:
+            dop.adjoint(y_d, x)
+        eng.has_positions = False
+        lo, hi = -0.5 * cfg.peak, 1.5 * cfg.peak
+        self.events = ([[t.cuda.Event(enable_timing=True) for _ in range(4)]
+                        for _ in range(iters)] if events else None)
+        last = -1
+        refresh_no = 0
+        for it in range(iters):
+            ev = self.events[it] if events else None
+            if ev:
+                ev[0].record()
+            sigma = cfg.sigma_at(it)
+            if (not eng.has_positions) or it - last >= cfg.match_refresh_interval:
+                if positions_override is not None:
+                    anc, pos = positions_override[refresh_no]
+                    eng.set_positions(np.asarray(anc), np.asarray(pos))
+                else:
+                    eng.refresh(x)
+                if trace is not None:
+                    a, pz, _ = eng.positions_host()
+                    trace.append((a.tolist(), pz.tolist()))
+                last = it
+                refresh_no += 1
+            if ev:
+                ev[1].record()
+            has = eng.regularize(x, sigma)
+            if ev:
+                ev[2].record()
+            dop.gap_update(eng.acc if has else None, eng.cnt if has else None, eng.frac, x, y_d,
+                           lo, hi, x_next, self.resid_sq[it:it + 1], eng.gap_ws)
+            if ev:
+                ev[3].record()
+            x, x_next = x_next, x
+            if on_iter is not None:
+                on_iter(it, x)
+        return x
+
+
 def gap_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = None,
               process_group=None, positions_override=None, trace=None):
     """solvers.py:284-308 — regularize, then project onto the measurement-
@@ -211,56 +285,24 @@ def gap_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = Non
     t = D.torch()
     t_start = time.perf_counter()
     report = ReconReport()
-    dop = DeviceOperator(op)
-    eng = GlrEngine(op.x_shape, cfg.match, cfg.peak, cfg.wnnm.c_weight, cfg.wnnm.eps,
-                    process_group=process_group)
+    runner = GapRunner(op, cfg, process_group=process_group)
+    dop = runner.dop
     y_d = dop.upload_y(y)
-    x = _init_device(dop, y_d, cfg)
-    x_next = D.empty(dop.shape, t.float64)
     iters = cfg.max_iters
-    resid_sq = D.zeros((iters,), t.float64)
     ref_d = D.f64(ref) if ref is not None else None
-    sq = D.zeros((iters,), t.float64) if ref is not None else None
-    sq_ws = D.empty((N.query("glr_gap_workspace", 1, 1),), t.uint8) if ref is not None else None
-    lo, hi = -0.5 * cfg.peak, 1.5 * cfg.peak
-    ev = [[t.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(iters)]
-    last = -1
-    refresh_no = 0
-    refreshed = []
     ssims = []
-    for it in range(iters):
-        e0, e1, e2, e3 = ev[it]
-        e0.record()
-        sigma = cfg.sigma_at(it)
-        is_refresh = (not eng.has_positions) or it - last >= cfg.match_refresh_interval
-        if is_refresh:
-            if positions_override is not None:
-                anc, pos = positions_override[refresh_no]
-                eng.set_positions(np.asarray(anc), np.asarray(pos))
-            else:
-                eng.refresh(x)
-            if trace is not None:
-                a, pz, _ = eng.positions_host()
-                trace.append((a.tolist(), pz.tolist()))
-            last = it
-            refresh_no += 1
-        refreshed.append(is_refresh)
-        e1.record()
-        has = eng.regularize(x, sigma)
-        e2.record()
-        dop.gap_update(eng.acc if has else None, eng.cnt if has else None, eng.frac, x, y_d,
-                       lo, hi, x_next, resid_sq[it:it + 1], eng.gap_ws)
-        e3.record()
-        x, x_next = x_next, x
+
+    def on_iter(it, x):
         if ref_d is not None:
-            n_el = int(np.prod(dop.shape))
-            N.call("glr_sq_err", x.data_ptr(), ref_d.data_ptr(), n_el, float(cfg.peak),
-                   sq[it:it + 1].data_ptr(), sq_ws.data_ptr(), D.stream())
-            xc = np.clip(D.host(x), 0.0, cfg.peak)
-            ssims.append(ssim(ref, xc, cfg.peak))
+            runner.sq_err(x, ref_d, it)
+            ssims.append(ssim(ref, np.clip(D.host(x), 0.0, cfg.peak), cfg.peak))
+
+    x = runner.run(y_d, positions_override=positions_override, trace=trace,
+                   on_iter=on_iter, events=True)
     t.cuda.synchronize()
-    res = np.sqrt(D.host(resid_sq)).tolist()
-    sqh = D.host(sq) if sq is not None else None
+    res = np.sqrt(D.host(runner.resid_sq)).tolist()
+    sqh = D.host(runner.sq) if ref_d is not None else None
+    ev = runner.events
     for it in range(iters):
         e0, e1, e2, e3 = ev[it]
         row = {"iteration": it, "residual": float(res[it]),
@@ -277,7 +319,7 @@ def gap_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = Non
     y_norm = float(np.linalg.norm(y.ravel()))
     for k in range(21, iters + 1):
         _check_divergence(res[:k], y_norm)
-    out = D.host(x)
+    out = D.host(x).copy()
     if dop.clip:
         out = np.clip(out, 0.0, cfg.peak)
     return out, report

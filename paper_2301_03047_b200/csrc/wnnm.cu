@@ -66,10 +66,10 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
   extern __shared__ __align__(16) double sm[];
   double* G = sm;                 // KMAX x LD (Gram, then Wm)
   double* V = G + KMAX * LD;      // KMAX x LD (eigenvectors, then row tiles)
-  double* T = V + KMAX * LD;      // ROWS x KMAX tile of M
+  double* T = V + KMAX * LD;      // 2 x ROWS x TS double-buffered tiles of M
   __shared__ double ratio[KMAX];
   __shared__ double s_tiny;
-  __shared__ int s_flag[2], s_bad;
+  __shared__ int s_flag[2];
 
   const int g = blockIdx.x;
   const int N = a.n_dev ? min(*a.n_dev, a.n_max) : a.n_max;
@@ -98,41 +98,52 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
     cbase[tid] = b;
   }
   __syncthreads();
-  // coalesced tile fill: warp w loads columns w, w+8, ..., lanes run down rows
-  auto fill = [&](double* Tt, int r0, int R, bool& bad) {
+  // Asynchronous, coalesced tile fill (cp.async, no register staging): warp w
+  // takes columns w, w+8, ...; lanes run down consecutive rows, which are
+  // contiguous in the image within one patch row. Padding stays zero.
+  auto fill = [&](double* Tt, int r0, int R) {
     for (int rr = lane; rr < R; rr += 32) {
       const int r = r0 + rr;
       const bool rok = r < m;
       const int64_t off = rok ? (int64_t)(r / PC) * rs + (r % PC) : 0;
 #pragma unroll 4
       for (int j = warp; j < KMAX; j += THREADS / 32) {
-        double v = 0.0;
-        if (rok && j < K) v = src[cbase[j] + off];
-        bad |= !isfinite(v);
-        Tt[rr * TS + j] = v;
+        if (rok && j < K)
+          cp_async8(&Tt[rr * TS + j], src + cbase[j] + off);
+        else
+          Tt[rr * TS + j] = 0.0;
       }
     }
+    cp_async_commit();
   };
 
-  // ---- Gram G = M^T M (K padded to 64 with zero columns); 4x4 block per thread
+  // ---- Gram G = M^T M (K padded to 64 with zero columns), double-buffered
+  // row tiles; thread (bi, bj) owns G[bi + 16i][bj + 16j], i, j < 4, so every
+  // shared load of a warp is a broadcast or one 128-byte wavefront.
   const int bi = tid >> 4, bj = tid & 15;
   double acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-  bool bad = false;
-  for (int r0 = 0; r0 < m; r0 += ROWS) {
-    fill(T, r0, ROWS, bad);
+  const int ntiles = (m + ROWS - 1) / ROWS;
+  fill(T, 0, ROWS);
+  for (int tt = 0; tt < ntiles; ++tt) {
+    if (tt + 1 < ntiles)
+      fill(T + ((tt + 1) & 1) * ROWS * TS, (tt + 1) * ROWS, ROWS);
+    else
+      cp_async_commit();
+    cp_async_wait<1>();
     __syncthreads();
-    const int rmax = min(ROWS, m - r0);
+    const double* Tc = T + (tt & 1) * ROWS * TS;
+    const int rmax = min(ROWS, m - tt * ROWS);
     for (int rr = 0; rr < rmax; ++rr) {
-      const double2 x01 = *reinterpret_cast<const double2*>(&T[rr * TS + 4 * bi]);
-      const double2 x23 = *reinterpret_cast<const double2*>(&T[rr * TS + 4 * bi + 2]);
-      const double2 y01 = *reinterpret_cast<const double2*>(&T[rr * TS + 4 * bj]);
-      const double2 y23 = *reinterpret_cast<const double2*>(&T[rr * TS + 4 * bj + 2]);
-      const double x[4] = {x01.x, x01.y, x23.x, x23.y};
-      const double y[4] = {y01.x, y01.y, y23.x, y23.y};
+      double x[4], y[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        x[k] = Tc[rr * TS + bi + 16 * k];
+        y[k] = Tc[rr * TS + bj + 16 * k];
+      }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -140,16 +151,11 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
     }
     __syncthreads();
   }
-  if (tid == 0) {
-    s_bad = 0;
-    s_flag[0] = s_flag[1] = 0;
-  }
-  __syncthreads();
-  if (bad) s_bad = 1;
+  if (tid == 0) s_flag[0] = s_flag[1] = 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) G[(4 * bi + i) * LD + 4 * bj + j] = acc[i][j];
+    for (int j = 0; j < 4; ++j) G[(bi + 16 * i) * LD + bj + 16 * j] = acc[i][j];
   double* vc = a.vcache ? a.vcache + (size_t)g * KMAX * KMAX : nullptr;
   if (!(vc && a.warm)) {
     for (int t = tid; t < KMAX * KMAX; t += THREADS) {
@@ -158,10 +164,6 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
     }
   }
   __syncthreads();
-  if (s_bad) {
-    if (tid == 0 && a.nonfinite) atomicExch(a.nonfinite, 1);
-    return;
-  }
   if (vc && a.warm) {
     // Warm start from this group's eigenvectors of the previous iteration
     // (same positions, slightly changed pixels): G <- Vp^T G Vp, V <- Vp, so
@@ -363,12 +365,19 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
   // ---- out = M Wm over 64-row tiles (in V's space); 4 rows x 4 cols / thread
   // thread -> rows {r16 + 16u} x columns {4 cq .. 4 cq + 3}: lanes of a half
   // warp run down consecutive rows, so the scatter atomics coalesce.
-  double* R = V;  // 64 x TS row tile
+  // 64-row tiles, double-buffered between V's space and the two T halves.
   const int r16 = tid & 15, cq = tid >> 4;
-  for (int r0 = 0; r0 < m; r0 += 64) {
-    bool dummy = false;
-    fill(R, r0, 64, dummy);
+  const int napply = (m + 63) / 64;
+  fill(V, 0, 64);
+  for (int tt = 0; tt < napply; ++tt) {
+    const int r0 = tt * 64;
+    if (tt + 1 < napply)
+      fill((tt & 1) ? V : T, r0 + 64, 64);
+    else
+      cp_async_commit();
+    cp_async_wait<1>();
     __syncthreads();
+    const double* R = (tt & 1) ? T : V;
     double o[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -482,7 +491,7 @@ static int blocks_for(int64_t n, int threads = 256) {
 }
 
 static size_t wnnm_smem() {
-  return (size_t)(2 * wn::KMAX * wn::LD + wn::ROWS * wn::TS) * sizeof(double);
+  return (size_t)(2 * wn::KMAX * wn::LD + 2 * wn::ROWS * wn::TS) * sizeof(double);
 }
 
 template <bool FROM_IMAGE>

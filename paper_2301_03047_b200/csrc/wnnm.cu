@@ -244,8 +244,10 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
   // A rotation is skipped once |g_pq| is at rounding level relative to its
   // diagonal pair (or to 1e-17 trace); stop after a sweep without rotations.
   const int pk = tid >> 3, l = tid & 7;
+  // s_flag[s & 1] records a rotation in sweep s; the flag of sweep s+1 is
+  // cleared after the first barrier of sweep s (all reads of it from the end
+  // of sweep s-1 are done by then, and it is next written in sweep s+1).
   for (int sweep = 0; sweep < MAX_SWEEPS; ++sweep) {
-    if (tid == 0) s_flag[(sweep + 1) & 1] = 0;
     for (int round = 0; round < KMAX - 1; ++round) {
       int p = 0, q;
       if (pk != 0) {
@@ -285,6 +287,7 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
         }
       }
       __syncthreads();
+      if (round == 0 && tid == 0) s_flag[(sweep + 1) & 1] = 0;
       if (rot) {
         // columns p, q: G <- G J, V <- V J
         double gp[KMAX / 8], gq[KMAX / 8], vp[KMAX / 8], vq[KMAX / 8];

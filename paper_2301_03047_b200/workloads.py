@@ -143,7 +143,11 @@ def make(name: str, seed: int = 0) -> Workload:
         z = scene[:, :, 0] + 1j * scene[:, :, 1]
         y = mask * (np.fft.fft2(z, norm="ortho")
                     + 0.005 * (rng.normal(size=(h, w)) + 1j * rng.normal(size=(h, w))))
-        mc = MatchConfig(patch_size=8, group_size=48, max_corners=2048, exemplar_stride=171)
+        # the piecewise-constant phantom yields a few hundred Shi-Tomasi corners;
+        # the reference's glr mode unions them with a uniform grid
+        # (solvers.py:165-167), here at interval 12 (exemplar_stride 4, 43 x 43
+        # anchors) for ~2048 exemplars in total
+        mc = MatchConfig(patch_size=8, group_size=48, max_corners=2048, exemplar_stride=4)
         return Workload(name, "fourier", scene, mask, y, 40, mc, 0.005)
     if name == "C4":
         h = w = 512

@@ -59,7 +59,8 @@ SIGNATURES: dict[str, tuple] = {
     "glr_wnnm_workspace": (sz, [i32, i32]),
     "glr_wnnm": (i32, [vp, i32, i32, i32, f64, f64, f64, f64, vp, vp, vp, sz, vp]),
     "glr_wnnm_scatter": (i32, [vp, i32, i32, i32, i32, vp, i32, vp, i32, f64, f64, f64, i32, vp,
-                               vp, i32, vp, sz, vp]),
+                               vp, i32, vp, vp, sz, vp]),
+    "glr_vcache_remap": (i32, [vp, i32, i32, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp]),
     "glr_scatter_count": (i32, [vp, i32, vp, i32, i32, i32, i32, vp, vp]),
     "glr_scatter_add_f64": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, vp, vp, vp]),
     "glr_scatter_fixed": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, vp]),
@@ -134,7 +135,7 @@ KERNELS_PER_CALL = {
     "glr_wnnm_scatter": 1, "glr_scatter_count": 1, "glr_scatter_fixed": 1,
     "glr_scatter_add_f64": 1, "glr_normalize": 1, "glr_masksum_forward": 1,
     "glr_masksum_adjoint": 1, "glr_gap_masksum": 2, "glr_fourier_forward": 4,
-    "glr_fourier_adjoint": 4, "glr_gap_fourier": 11, "glr_sq_err": 2,
+    "glr_fourier_adjoint": 4, "glr_gap_fourier": 11, "glr_sq_err": 2, "glr_vcache_remap": 3,
 }
 launch_count = 0
 

@@ -24,7 +24,8 @@ constexpr int THREADS = 256;
 constexpr int KMAX = 64;
 constexpr int LD = KMAX + 2;  // padded leading dimension of G / V / Wm (16-byte rows)
 constexpr int ROWS = 32;      // rows of M per tile
-constexpr int TS = KMAX + 2;  // row stride of the M tiles (16-byte rows, 2-way STS banks)
+constexpr int GRS = ROWS + 1;  // column stride of the Gram tiles (odd: conflict-free)
+constexpr int ARS = 64 + 1;    // column stride of the 64-row apply tiles
 constexpr int MAX_SWEEPS = 24;
 }  // namespace wn
 
@@ -44,20 +45,30 @@ struct WnnmArgs {
   double scale;  // 2^frac_bits
   int32_t* nonfinite;
   double* vcache;  // optional per-group eigenvector cache (n_max x 64 x 64)
-  int warm;        // start the Jacobi sweeps from vcache
+  int warm;        // 0 cold, 1 start every group from vcache, 2 only where warm_flags[g]
+  const uint8_t* warm_flags;
 };
 
-template <bool FROM_IMAGE>
-__device__ __forceinline__ double load_m(const WnnmArgs& a, int g, int r, int j) {
-  if constexpr (FROM_IMAGE) {
-    const int32_t* q = a.pos + ((size_t)g * a.K + j) * 2;
-    const int PC = a.P * a.C;
-    const int rr = q[0] + r / PC;
-    const int cc = q[1] + (r / a.C) % a.P;
-    return a.x[((int64_t)rr * a.W + cc) * a.C + (r % a.C)];
-  } else {
-    return a.groups[((size_t)g * a.K + j) * a.m + r];
-  }
+// Carry eigenvectors across a matching refresh: a new group whose anchor was
+// also an anchor before (and whose old group lived in this rank's old shard)
+// starts its Jacobi sweeps from the old group's eigenvectors.
+__global__ void anchor_map_kernel(const int32_t* __restrict__ anchors, int lo, int hi, int W,
+                                  int32_t* __restrict__ map, int set) {
+  for (int i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += gridDim.x * blockDim.x)
+    map[anchors[2 * i] * W + anchors[2 * i + 1]] = set ? i : -1;
+}
+
+__global__ void vcache_remap_kernel(const int32_t* __restrict__ new_anchors, int lo, int W,
+                                    const int32_t* __restrict__ map,
+                                    const double* __restrict__ vc_old, double* __restrict__ vc_new,
+                                    uint8_t* __restrict__ flags) {
+  const int g = lo + blockIdx.x;
+  const int old = map[new_anchors[2 * g] * W + new_anchors[2 * g + 1]];
+  if (threadIdx.x == 0) flags[g] = old >= 0 ? 1 : 0;
+  if (old < 0) return;
+  const double2* src = reinterpret_cast<const double2*>(vc_old + (size_t)old * 4096);
+  double2* dst = reinterpret_cast<double2*>(vc_new + (size_t)g * 4096);
+  for (int t = threadIdx.x; t < 2048; t += blockDim.x) dst[t] = src[t];
 }
 
 template <bool FROM_IMAGE>
@@ -69,7 +80,6 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
   double* T = V + KMAX * LD;      // 2 x ROWS x TS double-buffered tiles of M
   __shared__ double ratio[KMAX];
   __shared__ double s_tiny;
-  __shared__ int s_flag[2];
 
   const int g = blockIdx.x;
   const int N = a.n_dev ? min(*a.n_dev, a.n_max) : a.n_max;
@@ -101,7 +111,11 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
   // Asynchronous, coalesced tile fill (cp.async, no register staging): warp w
   // takes columns w, w+8, ...; lanes run down consecutive rows, which are
   // contiguous in the image within one patch row. Padding stays zero.
-  auto fill = [&](double* Tt, int r0, int R) {
+  // Tiles are column-major (element (rr, j) at Tt[j * RS + rr]) with an odd
+  // column stride RS, so both the fill (lanes along rr) and the compute
+  // loops (lanes along columns, or along rows within a column) hit
+  // distinct banks.
+  auto fill = [&](double* Tt, int r0, int R, int RS) {
     for (int rr = lane; rr < R; rr += 32) {
       const int r = r0 + rr;
       const bool rok = r < m;
@@ -109,62 +123,81 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
 #pragma unroll 4
       for (int j = warp; j < KMAX; j += THREADS / 32) {
         if (rok && j < K)
-          cp_async8(&Tt[rr * TS + j], src + cbase[j] + off);
+          cp_async8(&Tt[j * RS + rr], src + cbase[j] + off);
         else
-          Tt[rr * TS + j] = 0.0;
+          Tt[j * RS + rr] = 0.0;
       }
     }
     cp_async_commit();
   };
 
   // ---- Gram G = M^T M (K padded to 64 with zero columns), double-buffered
-  // row tiles; thread (bi, bj) owns G[bi + 16i][bj + 16j], i, j < 4, so every
-  // shared load of a warp is a broadcast or one 128-byte wavefront.
-  const int bi = tid >> 4, bj = tid & 15;
+  // row tiles. G is symmetric: the 136 threads t < 136 own the upper-triangle
+  // blocks (gi <= gj) of a 16 x 16 grid, block (gi, gj) = entries
+  // G[gi + 16i][gj + 16j], i, j < 4; warps 5-7 only help with the tile fills.
+  const int bi = tid >> 4, bj = tid & 15;  // square 4x4 blocks (later phases)
+  int gi = 0, gj = 0;
+  const bool gram_thread = tid < 136;
+  if (gram_thread) {
+    int rem = tid;
+    while (rem >= 16 - gi) {
+      rem -= 16 - gi;
+      ++gi;
+    }
+    gj = gi + rem;
+  }
   double acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
   const int ntiles = (m + ROWS - 1) / ROWS;
-  fill(T, 0, ROWS);
+  fill(T, 0, ROWS, GRS);
   for (int tt = 0; tt < ntiles; ++tt) {
     if (tt + 1 < ntiles)
-      fill(T + ((tt + 1) & 1) * ROWS * TS, (tt + 1) * ROWS, ROWS);
+      fill(T + ((tt + 1) & 1) * KMAX * GRS, (tt + 1) * ROWS, ROWS, GRS);
     else
       cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    const double* Tc = T + (tt & 1) * ROWS * TS;
+    const double* Tc = T + (tt & 1) * KMAX * GRS;
     const int rmax = min(ROWS, m - tt * ROWS);
-    for (int rr = 0; rr < rmax; ++rr) {
-      double x[4], y[4];
+    if (gram_thread) {
+#pragma unroll 4
+      for (int rr = 0; rr < rmax; ++rr) {
+        double x[4], y[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        x[k] = Tc[rr * TS + bi + 16 * k];
-        y[k] = Tc[rr * TS + bj + 16 * k];
+        for (int k = 0; k < 4; ++k) {
+          x[k] = Tc[(gi + 16 * k) * GRS + rr];
+          y[k] = Tc[(gj + 16 * k) * GRS + rr];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fma(x[i], y[j], acc[i][j]);
       }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(x[i], y[j], acc[i][j]);
     }
     __syncthreads();
   }
-  if (tid == 0) s_flag[0] = s_flag[1] = 0;
+  if (gram_thread) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) G[(bi + 16 * i) * LD + bj + 16 * j] = acc[i][j];
+      for (int j = 0; j < 4; ++j) {
+        G[(gi + 16 * i) * LD + gj + 16 * j] = acc[i][j];
+        G[(gj + 16 * j) * LD + gi + 16 * i] = acc[i][j];  // mirror (same value on gi == gj)
+      }
+  }
   double* vc = a.vcache ? a.vcache + (size_t)g * KMAX * KMAX : nullptr;
-  if (!(vc && a.warm)) {
+  const bool warm = vc && (a.warm == 1 || (a.warm == 2 && a.warm_flags[g]));
+  if (!warm) {
     for (int t = tid; t < KMAX * KMAX; t += THREADS) {
       const int i = t >> 6, j = t & 63;
       V[i * LD + j] = (i == j) ? 1.0 : 0.0;
     }
   }
   __syncthreads();
-  if (vc && a.warm) {
+  if (warm) {
     // Warm start from this group's eigenvectors of the previous iteration
     // (same positions, slightly changed pixels): G <- Vp^T G Vp, V <- Vp, so
     // the Jacobi sweeps only have to remove a small off-diagonal residue.
@@ -244,10 +277,19 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
   // A rotation is skipped once |g_pq| is at rounding level relative to its
   // diagonal pair (or to 1e-17 trace); stop after a sweep without rotations.
   const int pk = tid >> 3, l = tid & 7;
-  // s_flag[s & 1] records a rotation in sweep s; the flag of sweep s+1 is
-  // cleared after the first barrier of sweep s (all reads of it from the end
-  // of sweep s-1 are done by then, and it is next written in sweep s+1).
   for (int sweep = 0; sweep < MAX_SWEEPS; ++sweep) {
+    // A sweep changes G only if some pair passes the rotation test on the
+    // current G (otherwise no round rotates, by induction), so test all
+    // pairs up front and stop without paying for a no-op sweep.
+    bool need = false;
+    for (int t = tid; t < KMAX * KMAX; t += THREADS) {
+      const int i = t >> 6, j = t & 63;
+      if (i < j) {
+        const double apq = G[i * LD + j];
+        need |= fabs(apq) > fmax(1e-15 * sqrt(fabs(G[i * LD + i] * G[j * LD + j])), tiny);
+      }
+    }
+    if (!__syncthreads_or(need)) break;
     for (int round = 0; round < KMAX - 1; ++round) {
       int p = 0, q;
       if (pk != 0) {
@@ -272,7 +314,6 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
                              : (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
         c = 1.0 / sqrt(1.0 + t * t);
         s = t * c;
-        if (l == 0) s_flag[sweep & 1] = 1;
         // rows p, q: G <- J^T G (all loads issued before any store)
         double gp[KMAX / 8], gq[KMAX / 8];
 #pragma unroll
@@ -287,7 +328,6 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
         }
       }
       __syncthreads();
-      if (round == 0 && tid == 0) s_flag[(sweep + 1) & 1] = 0;
       if (rot) {
         // columns p, q: G <- G J, V <- V J
         double gp[KMAX / 8], gq[KMAX / 8], vp[KMAX / 8], vq[KMAX / 8];
@@ -310,7 +350,6 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
       }
       __syncthreads();
     }
-    if (!s_flag[sweep & 1]) break;
   }
 
   if (vc) {
@@ -371,11 +410,11 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
   // 64-row tiles, double-buffered between V's space and the two T halves.
   const int r16 = tid & 15, cq = tid >> 4;
   const int napply = (m + 63) / 64;
-  fill(V, 0, 64);
+  fill(V, 0, 64, ARS);
   for (int tt = 0; tt < napply; ++tt) {
     const int r0 = tt * 64;
     if (tt + 1 < napply)
-      fill((tt & 1) ? V : T, r0 + 64, 64);
+      fill((tt & 1) ? V : T, r0 + 64, 64, ARS);
     else
       cp_async_commit();
     cp_async_wait<1>();
@@ -386,10 +425,11 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) o[i][j] = 0.0;
+#pragma unroll 4
     for (int i = 0; i < K; ++i) {
       double mv[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) mv[u] = R[(r16 + 16 * u) * TS + i];
+      for (int u = 0; u < 4; ++u) mv[u] = R[i * ARS + r16 + 16 * u];
       const double2 w01 = *reinterpret_cast<const double2*>(&G[i * LD + 4 * cq]);
       const double2 w23 = *reinterpret_cast<const double2*>(&G[i * LD + 4 * cq + 2]);
       const double wv[4] = {w01.x, w01.y, w23.x, w23.y};
@@ -494,7 +534,8 @@ static int blocks_for(int64_t n, int threads = 256) {
 }
 
 static size_t wnnm_smem() {
-  return (size_t)(2 * wn::KMAX * wn::LD + 2 * wn::ROWS * wn::TS) * sizeof(double);
+  static_assert(2 * wn::GRS >= wn::ARS && wn::LD >= wn::ARS, "tile buffers");
+  return (size_t)(2 * wn::KMAX * wn::LD + 2 * wn::KMAX * wn::GRS) * sizeof(double);
 }
 
 template <bool FROM_IMAGE>
@@ -538,7 +579,8 @@ extern "C" int glr_wnnm(const double* groups_d, int G, int m, int K, double sigm
 extern "C" int glr_wnnm_scatter(const double* x_d, int H, int W, int C, int P,
                                 const int32_t* positions_d, int n_max, const int32_t* n_dev_d,
                                 int K, double sigma, double c_weight, double eps, int frac_bits,
-                                int64_t* acc_d, double* vcache_d, int warm, void* ws_d,
+                                int64_t* acc_d, double* vcache_d, int warm,
+                                const uint8_t* warm_flags_d, void* ws_d,
                                 size_t ws_bytes, void* stream) {
   GLR_REQUIRE(K >= 1 && K <= wn::KMAX, GLR_ERR_UNSUPPORTED, "wnnm: K=%d outside [1, %d]", K,
               wn::KMAX);
@@ -564,7 +606,32 @@ extern "C" int glr_wnnm_scatter(const double* x_d, int H, int W, int C, int P,
   a.scale = ldexp(1.0, frac_bits);
   a.vcache = vcache_d;
   a.warm = warm;
+  a.warm_flags = warm_flags_d;
+  GLR_REQUIRE(warm != 2 || warm_flags_d != nullptr, GLR_ERR_INVALID, "warm=2 needs warm flags");
   return launch_wnnm<true>(a, n_max, (cudaStream_t)stream);
+}
+
+extern "C" int glr_vcache_remap(const int32_t* old_anchors_d, int old_lo, int old_hi,
+                                const int32_t* new_anchors_d, int new_lo, int new_hi, int H,
+                                int W, const double* vc_old_d, double* vc_new_d,
+                                uint8_t* flags_d, int32_t* map_d, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (old_hi > old_lo) {
+    anchor_map_kernel<<<blocks_for(old_hi - old_lo), 256, 0, st>>>(old_anchors_d, old_lo, old_hi,
+                                                                  W, map_d, 1);
+    GLR_CUDA(cudaGetLastError());
+  }
+  if (new_hi > new_lo) {
+    vcache_remap_kernel<<<new_hi - new_lo, 256, 0, st>>>(new_anchors_d, new_lo, W, map_d,
+                                                        vc_old_d, vc_new_d, flags_d);
+    GLR_CUDA(cudaGetLastError());
+  }
+  if (old_hi > old_lo) {
+    anchor_map_kernel<<<blocks_for(old_hi - old_lo), 256, 0, st>>>(old_anchors_d, old_lo, old_hi,
+                                                                  W, map_d, 0);
+    GLR_CUDA(cudaGetLastError());
+  }
+  return GLR_OK;
 }
 
 extern "C" int glr_scatter_count(const int32_t* positions_d, int n_max, const int32_t* n_dev_d,

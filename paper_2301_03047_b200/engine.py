@@ -147,12 +147,24 @@ class GlrEngine:
         self.heat = D.empty((self.heat_chunk, self.stride), t.int16)
         self.ws_heat = D.empty((N.query("glr_heat_workspace", c, p, self.heat_chunk),), t.uint8)
         # per-group Jacobi eigenvectors, warm start between refreshes
-        self.vcache = D.empty((self.max_anchors, KMAX, KMAX), t.float64)
-        self.warm = False
+        # (double-buffered so a refresh can carry them over by anchor, see
+        # glr_vcache_remap); warm: 0 cold, 1 all groups, 2 per-group flags
+        self._vc = [D.empty((self.max_anchors, KMAX, KMAX), t.float64) for _ in range(2)]
+        self._vcur = 0
+        self.vcache_valid = False
+        self.warm_flags = D.zeros((self.max_anchors,), t.uint8)
+        self.anchor_map = D.empty((h * w,), t.int32).fill_(-1)
+        self._anc = [self.anchors, D.empty((self.max_anchors, 2), t.int32)]
+        self._acur = 0
+        self.warm = 0
         self.timing = None  # list of (name, start, end) CUDA events when profiling
         self.n = 0          # anchors in the current match state (all ranks)
         self.lo = self.hi = 0
         self.has_positions = False
+
+    @property
+    def vcache(self):
+        return self._vc[self._vcur]
 
     def _ev(self):
         if self.timing is None:
@@ -177,6 +189,9 @@ class GlrEngine:
         N.call("glr_corners", self.resp.data_ptr(), h, w, mc.max_corners, mc.nms,
                float(mc.corner_quality), self.corners.data_ptr(), self.n_corners.data_ptr(),
                self.ws_nms.data_ptr(), self.ws_nms.numel(), s)
+        old_anchors, old_n, old_lo, old_hi = self.anchors, self.n, self.lo, self.hi
+        self._acur ^= 1
+        self.anchors = self._anc[self._acur]
         N.call("glr_select_anchors", self.corners.data_ptr(), self.n_corners.data_ptr(),
                mc.max_corners, h, w, self.p, self.grid_interval, self.max_anchors,
                self.anchors.data_ptr(), self.tags.data_ptr(), self.n_anchors.data_ptr(),
@@ -185,7 +200,17 @@ class GlrEngine:
         self.n = n
         self.lo, self.hi = shard_bounds(n, self.rank, self.world)
         self.has_positions = True
-        self.warm = False
+        self.warm = 0
+        if n and old_n and self.vcache_valid:
+            # groups keeping their anchor start from their old eigenvectors
+            vc_old = self._vc[self._vcur]
+            self._vcur ^= 1
+            N.call("glr_vcache_remap", old_anchors.data_ptr(), old_lo, old_hi,
+                   self.anchors.data_ptr(), self.lo, self.hi, h, w, vc_old.data_ptr(),
+                   self.vcache.data_ptr(), self.warm_flags.data_ptr(),
+                   self.anchor_map.data_ptr(), s)
+            self.warm = 2
+        self.vcache_valid = False
         if n == 0:
             return 0
         N.call("glr_sobel", x_d.data_ptr(), h, w, c, self.gh.data_ptr(), self.gv.data_ptr(), s)
@@ -229,7 +254,8 @@ class GlrEngine:
         self.n = n
         self.lo, self.hi = shard_bounds(n, self.rank, self.world)
         self.has_positions = True
-        self.warm = False
+        self.warm = 0
+        self.vcache_valid = False
         if n:
             self.anchors[:n].copy_(D.i32(np.asarray(anchors).reshape(n, 2)))
             self.positions[:n].copy_(D.i32(np.asarray(positions).reshape(n, self.k, 2)))
@@ -249,9 +275,10 @@ class GlrEngine:
             N.call("glr_wnnm_scatter", x_d.data_ptr(), h, w, c, self.p,
                    self.positions[self.lo:self.hi].data_ptr(), nloc, None, self.k, float(sigma),
                    float(self.c_weight), float(self.eps), self.frac, self.acc.data_ptr(),
-                   self.vcache[self.lo:self.hi].data_ptr(), 1 if self.warm else 0, None, 0,
-                   D.stream())
-            self.warm = True
+                   self.vcache[self.lo:self.hi].data_ptr(), self.warm,
+                   self.warm_flags[self.lo:self.hi].data_ptr(), None, 0, D.stream())
+            self.warm = 1
+            self.vcache_valid = True
             self._log(("wnnm_scatter", nloc), e)
         self._all_reduce(self.acc)
         return True

@@ -21,8 +21,13 @@
 //     reference's row-major slice index, matching.py:177-178), rows padded
 //     to a multiple of 8 entries (glr_heat_stride) for 16-byte loads.
 //
-// Warp roles (128 threads): warp0.lane0 = TMA producer, warp1.lane0 = MMA
-// issuer, warp1 owns the TMEM allocation, all four warps run the epilogue.
+// Persistent, warp-specialised kernel (256 threads, one CTA per SM):
+//   warp 0 (one lane)  TMA producer, 4-stage smem ring (full/empty mbarriers);
+//   warp 1 (one lane)  tcgen05.mma issuer into one of two TMEM accumulators;
+//   warp 2             owns the 512-column TMEM allocation;
+//   warps 4-7          epilogue: tcgen05.ld -> u16 stores, then release the
+//                      accumulator, so tile i's epilogue overlaps tile i+1's
+//                      MMAs (accumulator handoff via tmem_full/tmem_empty).
 #include <cstdio>
 #include <cudaTypedefs.h>
 
@@ -36,11 +41,13 @@ constexpr int BN = 256;      // exemplars per tile (UMMA N)
 constexpr int BK = 128;      // bytes of K per stage (one 128B swizzle row)
 constexpr int UK = 32;       // K per tcgen05.mma kind::i8
 constexpr int STAGES = 4;
+constexpr int ACC = 2;       // TMEM accumulators (2 x 256 columns)
+constexpr int THREADS = 256;
 constexpr int A_BYTES = BM * BK;
 constexpr int B_BYTES = BN * BK;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr uint32_t TMEM_COLS = 256;
+constexpr uint32_t TMEM_COLS = 512;
 }  // namespace heat
 
 struct HeatGeom {
@@ -65,12 +72,12 @@ static HeatGeom heat_geom(int H, int W, int C, int P, int e) {
 }
 
 struct HeatParams {
-  int oh, ow, Mpad, n_max, n_tiles, m_tiles_per_row, S, kchunks, e;
+  int oh, ow, Mpad, n_max, m_tiles_per_row, S, kchunks, e;
   const int32_t* n_dev;
   uint16_t* heat;
 };
 
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(heat::THREADS, 1)
     heat_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB, HeatParams p) {
   using namespace heat;
@@ -81,17 +88,14 @@ __global__ void __launch_bounds__(128, 1)
   uint8_t* sB = smem + STAGES * A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* done = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + ACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + ACC);
 
-  const int n_tile = blockIdx.x % p.n_tiles;
-  const int m_tile = blockIdx.x / p.n_tiles;
-  const int n0 = n_tile * BN;
   const int N = p.n_dev ? min(*p.n_dev, p.n_max) : p.n_max;
-  if (n0 >= N) return;  // block-uniform, before any barrier
-  const int u = m_tile / p.m_tiles_per_row;
-  const int v0 = (m_tile % p.m_tiles_per_row) * BM;
-
+  const int n_tiles = (N + BN - 1) / BN;
+  const int total = p.oh * p.m_tiles_per_row * n_tiles;  // n fastest: CTAs share A tiles in L2
+  const int num_k = p.S * p.kchunks;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
@@ -100,75 +104,104 @@ __global__ void __launch_bounds__(128, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    for (int a = 0; a < ACC; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+    }
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
   }
-  if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
+  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int num_k = p.S * p.kchunks;
 
-  if (warp == 0 && lane == 0) {
-    // ---- TMA producer ----
-    for (int kb = 0; kb < num_k; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      if (kb >= STAGES) mbar_wait(&empty[s], ph ^ 1);
-      mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-      const int slab = kb / p.kchunks;
-      const int kc = kb - slab * p.kchunks;
-      tma_load_3d(sA + s * A_BYTES, &tmA, &full[s], kc * BK, v0, u + slab * p.e);
-      tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, n0);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---- MMA issuer ----
-    constexpr uint32_t idesc = idesc_u8_s32(BM, BN);
-    for (int kb = 0; kb < num_k; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      mbar_wait(&full[s], ph);
-      tc_fence_after();
-      const uint64_t ad = smem_desc_k_sw128(sA + s * A_BYTES);
-      const uint64_t bd = smem_desc_k_sw128(sB + s * B_BYTES);
-#pragma unroll
-      for (int k = 0; k < BK / UK; ++k) {
-        // advance the start address by k*32 bytes inside the 128B swizzle atom
-        umma_i8(tmem, ad + (uint64_t)((k * UK) >> 4), bd + (uint64_t)((k * UK) >> 4), idesc,
-                (kb | k) != 0);
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer ----
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int n0 = (t % n_tiles) * BN;
+        const int m_tile = t / n_tiles;
+        const int u = m_tile / p.m_tiles_per_row;
+        const int v0 = (m_tile % p.m_tiles_per_row) * BM;
+        for (int kb = 0; kb < num_k; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          if (it >= STAGES) mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+          const int slab = kb / p.kchunks;
+          const int kc = kb - slab * p.kchunks;
+          tma_load_3d(sA + s * A_BYTES, &tmA, &full[s], kc * BK, v0, u + slab * p.e);
+          tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, n0);
+        }
       }
-      umma_commit(&empty[s]);
     }
-    umma_commit(done);
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---- MMA issuer ----
+      constexpr uint32_t idesc = idesc_u8_s32(BM, BN);
+      int it = 0, lt = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+        const int acc = lt & 1, use = lt >> 1;
+        if (use > 0) mbar_wait(&tempty[acc], (use - 1) & 1);  // epilogue drained it
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < num_k; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint64_t ad = smem_desc_k_sw128(sA + s * A_BYTES);
+          const uint64_t bd = smem_desc_k_sw128(sB + s * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)  // +32 bytes inside the 128B swizzle atom
+            umma_i8(d, ad + (uint64_t)((k * UK) >> 4), bd + (uint64_t)((k * UK) >> 4), idesc,
+                    (kb | k) != 0);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---- epilogue: TMEM -> registers -> u16 exemplar-major rows ----
+    const int ew = warp - 4;  // TMEM lanes 32*ew .. 32*ew+31 (warp id % 4)
+    int lt = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+      const int acc = lt & 1, use = lt >> 1;
+      const int n0 = (t % n_tiles) * BN;
+      const int m_tile = t / n_tiles;
+      const int u = m_tile / p.m_tiles_per_row;
+      const int v = (m_tile % p.m_tiles_per_row) * BM + ew * 32 + lane;
+      mbar_wait(&tfull[acc], use & 1);
+      tc_fence_after();
+      const bool v_ok = v < p.ow;
+      uint16_t* out = p.heat + (size_t)u * p.ow + v;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * BN + c * 32), r);
+        tmem_ld_wait();
+        const int nb = n0 + c * 32;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int n = nb + j;
+          if (v_ok && n < N) out[(size_t)n * p.Mpad] = (uint16_t)r[j];
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
   }
   __syncwarp();
-
-  // ---- epilogue: TMEM -> registers -> u16 exemplar-major rows ----
-  mbar_wait(done, 0);
-  tc_fence_after();
-  const int v = v0 + warp * 32 + lane;
-  const bool v_ok = v < p.ow;
-  uint16_t* out = p.heat + (size_t)u * p.ow + v;
-#pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
-    uint32_t r[32];
-    tmem_ld_32x32b_x32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * 32), r);
-    tmem_ld_wait();
-    const int nb = n0 + c * 32;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int n = nb + j;
-      if (v_ok && n < N) out[(size_t)n * p.Mpad] = (uint16_t)r[j];
-    }
-  }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
+  if (warp == 2) tmem_dealloc<TMEM_COLS>(tmem);
 }
 
 // B operand: bmat[n][s*kchunks*BK + k'] = stack[r_n + s*e][c_n + k'/Ce][k' % Ce] for
@@ -300,7 +333,6 @@ extern "C" int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, 
   hp.ow = g.ow;
   hp.Mpad = (int)glr_heat_stride(H, W, P);
   hp.n_max = n_max;
-  hp.n_tiles = n_pad / heat::BN;
   hp.m_tiles_per_row = (int)cdiv(g.ow, heat::BM);
   hp.S = g.S;
   hp.kchunks = g.kchunks;
@@ -313,9 +345,12 @@ extern "C" int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, 
                                   heat::SMEM_BYTES));
     attr_set = true;
   }
-  int64_t grid = (int64_t)g.oh * hp.m_tiles_per_row * hp.n_tiles;
-  GLR_REQUIRE(grid < (1ll << 31), GLR_ERR_UNSUPPORTED, "heat_map: grid too large");
-  heat_gemm_kernel<<<(unsigned)grid, 128, heat::SMEM_BYTES, st>>>(tmA, tmB, hp);
+  const int64_t tiles = (int64_t)g.oh * hp.m_tiles_per_row * (n_pad / heat::BN);
+  GLR_REQUIRE(tiles < (1ll << 31), GLR_ERR_UNSUPPORTED, "heat_map: too many tiles");
+  int sms = kNumSMs;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);  // persistent: one CTA per SM
+  heat_gemm_kernel<<<grid, heat::THREADS, heat::SMEM_BYTES, st>>>(tmA, tmB, hp);
   GLR_CUDA(cudaGetLastError());
   return GLR_OK;
 }

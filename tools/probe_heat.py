@@ -32,12 +32,14 @@ def run(H, W, Cc, P, N, seed, dens=0.3):
     chk(lib.glr_stack_from_maps(C.c_void_p(dmaps.data_ptr()), H, W, Cc, e, C.c_void_p(stack.data_ptr()), None))
     danc = torch.from_numpy(anchors).cuda()
     oh, ow = H-P+1, W-P+1
-    heat = torch.full((N, oh*ow), 0xFFFF, dtype=torch.int32, device='cuda').to(torch.uint16) if False else torch.zeros((N, oh*ow), dtype=torch.int16, device='cuda')
+    lib.glr_heat_stride.restype = C.c_int64
+    stride = lib.glr_heat_stride(H, W, P)
+    heat = torch.zeros((N, stride), dtype=torch.int16, device='cuda')
     ws = torch.empty(ws_b, dtype=torch.uint8, device='cuda')
     lib.glr_heat_map.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
     chk(lib.glr_heat_map(stack.data_ptr(), H, W, Cc, P, e, danc.data_ptr(), N, None, heat.data_ptr(), ws.data_ptr(), ws_b, None))
     torch.cuda.synchronize()
-    got = heat.cpu().numpy().view(np.uint16).reshape(N, oh, ow).astype(np.int64)
+    got = heat.cpu().numpy().view(np.uint16)[:, :oh*ow].reshape(N, oh, ow).astype(np.int64)
     ref = heat_np(maps, anchors, P)
     ok = np.array_equal(got, ref)
     print(f"H={H} W={W} C={Cc} P={P} N={N} e={e}: {'OK' if ok else 'MISMATCH'}", flush=True)
@@ -58,7 +60,8 @@ e = lib.glr_heat_expand_factor(Cc, P)
 stack = torch.from_numpy((rng.random(H*W*4*Cc*e) < 0.2).astype(np.uint8)).cuda()
 anchors = torch.from_numpy(np.stack([rng.integers(0, H-P+1, N), rng.integers(0, W-P+1, N)], 1).astype(np.int32)).cuda()
 ws_b = lib.glr_heat_workspace(Cc, P, N); ws = torch.empty(ws_b, dtype=torch.uint8, device='cuda')
-heat = torch.empty((N, (H-P+1)*(W-P+1)), dtype=torch.int16, device='cuda')
+lib.glr_heat_stride.restype = C.c_int64
+heat = torch.empty((N, lib.glr_heat_stride(H, W, P)), dtype=torch.int16, device='cuda')
 for it in range(4):
     s = torch.cuda.Event(enable_timing=True); t = torch.cuda.Event(enable_timing=True)
     s.record()

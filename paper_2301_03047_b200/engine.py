@@ -284,7 +284,9 @@ class GlrEngine:
         return True
 
     def _all_reduce(self, t):
-        if self.pg is not None and self.world > 1:
+        # with a process group the collective always runs (also at world 1, so
+        # the sharded path is the one exercised when launched under torchrun)
+        if self.pg is not None:
             import torch.distributed as dist
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.pg)
 

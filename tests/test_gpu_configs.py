@@ -159,3 +159,27 @@ def test_full_size_configs_run(name):
     # the GAP projection makes the data term consistent up to clipping/rounding
     assert res[-1] <= max(res[0], 1e-9 * float(np.linalg.norm(np.abs(wl.y).ravel())))
     assert r.eng.n >= 1900, r.eng.n  # "2048 exemplars" (corners + reference grid)
+
+
+def test_c1_full_size_free_running_parity():
+    """C1 at full size (256x256x8, P=8, K=64, max_corners=512 + reference grid,
+    N ~ 700): the first 10 GAP-GLR iterations (2 matching refreshes) against
+    the oracle — every refresh's anchors and positions identical, max |x - x_o|
+    <= 1e-6 and PSNR within 0.05 dB (SURVEY §8c levels L1-L3)."""
+    wl = workloads.make("C1")
+    iters = 10
+    cfg = G.SolverConfig(max_iters=iters, match=wl.match)
+    trace = []
+    x, rep = G.gap_solve(G.cacti_operator(wl.masks), wl.y, cfg, trace=trace, ref=wl.scene)
+    otrace = []
+    xo, res_o, ps_o = O.gap_solve(O.Operator("cacti", masks=wl.masks), wl.y, iters,
+                                  patch_size=8, group_size=64, max_corners=512,
+                                  exemplar_stride=wl.match.exemplar_stride, trace=otrace,
+                                  ref=wl.scene)
+    assert len(trace) == len(otrace) == 2
+    for (a, p), (ao, po) in zip(trace, otrace):
+        assert len(a) > 600
+        assert np.array_equal(np.asarray(a), np.asarray(ao))
+        assert np.array_equal(np.asarray(p), np.asarray(po))
+    assert np.abs(x - xo).max() <= 1e-6
+    assert abs(rep.rows[-1]["psnr_db"] - ps_o[-1]) <= 0.05

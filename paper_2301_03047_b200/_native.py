@@ -131,8 +131,8 @@ def check(status: int, what: str = "") -> None:
 # bench's gpu_launches claim.
 KERNELS_PER_CALL = {
     "glr_sobel": 1, "glr_stack_from_maps": 1, "glr_corner_response": 6, "glr_corners": 3,
-    "glr_select_anchors": 1, "glr_heat_map": 2, "glr_topk": 1, "glr_gather": 1, "glr_wnnm": 1,
-    "glr_wnnm_scatter": 1, "glr_scatter_count": 1, "glr_scatter_fixed": 1,
+    "glr_select_anchors": 1, "glr_heat_map": 2, "glr_topk": 1, "glr_gather": 1, "glr_wnnm": 3,
+    "glr_wnnm_scatter": 3, "glr_scatter_count": 1, "glr_scatter_fixed": 1,
     "glr_scatter_add_f64": 1, "glr_normalize": 1, "glr_masksum_forward": 1,
     "glr_masksum_adjoint": 1, "glr_gap_masksum": 2, "glr_fourier_forward": 4,
     "glr_fourier_adjoint": 4, "glr_gap_fourier": 11, "glr_sq_err": 2, "glr_vcache_remap": 3,

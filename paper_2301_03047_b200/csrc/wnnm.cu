@@ -5,140 +5,102 @@
 // U diag(max(s - w, 0)) V^T) and :68-87 (glr_regularize: shrink every group,
 // scatter_group, divide by the count), glr/patches.py:57-70 (scatter_group).
 //
-// B200 formulation (one CTA per group, fp64 throughout):
-//   G = M^T M (K x K) accumulated over row tiles of the group, which is read
-//   straight from the image at its K positions (never materialised);
-//   parallel cyclic Jacobi on G (32 disjoint rotations per round) gives
-//   G = V diag(lambda) V^T, s = sqrt(lambda);
-//   Wm = V diag(f(s)/s) V^T with f the WNNM shrinkage; out = M Wm, since
-//   M V = U S makes M V diag(f(s)/s) V^T = U diag(f(s)) V^T.
-// The denoised patches are scatter-added into an int64 fixed-point
-// numerator with integer atomics: the sum is exact and order-independent,
-// hence bitwise deterministic and identical for any exemplar sharding.
+// B200 formulation, fp64 throughout, three kernels per batch of groups so each
+// runs at the occupancy its bottleneck wants:
+//   gram_kernel   G = M^T M (K x K, K padded to 64), the group read straight
+//                 from the image at its K positions with cp.async tiles
+//                 (never materialised); upper-triangle blocks only.
+//   eig_kernel    parallel cyclic Jacobi on G (32 disjoint rotations per
+//                 round), optionally warm-started from the group's cached
+//                 eigenvectors Vp (G <- Vp^T G Vp); s = sqrt(lambda), the WNNM
+//                 shrinkage f, and Wm = V diag(f(s)/s) V^T (written in place).
+//   apply_kernel  out = M Wm, since M V = U S makes M V diag(f(s)/s) V^T =
+//                 U diag(f(s)) V^T; the denoised patches are scatter-added
+//                 into an int64 fixed-point numerator with integer atomics
+//                 (exact, order-independent: bitwise deterministic for any
+//                 exemplar sharding), or written out for the explicit-group API.
 #include "common.cuh"
 
 namespace glr {
 
 namespace wn {
-constexpr int THREADS = 256;
 constexpr int KMAX = 64;
-constexpr int LD = KMAX + 2;  // padded leading dimension of G / V / Wm (16-byte rows)
-constexpr int ROWS = 32;      // rows of M per tile
-constexpr int GRS = ROWS + 1;  // column stride of the Gram tiles (odd: conflict-free)
-constexpr int ARS = 64 + 1;    // column stride of the 64-row apply tiles
+constexpr int LD = KMAX + 2;      // row stride of G / V / Wm in shared memory (16-byte rows)
+constexpr int GROWS = 32;         // rows of M per Gram tile
+constexpr int GRS = GROWS + 1;    // column stride of the Gram tiles (odd: conflict-free)
+constexpr int AROWS = 64;         // rows of M per apply tile
+constexpr int ARS = AROWS + 1;    // column stride of the apply tiles
+constexpr int GRAM_THREADS = 160; // 136 upper-triangle blocks + tile loaders
+constexpr int EIG_THREADS = 256;
+constexpr int APPLY_THREADS = 256;
 constexpr int MAX_SWEEPS = 24;
+constexpr int GSZ = KMAX * KMAX;  // doubles per group in the G / Wm / V buffers
 }  // namespace wn
 
-struct WnnmArgs {
-  // source: either explicit groups (G,K,m) column-major, or image + positions
-  const double* groups;
-  const double* x;
-  int H, W, C, P;
-  const int32_t* pos;
-  int n_max;
-  const int32_t* n_dev;
+// Element (r, j) of group g lives at src[cbase(g, j) + roff(r)]: for image
+// groups roff(r) = (r / PC) * W*C + r % PC (patch row dr, then the contiguous
+// (dc, ch) run of P*C values) and cbase = (row_j * W + col_j) * C; for
+// explicit (G, K, m) groups roff(r) = r and cbase = (g*K + j) * m.
+struct GroupSrc {
+  const double* src;
+  const int32_t* pos;  // image groups: (n, K, 2) top-left positions
+  int W, C, PC;
+  int64_t rs;
   int m, K;
-  double sigma, c_weight, eps, uniform_weight;
-  // outputs: explicit groups or fixed-point scatter
-  double* out;
-  int64_t* acc;
-  double scale;  // 2^frac_bits
-  int32_t* nonfinite;
-  double* vcache;  // optional per-group eigenvector cache (n_max x 64 x 64)
-  int warm;        // 0 cold, 1 start every group from vcache, 2 only where warm_flags[g]
-  const uint8_t* warm_flags;
 };
 
-// Carry eigenvectors across a matching refresh: a new group whose anchor was
-// also an anchor before (and whose old group lived in this rank's old shard)
-// starts its Jacobi sweeps from the old group's eigenvectors.
-__global__ void anchor_map_kernel(const int32_t* __restrict__ anchors, int lo, int hi, int W,
-                                  int32_t* __restrict__ map, int set) {
-  for (int i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += gridDim.x * blockDim.x)
-    map[anchors[2 * i] * W + anchors[2 * i + 1]] = set ? i : -1;
+template <bool IMG>
+__device__ __forceinline__ long long col_base(const GroupSrc& s, int g, int j) {
+  if constexpr (IMG) {
+    const int32_t* q = s.pos + ((size_t)g * s.K + j) * 2;
+    return ((long long)q[0] * s.W + q[1]) * s.C;
+  } else {
+    return ((long long)g * s.K + j) * s.m;
+  }
 }
 
-__global__ void vcache_remap_kernel(const int32_t* __restrict__ new_anchors, int lo, int W,
-                                    const int32_t* __restrict__ map,
-                                    const double* __restrict__ vc_old, double* __restrict__ vc_new,
-                                    uint8_t* __restrict__ flags) {
-  const int g = lo + blockIdx.x;
-  const int old = map[new_anchors[2 * g] * W + new_anchors[2 * g + 1]];
-  if (threadIdx.x == 0) flags[g] = old >= 0 ? 1 : 0;
-  if (old < 0) return;
-  const double2* src = reinterpret_cast<const double2*>(vc_old + (size_t)old * 4096);
-  double2* dst = reinterpret_cast<double2*>(vc_new + (size_t)g * 4096);
-  for (int t = threadIdx.x; t < 2048; t += blockDim.x) dst[t] = src[t];
+// Asynchronous coalesced fill of a column-major tile Tt[j * RS + rr] (rows
+// r0 .. r0+R-1): warp w takes columns w, w+nwarps, ...; lanes run down
+// consecutive rows (contiguous in the image within one patch row).
+template <int NWARPS>
+__device__ __forceinline__ void fill_tile(double* Tt, const GroupSrc& s, const long long* cbase,
+                                          int r0, int R, int RS) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int rr = lane; rr < R; rr += 32) {
+    const int r = r0 + rr;
+    const bool rok = r < s.m;
+    const int64_t off = rok ? (int64_t)(r / s.PC) * s.rs + (r % s.PC) : 0;
+#pragma unroll 4
+    for (int j = warp; j < wn::KMAX; j += NWARPS) {
+      if (rok && j < s.K)
+        cp_async8(&Tt[j * RS + rr], s.src + cbase[j] + off);
+      else
+        Tt[j * RS + rr] = 0.0;
+    }
+  }
+  cp_async_commit();
 }
 
-template <bool FROM_IMAGE>
-__global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
+// ---------------------------------------------------------------------------
+// K1: Gram. 136 threads own the upper-triangle blocks (gi <= gj) of a 16 x 16
+// block grid, block = entries G[gi + 16i][gj + 16j], i, j < 4; every shared
+// load of a warp is a broadcast or one 128-byte wavefront.
+
+template <bool IMG>
+__global__ void __launch_bounds__(wn::GRAM_THREADS) gram_kernel(GroupSrc s, int n,
+                                                               double* __restrict__ Gout) {
   using namespace wn;
   extern __shared__ __align__(16) double sm[];
-  double* G = sm;                 // KMAX x LD (Gram, then Wm)
-  double* V = G + KMAX * LD;      // KMAX x LD (eigenvectors, then row tiles)
-  double* T = V + KMAX * LD;      // 2 x ROWS x TS double-buffered tiles of M
-  __shared__ double ratio[KMAX];
-  __shared__ double s_tiny;
-
-  const int g = blockIdx.x;
-  const int N = a.n_dev ? min(*a.n_dev, a.n_max) : a.n_max;
-  if (g >= N) return;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int K = a.K, m = a.m;
-
-  // Element (r, j) of the group matrix lives at src[cbase[j] + roff(r)]: for
-  // image groups roff(r) = (r / PC) * W*C + r % PC (patch row dr, then the
-  // contiguous (dc, ch) run of P*C values), for explicit groups roff(r) = r.
-  const double* src = FROM_IMAGE ? a.x : a.groups;
-  const int PC = FROM_IMAGE ? a.P * a.C : m;
-  const int64_t rs = FROM_IMAGE ? (int64_t)a.W * a.C : 0;
+  double* T = sm;  // 2 x KMAX x GRS
   __shared__ long long cbase[KMAX];
-  if (tid < KMAX) {
-    long long b = 0;
-    if (tid < K) {
-      if constexpr (FROM_IMAGE) {
-        const int32_t* q = a.pos + ((size_t)g * K + tid) * 2;
-        b = ((long long)q[0] * a.W + q[1]) * a.C;
-      } else {
-        b = ((long long)g * K + tid) * m;
-      }
-    }
-    cbase[tid] = b;
-  }
+  const int g = blockIdx.x;
+  if (g >= n) return;
+  const int tid = threadIdx.x;
+  if (tid < KMAX) cbase[tid] = tid < s.K ? col_base<IMG>(s, g, tid) : 0;
   __syncthreads();
-  // Asynchronous, coalesced tile fill (cp.async, no register staging): warp w
-  // takes columns w, w+8, ...; lanes run down consecutive rows, which are
-  // contiguous in the image within one patch row. Padding stays zero.
-  // Tiles are column-major (element (rr, j) at Tt[j * RS + rr]) with an odd
-  // column stride RS, so both the fill (lanes along rr) and the compute
-  // loops (lanes along columns, or along rows within a column) hit
-  // distinct banks.
-  auto fill = [&](double* Tt, int r0, int R, int RS) {
-    for (int rr = lane; rr < R; rr += 32) {
-      const int r = r0 + rr;
-      const bool rok = r < m;
-      const int64_t off = rok ? (int64_t)(r / PC) * rs + (r % PC) : 0;
-#pragma unroll 4
-      for (int j = warp; j < KMAX; j += THREADS / 32) {
-        if (rok && j < K)
-          cp_async8(&Tt[j * RS + rr], src + cbase[j] + off);
-        else
-          Tt[j * RS + rr] = 0.0;
-      }
-    }
-    cp_async_commit();
-  };
-
-  // ---- Gram G = M^T M (K padded to 64 with zero columns), double-buffered
-  // row tiles. G is symmetric: the 136 threads t < 136 own the upper-triangle
-  // blocks (gi <= gj) of a 16 x 16 grid, block (gi, gj) = entries
-  // G[gi + 16i][gj + 16j], i, j < 4; warps 5-7 only help with the tile fills.
-  const int bi = tid >> 4, bj = tid & 15;  // square 4x4 blocks (later phases)
   int gi = 0, gj = 0;
-  const bool gram_thread = tid < 136;
-  if (gram_thread) {
+  const bool active = tid < 136;
+  if (active) {
     int rem = tid;
     while (rem >= 16 - gi) {
       rem -= 16 - gi;
@@ -151,19 +113,19 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-  const int ntiles = (m + ROWS - 1) / ROWS;
-  fill(T, 0, ROWS, GRS);
+  const int ntiles = (s.m + GROWS - 1) / GROWS;
+  fill_tile<GRAM_THREADS / 32>(T, s, cbase, 0, GROWS, GRS);
   for (int tt = 0; tt < ntiles; ++tt) {
     if (tt + 1 < ntiles)
-      fill(T + ((tt + 1) & 1) * KMAX * GRS, (tt + 1) * ROWS, ROWS, GRS);
+      fill_tile<GRAM_THREADS / 32>(T + ((tt + 1) & 1) * KMAX * GRS, s, cbase, (tt + 1) * GROWS,
+                                   GROWS, GRS);
     else
       cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
     const double* Tc = T + (tt & 1) * KMAX * GRS;
-    const int rmax = min(ROWS, m - tt * ROWS);
-    if (gram_thread) {
-#pragma unroll 4
+    const int rmax = min(GROWS, s.m - tt * GROWS);
+    if (active) {
       for (int rr = 0; rr < rmax; ++rr) {
         double x[4], y[4];
 #pragma unroll
@@ -179,82 +141,115 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
     }
     __syncthreads();
   }
-  if (gram_thread) {
+  if (active) {
+    double* Gg = Gout + (size_t)g * GSZ;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        G[(gi + 16 * i) * LD + gj + 16 * j] = acc[i][j];
-        G[(gj + 16 * j) * LD + gi + 16 * i] = acc[i][j];  // mirror (same value on gi == gj)
+        Gg[(gi + 16 * i) * KMAX + gj + 16 * j] = acc[i][j];
+        Gg[(gj + 16 * j) * KMAX + gi + 16 * i] = acc[i][j];  // mirror (same value on gi == gj)
       }
   }
-  double* vc = a.vcache ? a.vcache + (size_t)g * KMAX * KMAX : nullptr;
+}
+
+// ---------------------------------------------------------------------------
+// K2: eigen-decomposition + shrinkage -> Wm (in place over G)
+
+struct EigArgs {
+  double* G;  // n x 64 x 64: G in, Wm out
+  int n, K;
+  double sigma, c_weight, eps, uniform_weight;
+  double* vcache;  // optional per-group eigenvector cache (n x 64 x 64)
+  int warm;        // 0 cold, 1 start every group from vcache, 2 only where warm_flags[g]
+  const uint8_t* warm_flags;
+};
+
+__global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
+  using namespace wn;
+  extern __shared__ __align__(16) double sm[];
+  double* G = sm;             // KMAX x LD
+  double* V = G + KMAX * LD;  // KMAX x LD
+  __shared__ double ratio[KMAX];
+  __shared__ double s_tiny;
+  const int g = blockIdx.x;
+  if (g >= a.n) return;
+  const int tid = threadIdx.x;
+  const int K = a.K;
+  const int bi = tid >> 4, bj = tid & 15;  // 4x4 blocks for the small products
+  double* Gg = a.G + (size_t)g * GSZ;
+  double* vc = a.vcache ? a.vcache + (size_t)g * GSZ : nullptr;
   const bool warm = vc && (a.warm == 1 || (a.warm == 2 && a.warm_flags[g]));
-  if (!warm) {
-    for (int t = tid; t < KMAX * KMAX; t += THREADS) {
-      const int i = t >> 6, j = t & 63;
+
+  for (int t = tid; t < GSZ / 2; t += EIG_THREADS) {
+    const int i = (2 * t) >> 6, j = (2 * t) & 63;
+    *reinterpret_cast<double2*>(&G[i * LD + j]) = reinterpret_cast<const double2*>(Gg)[t];
+    if (warm) {
+      *reinterpret_cast<double2*>(&V[i * LD + j]) = reinterpret_cast<const double2*>(vc)[t];
+    } else {
       V[i * LD + j] = (i == j) ? 1.0 : 0.0;
+      V[i * LD + j + 1] = (i == j + 1) ? 1.0 : 0.0;
     }
   }
   __syncthreads();
+  if (tid == 0) {
+    double tr = 0.0;
+    for (int i = 0; i < K; ++i) tr += fabs(G[i * LD + i]);
+    s_tiny = 1e-17 * tr;
+  }
   if (warm) {
-    // Warm start from this group's eigenvectors of the previous iteration
-    // (same positions, slightly changed pixels): G <- Vp^T G Vp, V <- Vp, so
-    // the Jacobi sweeps only have to remove a small off-diagonal residue.
-    {
-      double y[4][4];  // Y = G Vp, 4x4 block per thread, into V's buffer
+    // Warm start from this group's eigenvectors of a previous iteration:
+    // G <- Vp^T G Vp (two 64^3 products through the Wm-sized scratch in
+    // global memory is avoided: Y = G Vp goes to registers, then to G's rows
+    // after a barrier), V stays Vp. The sweeps then only remove a small
+    // off-diagonal residue.
+    double y[4][4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) y[i][j] = 0.0;
-      for (int k = 0; k < KMAX; ++k) {
-        const double2 v01 = *reinterpret_cast<const double2*>(vc + k * KMAX + 4 * bj);
-        const double2 v23 = *reinterpret_cast<const double2*>(vc + k * KMAX + 4 * bj + 2);
-        const double vv[4] = {v01.x, v01.y, v23.x, v23.y};
+      for (int j = 0; j < 4; ++j) y[i][j] = 0.0;
+    for (int k = 0; k < KMAX; ++k) {
+      const double2 v01 = *reinterpret_cast<const double2*>(&V[k * LD + 4 * bj]);
+      const double2 v23 = *reinterpret_cast<const double2*>(&V[k * LD + 4 * bj + 2]);
+      const double vv[4] = {v01.x, v01.y, v23.x, v23.y};
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const double gk = G[(4 * bi + i) * LD + k];
+      for (int i = 0; i < 4; ++i) {
+        const double gk = G[(4 * bi + i) * LD + k];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) y[i][j] = fma(gk, vv[j], y[i][j]);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) V[(4 * bi + i) * LD + 4 * bj + j] = y[i][j];
-    }
-    __syncthreads();
-    {
-      double z[4][4];  // G' = Vp^T Y
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) z[i][j] = 0.0;
-      for (int k = 0; k < KMAX; ++k) {
-        const double2 v01 = *reinterpret_cast<const double2*>(vc + k * KMAX + 4 * bi);
-        const double2 v23 = *reinterpret_cast<const double2*>(vc + k * KMAX + 4 * bi + 2);
-        const double vv[4] = {v01.x, v01.y, v23.x, v23.y};
-        const double2 y01 = *reinterpret_cast<const double2*>(&V[k * LD + 4 * bj]);
-        const double2 y23 = *reinterpret_cast<const double2*>(&V[k * LD + 4 * bj + 2]);
-        const double yy[4] = {y01.x, y01.y, y23.x, y23.y};
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) z[i][j] = fma(vv[i], yy[j], z[i][j]);
-      }
-      __syncthreads();
-      // symmetrise (the product is symmetric up to rounding) and reload Vp
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) G[(4 * bi + i) * LD + 4 * bj + j] = z[i][j];
-      for (int t = tid; t < KMAX * KMAX; t += THREADS) {
-        const int i = t >> 6, j = t & 63;
-        V[i * LD + j] = vc[t];
+        for (int j = 0; j < 4; ++j) y[i][j] = fma(gk, vv[j], y[i][j]);
       }
     }
     __syncthreads();
-    for (int t = tid; t < KMAX * KMAX; t += THREADS) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) G[(4 * bi + i) * LD + 4 * bj + j] = y[i][j];
+    __syncthreads();
+    double z[4][4];  // G' = Vp^T Y
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) z[i][j] = 0.0;
+    for (int k = 0; k < KMAX; ++k) {
+      const double2 v01 = *reinterpret_cast<const double2*>(&V[k * LD + 4 * bi]);
+      const double2 v23 = *reinterpret_cast<const double2*>(&V[k * LD + 4 * bi + 2]);
+      const double vv[4] = {v01.x, v01.y, v23.x, v23.y};
+      const double2 y01 = *reinterpret_cast<const double2*>(&G[k * LD + 4 * bj]);
+      const double2 y23 = *reinterpret_cast<const double2*>(&G[k * LD + 4 * bj + 2]);
+      const double yy[4] = {y01.x, y01.y, y23.x, y23.y};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) z[i][j] = fma(vv[i], yy[j], z[i][j]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) G[(4 * bi + i) * LD + 4 * bj + j] = z[i][j];
+    __syncthreads();
+    // symmetrise (the product is symmetric up to rounding)
+    for (int t = tid; t < GSZ; t += EIG_THREADS) {
       const int i = t >> 6, j = t & 63;
       if (i < j) {
         const double v = 0.5 * (G[i * LD + j] + G[j * LD + i]);
@@ -262,32 +257,25 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
         G[j * LD + i] = v;
       }
     }
-    __syncthreads();
-  }
-  if (tid == 0) {
-    double tr = 0.0;
-    for (int i = 0; i < K; ++i) tr += fabs(G[i * LD + i]);
-    s_tiny = 1e-17 * tr;
   }
   __syncthreads();
   const double tiny = s_tiny;
 
   // ---- parallel cyclic Jacobi: 32 disjoint rotations per round (circle
-  // schedule over 64 indices); 8 threads per pair, 2 barriers per round.
-  // A rotation is skipped once |g_pq| is at rounding level relative to its
-  // diagonal pair (or to 1e-17 trace); stop after a sweep without rotations.
+  // schedule over 64 indices); 8 threads per pair, 2 barriers per round. A
+  // rotation is skipped once |g_pq| is at rounding level relative to its
+  // diagonal pair (or to 1e-17 trace).
   const int pk = tid >> 3, l = tid & 7;
   for (int sweep = 0; sweep < MAX_SWEEPS; ++sweep) {
     // A sweep changes G only if some pair passes the rotation test on the
-    // current G (otherwise no round rotates, by induction), so test all
-    // pairs up front and stop without paying for a no-op sweep.
+    // current G (otherwise no round rotates, by induction): test all pairs
+    // up front and stop without paying for a no-op sweep.
     bool need = false;
-    for (int t = tid; t < KMAX * KMAX; t += THREADS) {
+    for (int t = tid; t < GSZ; t += EIG_THREADS) {
       const int i = t >> 6, j = t & 63;
-      if (i < j) {
-        const double apq = G[i * LD + j];
-        need |= fabs(apq) > fmax(1e-15 * sqrt(fabs(G[i * LD + i] * G[j * LD + j])), tiny);
-      }
+      if (i < j)
+        need |= fabs(G[i * LD + j]) >
+                fmax(1e-15 * sqrt(fabs(G[i * LD + i] * G[j * LD + j])), tiny);
     }
     if (!__syncthreads_or(need)) break;
     for (int round = 0; round < KMAX - 1; ++round) {
@@ -306,14 +294,14 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
       const double app = G[p * LD + p], aqq = G[q * LD + q], apq = G[p * LD + q];
       __syncwarp();
       const bool rot = fabs(apq) > fmax(1e-15 * sqrt(fabs(app * aqq)), tiny);
-      double c = 1.0, s = 0.0;
+      double c = 1.0, sn = 0.0;
       if (rot) {
         const double tau = (aqq - app) / (2.0 * apq);
         const double t = fabs(tau) > 1e150
                              ? 0.5 / tau
                              : (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
         c = 1.0 / sqrt(1.0 + t * t);
-        s = t * c;
+        sn = t * c;
         // rows p, q: G <- J^T G (all loads issued before any store)
         double gp[KMAX / 8], gq[KMAX / 8];
 #pragma unroll
@@ -323,29 +311,32 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
         }
 #pragma unroll
         for (int i = 0; i < KMAX / 8; ++i) {
-          G[p * LD + l + 8 * i] = c * gp[i] - s * gq[i];
-          G[q * LD + l + 8 * i] = s * gp[i] + c * gq[i];
+          G[p * LD + l + 8 * i] = c * gp[i] - sn * gq[i];
+          G[q * LD + l + 8 * i] = sn * gp[i] + c * gq[i];
         }
       }
       __syncthreads();
       if (rot) {
         // columns p, q: G <- G J, V <- V J
-        double gp[KMAX / 8], gq[KMAX / 8], vp[KMAX / 8], vq[KMAX / 8];
 #pragma unroll
-        for (int i = 0; i < KMAX / 8; ++i) {
-          const int r = l + 8 * i;
-          gp[i] = G[r * LD + p];
-          gq[i] = G[r * LD + q];
-          vp[i] = V[r * LD + p];
-          vq[i] = V[r * LD + q];
-        }
+        for (int h = 0; h < 2; ++h) {
+          double gp[KMAX / 16], gq[KMAX / 16], vp[KMAX / 16], vq[KMAX / 16];
 #pragma unroll
-        for (int i = 0; i < KMAX / 8; ++i) {
-          const int r = l + 8 * i;
-          G[r * LD + p] = c * gp[i] - s * gq[i];
-          G[r * LD + q] = s * gp[i] + c * gq[i];
-          V[r * LD + p] = c * vp[i] - s * vq[i];
-          V[r * LD + q] = s * vp[i] + c * vq[i];
+          for (int i = 0; i < KMAX / 16; ++i) {
+            const int r = l + 8 * (i + h * (KMAX / 16));
+            gp[i] = G[r * LD + p];
+            gq[i] = G[r * LD + q];
+            vp[i] = V[r * LD + p];
+            vq[i] = V[r * LD + q];
+          }
+#pragma unroll
+          for (int i = 0; i < KMAX / 16; ++i) {
+            const int r = l + 8 * (i + h * (KMAX / 16));
+            G[r * LD + p] = c * gp[i] - sn * gq[i];
+            G[r * LD + q] = sn * gp[i] + c * gq[i];
+            V[r * LD + p] = c * vp[i] - sn * vq[i];
+            V[r * LD + q] = sn * vp[i] + c * vq[i];
+          }
         }
       }
       __syncthreads();
@@ -353,9 +344,11 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
   }
 
   if (vc) {
-    for (int t = tid; t < KMAX * KMAX; t += THREADS) vc[t] = V[(t >> 6) * LD + (t & 63)];
+    for (int t = tid; t < GSZ / 2; t += EIG_THREADS) {
+      const int i = (2 * t) >> 6, j = (2 * t) & 63;
+      reinterpret_cast<double2*>(vc)[t] = *reinterpret_cast<const double2*>(&V[i * LD + j]);
+    }
   }
-
   // ---- shrinkage weights (lowrank.py:58-64) ----
   if (tid < KMAX) {
     double r = 0.0;
@@ -375,63 +368,83 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
     ratio[tid] = r;
   }
   __syncthreads();
-  // Wm = V diag(ratio) V^T into G (4x4 block per thread)
-  {
-    double o[4][4];
+  // Wm = V diag(ratio) V^T -> global (4x4 block per thread)
+  double o[4][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) o[i][j] = 0.0;
-    for (int k = 0; k < KMAX; ++k) {
-      const double rk = ratio[k];
-      if (rk == 0.0) continue;
-      double x[4], y[4];
+    for (int j = 0; j < 4; ++j) o[i][j] = 0.0;
+  for (int k = 0; k < KMAX; ++k) {
+    const double rk = ratio[k];
+    if (rk == 0.0) continue;
+    double x[4], y[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        x[i] = V[(4 * bi + i) * LD + k] * rk;
-        y[i] = V[(4 * bj + i) * LD + k];
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) o[i][j] = fma(x[i], y[j], o[i][j]);
+    for (int i = 0; i < 4; ++i) {
+      x[i] = V[(4 * bi + i) * LD + k] * rk;
+      y[i] = V[(4 * bj + i) * LD + k];
     }
-    __syncthreads();
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) G[(4 * bi + i) * LD + 4 * bj + j] = o[i][j];
+      for (int j = 0; j < 4; ++j) o[i][j] = fma(x[i], y[j], o[i][j]);
   }
-  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double2* dst = reinterpret_cast<double2*>(Gg + (4 * bi + i) * KMAX + 4 * bj);
+    dst[0] = make_double2(o[i][0], o[i][1]);
+    dst[1] = make_double2(o[i][2], o[i][3]);
+  }
+}
 
-  // ---- out = M Wm over 64-row tiles (in V's space); 4 rows x 4 cols / thread
-  // thread -> rows {r16 + 16u} x columns {4 cq .. 4 cq + 3}: lanes of a half
-  // warp run down consecutive rows, so the scatter atomics coalesce.
-  // 64-row tiles, double-buffered between V's space and the two T halves.
+// ---------------------------------------------------------------------------
+// K3: out = M Wm over 64-row tiles; thread -> rows {r16 + 16u} x columns
+// {4 cq .. 4 cq + 3}: lanes of a half warp run down consecutive rows, so the
+// fixed-point scatter atomics coalesce.
+
+template <bool IMG>
+__global__ void __launch_bounds__(wn::APPLY_THREADS, 2)
+    apply_kernel(GroupSrc s, int n, const double* __restrict__ Wm, double scale,
+                 int64_t* __restrict__ acc_out, double* __restrict__ out) {
+  using namespace wn;
+  extern __shared__ __align__(16) double sm[];
+  double* Ws = sm;              // KMAX x LD
+  double* T = Ws + KMAX * LD;   // 2 x KMAX x ARS
+  __shared__ long long cbase[KMAX];
+  const int g = blockIdx.x;
+  if (g >= n) return;
+  const int tid = threadIdx.x;
+  const int K = s.K, m = s.m;
+  if (tid < KMAX) cbase[tid] = tid < K ? col_base<IMG>(s, g, tid) : 0;
+  __syncthreads();
+  fill_tile<APPLY_THREADS / 32>(T, s, cbase, 0, AROWS, ARS);
+  const double* Wg = Wm + (size_t)g * GSZ;
+  for (int t = tid; t < GSZ / 2; t += APPLY_THREADS) {
+    const int i = (2 * t) >> 6, j = (2 * t) & 63;
+    *reinterpret_cast<double2*>(&Ws[i * LD + j]) = reinterpret_cast<const double2*>(Wg)[t];
+  }
   const int r16 = tid & 15, cq = tid >> 4;
-  const int napply = (m + 63) / 64;
-  fill(V, 0, 64, ARS);
-  for (int tt = 0; tt < napply; ++tt) {
-    const int r0 = tt * 64;
-    if (tt + 1 < napply)
-      fill((tt & 1) ? V : T, r0 + 64, 64, ARS);
+  const int ntiles = (m + AROWS - 1) / AROWS;
+  for (int tt = 0; tt < ntiles; ++tt) {
+    const int r0 = tt * AROWS;
+    if (tt + 1 < ntiles)
+      fill_tile<APPLY_THREADS / 32>(T + ((tt + 1) & 1) * KMAX * ARS, s, cbase, r0 + AROWS,
+                                    AROWS, ARS);
     else
       cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    const double* R = (tt & 1) ? T : V;
+    const double* R = T + (tt & 1) * KMAX * ARS;
     double o[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) o[i][j] = 0.0;
-#pragma unroll 4
     for (int i = 0; i < K; ++i) {
       double mv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) mv[u] = R[i * ARS + r16 + 16 * u];
-      const double2 w01 = *reinterpret_cast<const double2*>(&G[i * LD + 4 * cq]);
-      const double2 w23 = *reinterpret_cast<const double2*>(&G[i * LD + 4 * cq + 2]);
+      const double2 w01 = *reinterpret_cast<const double2*>(&Ws[i * LD + 4 * cq]);
+      const double2 w23 = *reinterpret_cast<const double2*>(&Ws[i * LD + 4 * cq + 2]);
       const double wv[4] = {w01.x, w01.y, w23.x, w23.y};
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -442,23 +455,50 @@ __global__ void __launch_bounds__(wn::THREADS, 2) wnnm_kernel(WnnmArgs a) {
     for (int u = 0; u < 4; ++u) {
       const int r = r0 + r16 + 16 * u;
       if (r >= m) break;
-      const int64_t off = (int64_t)(r / PC) * rs + (r % PC);
+      const int64_t off = (int64_t)(r / s.PC) * s.rs + (r % s.PC);
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
         const int j = 4 * cq + v;
         if (j >= K) break;
-        if constexpr (FROM_IMAGE) {
-          const long long val = __double2ll_rn(o[u][v] * a.scale);
-          atomicAdd(reinterpret_cast<unsigned long long*>(a.acc + cbase[j] + off),
+        if constexpr (IMG) {
+          const long long val = __double2ll_rn(o[u][v] * scale);
+          atomicAdd(reinterpret_cast<unsigned long long*>(acc_out + cbase[j] + off),
                     (unsigned long long)val);
         } else {
-          a.out[cbase[j] + off] = o[u][v];
+          out[cbase[j] + off] = o[u][v];
         }
       }
     }
     __syncthreads();
   }
 }
+
+// ---------------------------------------------------------------------------
+// Eigenvector carry-over across a matching refresh: a new group whose anchor
+// was also an anchor before (and whose old group lived in this rank's old
+// shard) starts its Jacobi sweeps from the old group's eigenvectors.
+
+__global__ void anchor_map_kernel(const int32_t* __restrict__ anchors, int lo, int hi, int W,
+                                  int32_t* __restrict__ map, int set) {
+  for (int i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += gridDim.x * blockDim.x)
+    map[anchors[2 * i] * W + anchors[2 * i + 1]] = set ? i : -1;
+}
+
+__global__ void vcache_remap_kernel(const int32_t* __restrict__ new_anchors, int lo, int W,
+                                    const int32_t* __restrict__ map,
+                                    const double* __restrict__ vc_old, double* __restrict__ vc_new,
+                                    uint8_t* __restrict__ flags) {
+  const int g = lo + blockIdx.x;
+  const int old = map[new_anchors[2 * g] * W + new_anchors[2 * g + 1]];
+  if (threadIdx.x == 0) flags[g] = old >= 0 ? 1 : 0;
+  if (old < 0) return;
+  const double2* src = reinterpret_cast<const double2*>(vc_old + (size_t)old * wn::GSZ);
+  double2* dst = reinterpret_cast<double2*>(vc_new + (size_t)g * wn::GSZ);
+  for (int t = threadIdx.x; t < wn::GSZ / 2; t += blockDim.x) dst[t] = src[t];
+}
+
+// ---------------------------------------------------------------------------
+// counters / explicit-group scatter / normalisation
 
 // cnt[pixel] += 1 for every patch covering it (channel-invariant counter)
 __global__ void scatter_count_kernel(const int32_t* __restrict__ pos, int n_max,
@@ -533,25 +573,42 @@ static int blocks_for(int64_t n, int threads = 256) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, threads), (int64_t)kNumSMs * 32));
 }
 
-static size_t wnnm_smem() {
-  static_assert(2 * wn::GRS >= wn::ARS && wn::LD >= wn::ARS, "tile buffers");
-  return (size_t)(2 * wn::KMAX * wn::LD + 2 * wn::KMAX * wn::GRS) * sizeof(double);
-}
+constexpr size_t kGramSmem = 2 * wn::KMAX * wn::GRS * sizeof(double);
+constexpr size_t kEigSmem = 2 * wn::KMAX * wn::LD * sizeof(double);
+constexpr size_t kApplySmem = (wn::KMAX * wn::LD + 2 * wn::KMAX * wn::ARS) * sizeof(double);
 
-template <bool FROM_IMAGE>
-static int launch_wnnm(const WnnmArgs& a, int grid, cudaStream_t st) {
-  const size_t smem = wnnm_smem();
-  GLR_CUDA(cudaFuncSetAttribute(wnnm_kernel<FROM_IMAGE>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  wnnm_kernel<FROM_IMAGE><<<grid, wn::THREADS, smem, st>>>(a);
-  return check_launch("wnnm_kernel");
+// Gram -> eigen/shrink -> apply for n groups; ws holds n x 64 x 64 doubles.
+template <bool IMG>
+static int run_wnnm(const GroupSrc& s, int n, const EigArgs& ea_in, double scale,
+                    int64_t* acc_out, double* out, double* ws, cudaStream_t st) {
+  static bool attrs = false;
+  if (!attrs) {
+    GLR_CUDA(cudaFuncSetAttribute(gram_kernel<IMG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kGramSmem));
+    GLR_CUDA(cudaFuncSetAttribute(eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kEigSmem));
+    GLR_CUDA(cudaFuncSetAttribute(apply_kernel<IMG>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem));
+    attrs = true;
+  }
+  gram_kernel<IMG><<<n, wn::GRAM_THREADS, kGramSmem, st>>>(s, n, ws);
+  GLR_CUDA(cudaGetLastError());
+  EigArgs ea = ea_in;
+  ea.G = ws;
+  ea.n = n;
+  eig_kernel<<<n, wn::EIG_THREADS, kEigSmem, st>>>(ea);
+  GLR_CUDA(cudaGetLastError());
+  apply_kernel<IMG><<<n, wn::APPLY_THREADS, kApplySmem, st>>>(s, n, ws, scale, acc_out, out);
+  return check_launch("wnnm kernels");
 }
 
 }  // namespace glr
 
 using namespace glr;
 
-extern "C" size_t glr_wnnm_workspace(int G, int K) { return 0; }
+extern "C" size_t glr_wnnm_workspace(int G, int K) {
+  return (size_t)std::max(G, 1) * wn::GSZ * sizeof(double) + 256;
+}
 
 extern "C" int glr_wnnm(const double* groups_d, int G, int m, int K, double sigma, double c_weight,
                         double eps, double uniform_weight, double* out_d, int32_t* nonfinite_d,
@@ -562,53 +619,59 @@ extern "C" int glr_wnnm(const double* groups_d, int G, int m, int K, double sigm
   GLR_REQUIRE(sigma >= 0, GLR_ERR_INVALID, "noise_sigma must be nonnegative");
   GLR_REQUIRE(c_weight > 0 && eps > 0, GLR_ERR_INVALID, "c_weight and eps must be positive");
   if (G <= 0) return GLR_OK;
-  WnnmArgs a{};
-  a.groups = groups_d;
-  a.n_max = G;
-  a.m = m;
-  a.K = K;
-  a.sigma = sigma;
-  a.c_weight = c_weight;
-  a.eps = eps;
-  a.uniform_weight = uniform_weight;
-  a.out = out_d;
-  a.nonfinite = nonfinite_d;
-  return launch_wnnm<false>(a, G, (cudaStream_t)stream);
+  GLR_REQUIRE(ws_bytes >= glr_wnnm_workspace(G, K) - 256, GLR_ERR_WORKSPACE,
+              "wnnm: workspace %zu too small", ws_bytes);
+  GroupSrc s{};
+  s.src = groups_d;
+  s.PC = m;
+  s.rs = 0;
+  s.m = m;
+  s.K = K;
+  EigArgs ea{};
+  ea.K = K;
+  ea.sigma = sigma;
+  ea.c_weight = c_weight;
+  ea.eps = eps;
+  ea.uniform_weight = uniform_weight;
+  return run_wnnm<false>(s, G, ea, 1.0, nullptr, out_d, reinterpret_cast<double*>(ws_d),
+                         (cudaStream_t)stream);
 }
 
 extern "C" int glr_wnnm_scatter(const double* x_d, int H, int W, int C, int P,
                                 const int32_t* positions_d, int n_max, const int32_t* n_dev_d,
                                 int K, double sigma, double c_weight, double eps, int frac_bits,
                                 int64_t* acc_d, double* vcache_d, int warm,
-                                const uint8_t* warm_flags_d, void* ws_d,
-                                size_t ws_bytes, void* stream) {
+                                const uint8_t* warm_flags_d, void* ws_d, size_t ws_bytes,
+                                void* stream) {
   GLR_REQUIRE(K >= 1 && K <= wn::KMAX, GLR_ERR_UNSUPPORTED, "wnnm: K=%d outside [1, %d]", K,
               wn::KMAX);
   GLR_REQUIRE(P >= 1 && P <= H && P <= W, GLR_ERR_INVALID, "wnnm_scatter: bad patch size");
   GLR_REQUIRE(frac_bits >= 0 && frac_bits <= 52, GLR_ERR_INVALID, "frac_bits %d", frac_bits);
-  if (n_max <= 0) return GLR_OK;
-  WnnmArgs a{};
-  a.x = x_d;
-  a.H = H;
-  a.W = W;
-  a.C = C;
-  a.P = P;
-  a.pos = positions_d;
-  a.n_max = n_max;
-  a.n_dev = n_dev_d;
-  a.m = P * P * C;
-  a.K = K;
-  a.sigma = sigma;
-  a.c_weight = c_weight;
-  a.eps = eps;
-  a.uniform_weight = -1.0;
-  a.acc = acc_d;
-  a.scale = ldexp(1.0, frac_bits);
-  a.vcache = vcache_d;
-  a.warm = warm;
-  a.warm_flags = warm_flags_d;
   GLR_REQUIRE(warm != 2 || warm_flags_d != nullptr, GLR_ERR_INVALID, "warm=2 needs warm flags");
-  return launch_wnnm<true>(a, n_max, (cudaStream_t)stream);
+  GLR_REQUIRE(n_dev_d == nullptr, GLR_ERR_UNSUPPORTED, "wnnm_scatter: device-side count unsupported");
+  if (n_max <= 0) return GLR_OK;
+  GLR_REQUIRE(ws_bytes >= glr_wnnm_workspace(n_max, K) - 256, GLR_ERR_WORKSPACE,
+              "wnnm_scatter: workspace %zu too small", ws_bytes);
+  GroupSrc s{};
+  s.src = x_d;
+  s.pos = positions_d;
+  s.W = W;
+  s.C = C;
+  s.PC = P * C;
+  s.rs = (int64_t)W * C;
+  s.m = P * P * C;
+  s.K = K;
+  EigArgs ea{};
+  ea.K = K;
+  ea.sigma = sigma;
+  ea.c_weight = c_weight;
+  ea.eps = eps;
+  ea.uniform_weight = -1.0;
+  ea.vcache = vcache_d;
+  ea.warm = warm;
+  ea.warm_flags = warm_flags_d;
+  return run_wnnm<true>(s, n_max, ea, ldexp(1.0, frac_bits), acc_d, nullptr,
+                        reinterpret_cast<double*>(ws_d), (cudaStream_t)stream);
 }
 
 extern "C" int glr_vcache_remap(const int32_t* old_anchors_d, int old_lo, int old_hi,

@@ -146,6 +146,8 @@ class GlrEngine:
         self.heat_chunk = max(1, min(self.max_anchors, heat_budget_bytes // (2 * self.stride)))
         self.heat = D.empty((self.heat_chunk, self.stride), t.int16)
         self.ws_heat = D.empty((N.query("glr_heat_workspace", c, p, self.heat_chunk),), t.uint8)
+        self.ws_wnnm = D.empty((N.query("glr_wnnm_workspace", self.max_anchors, self.k),),
+                               t.uint8)
         # per-group Jacobi eigenvectors, warm start between refreshes
         # (double-buffered so a refresh can carry them over by anchor, see
         # glr_vcache_remap); warm: 0 cold, 1 all groups, 2 per-group flags
@@ -276,7 +278,8 @@ class GlrEngine:
                    self.positions[self.lo:self.hi].data_ptr(), nloc, None, self.k, float(sigma),
                    float(self.c_weight), float(self.eps), self.frac, self.acc.data_ptr(),
                    self.vcache[self.lo:self.hi].data_ptr(), self.warm,
-                   self.warm_flags[self.lo:self.hi].data_ptr(), None, 0, D.stream())
+                   self.warm_flags[self.lo:self.hi].data_ptr(), self.ws_wnnm.data_ptr(),
+                   self.ws_wnnm.numel(), D.stream())
             self.warm = 1
             self.vcache_valid = True
             self._log(("wnnm_scatter", nloc), e)

@@ -51,9 +51,10 @@ def wnnm_batch(mats: np.ndarray, params: WnnmParams) -> np.ndarray:
     src = D.f64(np.ascontiguousarray(mats.transpose(0, 2, 1)))  # (G, K, m) column-major
     out = D.empty((g, k, m), D.torch().float64)
     uw = -1.0 if params.uniform_weight is None else float(params.uniform_weight)
+    ws = D.workspace().get("wnnm", N.query("glr_wnnm_workspace", g, k))
     N.call("glr_wnnm", src.data_ptr(), g, m, k, float(params.noise_sigma),
-           float(params.c_weight), float(params.eps), uw, out.data_ptr(), None, None, 0,
-           D.stream())
+           float(params.c_weight), float(params.eps), uw, out.data_ptr(), None, ws.data_ptr(),
+           ws.numel(), D.stream())
     return D.host(out).transpose(0, 2, 1).copy()
 
 

@@ -25,14 +25,15 @@ namespace glr {
 
 namespace wn {
 constexpr int KMAX = 64;
-constexpr int LD = KMAX + 2;      // row stride of G / V / Wm in shared memory (16-byte rows)
+constexpr int LD = KMAX + 4;      // row stride of Wm in the apply kernel (== 4 mod 16)
+constexpr int ELD = KMAX + 2;     // row stride of G / V in the eigen kernel
 constexpr int GROWS = 32;         // rows of M per Gram tile
-constexpr int GRS = GROWS + 1;    // column stride of the Gram tiles (odd: conflict-free)
-constexpr int AROWS = 64;         // rows of M per apply tile
-constexpr int ARS = AROWS + 1;    // column stride of the apply tiles
-constexpr int GRAM_THREADS = 160; // 136 upper-triangle blocks + tile loaders
+constexpr int GRS = GROWS + 4;    // column stride of the Gram tiles (== 4 mod 16)
+constexpr int AROWS = 32;         // rows of M per apply tile (one 8-row tile row per warp)
+constexpr int ARS = AROWS + 8;    // column stride of the apply tiles (== 8 mod 16)
+constexpr int GRAM_THREADS = 96;  // three warps: super-blocks (0,0), (0,1), (1,1)
 constexpr int EIG_THREADS = 256;
-constexpr int APPLY_THREADS = 256;
+constexpr int APPLY_THREADS = 128;
 constexpr int MAX_SWEEPS = 24;
 constexpr int GSZ = KMAX * KMAX;  // doubles per group in the G / Wm / V buffers
 }  // namespace wn
@@ -82,9 +83,22 @@ __device__ __forceinline__ void fill_tile(double* Tt, const GroupSrc& s, const l
 }
 
 // ---------------------------------------------------------------------------
-// K1: Gram. 136 threads own the upper-triangle blocks (gi <= gj) of a 16 x 16
-// block grid, block = entries G[gi + 16i][gj + 16j], i, j < 4; every shared
-// load of a warp is a broadcast or one 128-byte wavefront.
+// fp64 tensor-core MMA (DMMA, mma.sync m8n8k4): D(8x8) += A(8x4) B(4x8).
+// Fragments: a = A[lane/4][lane%4], b = B[lane%4][lane/4],
+// d = {D[lane/4][2(lane%4)], D[lane/4][2(lane%4)+1]}. Each warp reuses its A
+// and B fragments across a block of 8x8 tiles, so shared-memory traffic per
+// FMA is ~10x lower than a scalar 4x4 register block (which was bound by the
+// 128 B/clk shared pipe at half the FP64 rate).
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// K1: Gram G = M^T M on DMMA. Three warps own the 32x32 super-blocks (0,0),
+// (0,1), (1,1) of the symmetric 64x64 result (4x4 tiles of 8x8 each); the
+// (1,0) super-block is the mirror of (0,1). Column-major 32-row tiles with
+// column stride GRS = 36 (== 4 mod 16 doubles: fragment loads hit 2 wavefronts).
 
 template <bool IMG>
 __global__ void __launch_bounds__(wn::GRAM_THREADS) gram_kernel(GroupSrc s, int n,
@@ -95,24 +109,16 @@ __global__ void __launch_bounds__(wn::GRAM_THREADS) gram_kernel(GroupSrc s, int 
   __shared__ long long cbase[KMAX];
   const int g = blockIdx.x;
   if (g >= n) return;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid < KMAX) cbase[tid] = tid < s.K ? col_base<IMG>(s, g, tid) : 0;
   __syncthreads();
-  int gi = 0, gj = 0;
-  const bool active = tid < 136;
-  if (active) {
-    int rem = tid;
-    while (rem >= 16 - gi) {
-      rem -= 16 - gi;
-      ++gi;
-    }
-    gj = gi + rem;
-  }
-  double acc[4][4];
+  const int SI = warp == 2 ? 1 : 0, SJ = warp == 0 ? 0 : 1;
+  const int ar = lane >> 2, ak = lane & 3;
+  double acc[4][4][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   const int ntiles = (s.m + GROWS - 1) / GROWS;
   fill_tile<GRAM_THREADS / 32>(T, s, cbase, 0, GROWS, GRS);
   for (int tt = 0; tt < ntiles; ++tt) {
@@ -124,35 +130,32 @@ __global__ void __launch_bounds__(wn::GRAM_THREADS) gram_kernel(GroupSrc s, int 
     cp_async_wait<1>();
     __syncthreads();
     const double* Tc = T + (tt & 1) * KMAX * GRS;
-    const int rmax = min(GROWS, s.m - tt * GROWS);
-    if (active) {
-      for (int rr = 0; rr < rmax; ++rr) {
-        double x[4], y[4];
+#pragma unroll 2
+    for (int k0 = 0; k0 < GROWS; k0 += 4) {  // padding rows are zero
+      double fa[4], fb[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          x[k] = Tc[(gi + 16 * k) * GRS + rr];
-          y[k] = Tc[(gj + 16 * k) * GRS + rr];
-        }
+      for (int a = 0; a < 4; ++a) fa[a] = Tc[(32 * SI + 8 * a + ar) * GRS + k0 + ak];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+      for (int b = 0; b < 4; ++b) fb[b] = Tc[(32 * SJ + 8 * b + ar) * GRS + k0 + ak];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fma(x[i], y[j], acc[i][j]);
-      }
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
     }
     __syncthreads();
   }
-  if (active) {
-    double* Gg = Gout + (size_t)g * GSZ;
+  double* Gg = Gout + (size_t)g * GSZ;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        Gg[(gi + 16 * i) * KMAX + gj + 16 * j] = acc[i][j];
-        Gg[(gj + 16 * j) * KMAX + gi + 16 * i] = acc[i][j];  // mirror (same value on gi == gj)
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = 32 * SI + 8 * a + ar, j = 32 * SJ + 8 * b + 2 * ak + e;
+        Gg[i * KMAX + j] = acc[a][b][e];
+        if (SI != SJ) Gg[j * KMAX + i] = acc[a][b][e];
       }
-  }
 }
-
 // ---------------------------------------------------------------------------
 // K2: eigen-decomposition + shrinkage -> Wm (in place over G)
 
@@ -167,6 +170,7 @@ struct EigArgs {
 
 __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
   using namespace wn;
+  constexpr int LD = ELD;  // row stride of G / V here (Jacobi column access pattern)
   extern __shared__ __align__(16) double sm[];
   double* G = sm;             // KMAX x LD
   double* V = G + KMAX * LD;  // KMAX x LD
@@ -397,12 +401,14 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// K3: out = M Wm over 64-row tiles; thread -> rows {r16 + 16u} x columns
-// {4 cq .. 4 cq + 3}: lanes of a half warp run down consecutive rows, so the
-// fixed-point scatter atomics coalesce.
+// K3: out = M Wm on DMMA over 32-row tiles (column stride ARS = 40 == 8 mod
+// 16 doubles), Wm in shared memory (row stride LD = 68 == 4 mod 16). Warp w
+// owns tile row w (8 rows) x all 8 column tiles: per k-step one A fragment
+// and eight B fragments feed eight DMMAs. The denoised patch entries go to
+// the int64 fixed-point numerator with integer atomics (or to `out`).
 
 template <bool IMG>
-__global__ void __launch_bounds__(wn::APPLY_THREADS, 2)
+__global__ void __launch_bounds__(wn::APPLY_THREADS)
     apply_kernel(GroupSrc s, int n, const double* __restrict__ Wm, double scale,
                  int64_t* __restrict__ acc_out, double* __restrict__ out) {
   using namespace wn;
@@ -412,7 +418,7 @@ __global__ void __launch_bounds__(wn::APPLY_THREADS, 2)
   __shared__ long long cbase[KMAX];
   const int g = blockIdx.x;
   if (g >= n) return;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int K = s.K, m = s.m;
   if (tid < KMAX) cbase[tid] = tid < K ? col_base<IMG>(s, g, tid) : 0;
   __syncthreads();
@@ -422,7 +428,7 @@ __global__ void __launch_bounds__(wn::APPLY_THREADS, 2)
     const int i = (2 * t) >> 6, j = (2 * t) & 63;
     *reinterpret_cast<double2*>(&Ws[i * LD + j]) = reinterpret_cast<const double2*>(Wg)[t];
   }
-  const int r16 = tid & 15, cq = tid >> 4;
+  const int ar = lane >> 2, ak = lane & 3;
   const int ntiles = (m + AROWS - 1) / AROWS;
   for (int tt = 0; tt < ntiles; ++tt) {
     const int r0 = tt * AROWS;
@@ -434,40 +440,36 @@ __global__ void __launch_bounds__(wn::APPLY_THREADS, 2)
     cp_async_wait<1>();
     __syncthreads();
     const double* R = T + (tt & 1) * KMAX * ARS;
-    double o[4][4];
+    double o[8][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int b = 0; b < 8; ++b) o[b][0] = o[b][1] = 0.0;
+#pragma unroll 4
+    for (int k0 = 0; k0 < KMAX; k0 += 4) {  // zero columns beyond K contribute nothing
+      const double fa = R[(k0 + ak) * ARS + 8 * warp + ar];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) o[i][j] = 0.0;
-    for (int i = 0; i < K; ++i) {
-      double mv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) mv[u] = R[i * ARS + r16 + 16 * u];
-      const double2 w01 = *reinterpret_cast<const double2*>(&Ws[i * LD + 4 * cq]);
-      const double2 w23 = *reinterpret_cast<const double2*>(&Ws[i * LD + 4 * cq + 2]);
-      const double wv[4] = {w01.x, w01.y, w23.x, w23.y};
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) o[u][v] = fma(mv[u], wv[v], o[u][v]);
+      for (int b = 0; b < 8; ++b) {
+        const double fb = Ws[(k0 + ak) * LD + 8 * b + ar];
+        dmma(o[b][0], o[b][1], fa, fb);
+      }
     }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int r = r0 + r16 + 16 * u;
-      if (r >= m) break;
+    const int r = r0 + 8 * warp + ar;
+    if (r < m) {
       const int64_t off = (int64_t)(r / s.PC) * s.rs + (r % s.PC);
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int j = 4 * cq + v;
-        if (j >= K) break;
-        if constexpr (IMG) {
-          const long long val = __double2ll_rn(o[u][v] * scale);
-          atomicAdd(reinterpret_cast<unsigned long long*>(acc_out + cbase[j] + off),
-                    (unsigned long long)val);
-        } else {
-          out[cbase[j] + off] = o[u][v];
+      for (int b = 0; b < 8; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = 8 * b + 2 * ak + e;
+          if (j < K) {
+            if constexpr (IMG) {
+              const long long val = __double2ll_rn(o[b][e] * scale);
+              atomicAdd(reinterpret_cast<unsigned long long*>(acc_out + cbase[j] + off),
+                        (unsigned long long)val);
+            } else {
+              out[cbase[j] + off] = o[b][e];
+            }
+          }
         }
-      }
     }
     __syncthreads();
   }
@@ -574,7 +576,7 @@ static int blocks_for(int64_t n, int threads = 256) {
 }
 
 constexpr size_t kGramSmem = 2 * wn::KMAX * wn::GRS * sizeof(double);
-constexpr size_t kEigSmem = 2 * wn::KMAX * wn::LD * sizeof(double);
+constexpr size_t kEigSmem = 2 * wn::KMAX * wn::ELD * sizeof(double);
 constexpr size_t kApplySmem = (wn::KMAX * wn::LD + 2 * wn::KMAX * wn::ARS) * sizeof(double);
 
 // Gram -> eigen/shrink -> apply for n groups; ws holds n x 64 x 64 doubles.

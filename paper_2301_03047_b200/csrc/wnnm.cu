@@ -36,6 +36,11 @@ constexpr int EIG_THREADS = 256;
 constexpr int APPLY_THREADS = 128;
 constexpr int MAX_SWEEPS = 24;
 constexpr int GSZ = KMAX * KMAX;  // doubles per group in the G / Wm / V buffers
+// Jacobi rotation threshold: skip (p,q) once |g_pq| <= kRotTol sqrt(|g_pp g_qq|).
+// With quadratic convergence the last sweep above this level leaves the
+// off-diagonal at ~kRotTol^2; Wm = V diag(f(s)/s) V^T is then accurate to
+// ~1e-13 relative (tests: <= 1e-9 vs LAPACK gesdd).
+constexpr double kRotTol = 1e-12;
 }  // namespace wn
 
 // Element (r, j) of group g lives at src[cbase(g, j) + roff(r)]: for image
@@ -279,7 +284,7 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
       const int i = t >> 6, j = t & 63;
       if (i < j)
         need |= fabs(G[i * LD + j]) >
-                fmax(1e-15 * sqrt(fabs(G[i * LD + i] * G[j * LD + j])), tiny);
+                fmax(kRotTol * sqrt(fabs(G[i * LD + i] * G[j * LD + j])), tiny);
     }
     if (!__syncthreads_or(need)) break;
     for (int round = 0; round < KMAX - 1; ++round) {
@@ -297,7 +302,7 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
       }
       const double app = G[p * LD + p], aqq = G[q * LD + q], apq = G[p * LD + q];
       __syncwarp();
-      const bool rot = fabs(apq) > fmax(1e-15 * sqrt(fabs(app * aqq)), tiny);
+      const bool rot = fabs(apq) > fmax(kRotTol * sqrt(fabs(app * aqq)), tiny);
       double c = 1.0, sn = 0.0;
       if (rot) {
         const double tau = (aqq - app) / (2.0 * apq);

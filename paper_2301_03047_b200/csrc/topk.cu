@@ -70,12 +70,19 @@ __global__ void __launch_bounds__(topk::THREADS) topk_kernel(TopkParams p) {
   // 1. histogram
   for (int b = tid; b < p.bins; b += THREADS) hist[b] = 0;
   __syncthreads();
-  for (int64_t base = (int64_t)tid * VEC; base < M; base += (int64_t)THREADS * VEC) {
-    const uint4 v = *reinterpret_cast<const uint4*>(row + base);
-    const uint16_t* s = reinterpret_cast<const uint16_t*>(&v);
+  for (int64_t base = (int64_t)tid * VEC; base < M; base += (int64_t)THREADS * VEC * 2) {
+    // two independent 16-byte loads in flight per thread
+    const int64_t b1 = base + (int64_t)THREADS * VEC;
+    const uint4 v0 = *reinterpret_cast<const uint4*>(row + base);
+    const uint4 v1 = b1 < M ? *reinterpret_cast<const uint4*>(row + b1) : make_uint4(0, 0, 0, 0);
+    const uint16_t* s0 = reinterpret_cast<const uint16_t*>(&v0);
+    const uint16_t* s1 = reinterpret_cast<const uint16_t*>(&v1);
 #pragma unroll
     for (int j = 0; j < VEC; ++j)
-      if (base + j < M) atomicAdd(&hist[min((int)s[j], p.bins - 1)], 1);
+      if (base + j < M) atomicAdd(&hist[min((int)s0[j], p.bins - 1)], 1);
+#pragma unroll
+    for (int j = 0; j < VEC; ++j)
+      if (b1 + j < M) atomicAdd(&hist[min((int)s1[j], p.bins - 1)], 1);
   }
   __syncthreads();
 

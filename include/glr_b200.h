@@ -182,7 +182,8 @@ int glr_normalize(const int64_t* acc_d, const int32_t* cnt_d, const double* x_d,
  * Mask-sum family (CACTI operators.py:35-59, MSFA operators.py:160-185):
  *   A x = sum_t M_t x_t,  A^T y = M_t y,  gram = sum_t M_t^2.
  * glr_gap_masksum fuses normalize + z + A^T(safe_div(y - A z, gram)),
- * clip [lo, hi], and the per-block partial residual ||y - A x||^2.
+ * clip [lo, hi], and the per-block partial residual ||y - A x||^2; with
+ * rho > 0 the divisor is rho + gram (the ADMM x-update, solvers.py:329).
  * acc_d/cnt_d may be NULL (then z = x_in). x_out may alias x_in.
  * resid_d: 1 double (deterministic reduction).                              */
 int glr_masksum_forward(const double* x_d, const double* masks_d, int H, int W, int T,
@@ -193,7 +194,7 @@ size_t glr_gap_workspace(int H, int W);
 int glr_gap_masksum(const int64_t* acc_d, const int32_t* cnt_d, int frac_bits,
                     const double* x_in_d, const double* masks_d, const double* y_d,
                     const double* gram_d, int H, int W, int T, double lo, double hi,
-                    double* x_out_d, double* resid_d, void* ws_d, void* stream);
+                    double rho, double* x_out_d, double* resid_d, void* ws_d, void* stream);
 
 /* Masked unitary 2-D DFT (operators.py:65-89): real (C=1, adjoint keeps the
  * real part) or complex (C=2, (re,im) channels) images. y is complex128
@@ -206,8 +207,13 @@ int glr_fourier_adjoint(const double* y_d, const double* mask_d, int H, int W, i
                         double* x_d, void* ws_d, void* stream);
 int glr_gap_fourier(const int64_t* acc_d, const int32_t* cnt_d, int frac_bits,
                     const double* x_in_d, const double* mask_d, const double* y_d, int H, int W,
-                    int C, int clip, double lo, double hi, double* x_out_d, double* resid_d,
-                    void* ws_d, void* stream);
+                    int C, int clip, double lo, double hi, double rho, double* x_out_d,
+                    double* resid_d, void* ws_d, void* stream);
+
+/* glr_lincomb: out = clip((a*x + b*y) + c*z) elementwise, y/z optional (NULL),
+ * in that evaluation order (the ADMM bookkeeping of solvers.py:327-334). */
+int glr_lincomb(const double* x_d, double a, const double* y_d, double b, const double* z_d,
+                double c, int64_t n, int clip, double lo, double hi, double* out_d, void* stream);
 
 /* Squared-error sum vs a reference for PSNR (metrics.py:26-37), of
  * clip(x, 0, peak) (no clip when peak <= 0), deterministic. out_d: 1 double. */

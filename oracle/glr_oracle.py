@@ -457,6 +457,57 @@ def gap_solve(op: Operator, y, max_iters, patch_size=8, group_size=64, max_corne
     return out, residuals, psnrs
 
 
+def _glr_match(x, p, group_size, max_corners, exemplar_stride, edge_threshold, sep):
+    """solvers.py:187-203 for the "glr" regularizer: (anchors, positions)."""
+    anchors = build_exemplars(x, p, max_corners, None, 0.01, exemplar_stride)
+    if not anchors:
+        return anchors, []
+    gh, gv = sobel_gradients(x)
+    maps = binarize_gradients(gh, gv, edge_threshold)
+    heat = similarity_heatmap(maps, anchors, p)
+    positions, _ = match_positions(heat, anchors, group_size, sep)
+    return anchors, positions
+
+
+def admm_solve(op: Operator, y, max_iters, patch_size=8, group_size=64, max_corners=512,
+               exemplar_stride=6, edge_threshold=0.2, refresh=5, sigma0=0.10, sigma_min=0.003,
+               peak=1.0, rho=0.01, c_weight=2.0 * np.sqrt(2.0), eps=1e-16, min_separation=None,
+               clip=True, ref=None, trace=None):
+    """solvers.py:311-341 — scaled-form ADMM with the "glr" regularizer:
+    m = z - u; x = clip(m + A^T((y - A m) / (rho + gram))); z = clip(R(x + u));
+    u = u + x - z. Returns (x, residuals, psnrs)."""
+    p = patch_size
+    sep = -(-p // 4) if min_separation is None else min_separation
+    z = op.adjoint(y)
+    u = np.zeros_like(z)
+    lo, hi = -0.5 * peak, 1.5 * peak
+    positions, last = None, -1
+    residuals, psnrs = [], []
+    x = z.copy()
+    for it in range(max_iters):
+        m = z - u
+        x = m + op.adjoint((y - op.forward(m)) / (rho + op.gram))
+        if clip:
+            x = np.clip(x, lo, hi)
+        v = x + u
+        sigma = sigma_at(it, max_iters, sigma0, sigma_min, peak)
+        if positions is None or it - last >= refresh:
+            anchors, positions = _glr_match(v, p, group_size, max_corners, exemplar_stride,
+                                            edge_threshold, sep)
+            if trace is not None:
+                trace.append((list(anchors), [list(q) for q in positions]))
+            last = it
+        z = glr_regularize(v, positions, p, sigma, c_weight, eps) if positions else v.copy()
+        if clip:
+            z = np.clip(z, lo, hi)
+        u = u + x - z
+        residuals.append(float(np.linalg.norm((y - op.forward(x)).ravel())))
+        if ref is not None:
+            psnrs.append(psnr(ref, np.clip(x, 0.0, peak), peak))
+    out = np.clip(x, 0.0, peak) if clip else x
+    return out, residuals, psnrs
+
+
 def heat_flops(h, w, c, p, n):
     """2*M*(4*C*P^2)*N flops per refresh."""
     return 2.0 * (h - p + 1) * (w - p + 1) * 4 * c * p * p * n

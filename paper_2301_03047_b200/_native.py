@@ -69,13 +69,14 @@ SIGNATURES: dict[str, tuple] = {
     "glr_masksum_forward": (i32, [vp, vp, i32, i32, i32, vp, vp]),
     "glr_masksum_adjoint": (i32, [vp, vp, i32, i32, i32, vp, vp]),
     "glr_gap_workspace": (sz, [i32, i32]),
-    "glr_gap_masksum": (i32, [vp, vp, i32, vp, vp, vp, vp, i32, i32, i32, f64, f64, vp, vp, vp,
-                              vp]),
+    "glr_gap_masksum": (i32, [vp, vp, i32, vp, vp, vp, vp, i32, i32, i32, f64, f64, f64, vp, vp,
+                              vp, vp]),
     "glr_fft_workspace": (sz, [i32, i32]),
     "glr_fourier_forward": (i32, [vp, vp, i32, i32, i32, vp, vp, vp]),
     "glr_fourier_adjoint": (i32, [vp, vp, i32, i32, i32, vp, vp, vp]),
-    "glr_gap_fourier": (i32, [vp, vp, i32, vp, vp, vp, i32, i32, i32, i32, f64, f64, vp, vp, vp,
-                              vp]),
+    "glr_gap_fourier": (i32, [vp, vp, i32, vp, vp, vp, i32, i32, i32, i32, f64, f64, f64, vp, vp,
+                              vp, vp]),
+    "glr_lincomb": (i32, [vp, f64, vp, f64, vp, f64, i64, i32, f64, f64, vp, vp]),
     "glr_sq_err": (i32, [vp, vp, i32, f64, vp, vp, vp]),
 }
 
@@ -136,6 +137,7 @@ KERNELS_PER_CALL = {
     "glr_scatter_add_f64": 1, "glr_normalize": 1, "glr_masksum_forward": 1,
     "glr_masksum_adjoint": 1, "glr_gap_masksum": 2, "glr_fourier_forward": 4,
     "glr_fourier_adjoint": 4, "glr_gap_fourier": 11, "glr_sq_err": 2, "glr_vcache_remap": 3,
+    "glr_lincomb": 1,
 }
 launch_count = 0
 

@@ -139,16 +139,19 @@ __global__ void mask_copy_kernel(const double2* __restrict__ src, const double* 
   }
 }
 
-// buf <- M * safe_div(y - M * buf, M)
+// buf <- M * (y - M * buf) / (rho + M) (ADMM, solvers.py:329; rho = 0 is
+// GAP's safe_div, zero where the divisor is zero)
 __global__ void spectral_residual_kernel(double2* __restrict__ buf, const double2* __restrict__ y,
-                                         const double* __restrict__ mask, int64_t npix) {
+                                         const double* __restrict__ mask, int64_t npix,
+                                         double rho) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npix;
        i += (int64_t)gridDim.x * blockDim.x) {
     const double m = mask[i];
+    const double den = rho != 0.0 ? rho + m : m;
     double2 r = make_double2(0.0, 0.0);
-    if (m != 0.0) {
+    if (den != 0.0) {
       const double2 f = buf[i];
-      r = make_double2((y[i].x - m * f.x) / m, (y[i].y - m * f.y) / m);
+      r = make_double2((y[i].x - m * f.x) / den, (y[i].y - m * f.y) / den);
     }
     buf[i] = make_double2(m * r.x, m * r.y);
   }
@@ -257,9 +260,10 @@ extern "C" int glr_fourier_adjoint(const double* y_d, const double* mask_d, int 
 
 extern "C" int glr_gap_fourier(const int64_t* acc_d, const int32_t* cnt_d, int frac_bits,
                                const double* x_in_d, const double* mask_d, const double* y_d, int H,
-                               int W, int C, int clip, double lo, double hi, double* x_out_d,
-                               double* resid_d, void* ws_d, void* stream) {
+                               int W, int C, int clip, double lo, double hi, double rho,
+                               double* x_out_d, double* resid_d, void* ws_d, void* stream) {
   GLR_REQUIRE(C == 1 || C == 2, GLR_ERR_INVALID, "fourier: C=%d (1 real, 2 complex)", C);
+  GLR_REQUIRE(rho >= 0, GLR_ERR_INVALID, "rho must be nonnegative");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t npix = (int64_t)H * W;
   double2* buf = reinterpret_cast<double2*>(ws_d);
@@ -271,7 +275,7 @@ extern "C" int glr_gap_fourier(const int64_t* acc_d, const int32_t* cnt_d, int f
   GLR_CUDA(cudaGetLastError());
   int s = fft2_ortho(buf, H, W, -1, st);
   if (s) return s;
-  spectral_residual_kernel<<<eblocks(npix), 256, 0, st>>>(buf, y, mask_d, npix);
+  spectral_residual_kernel<<<eblocks(npix), 256, 0, st>>>(buf, y, mask_d, npix, rho);
   GLR_CUDA(cudaGetLastError());
   s = fft2_ortho(buf, H, W, +1, st);
   if (s) return s;

@@ -97,7 +97,7 @@ struct GapArgs {
   const double* gram;
   int64_t npix;
   int T;
-  double lo, hi;
+  double lo, hi, rho;
   double* x_out;
   double* part;
 };
@@ -126,7 +126,10 @@ __global__ void __launch_bounds__(gap::THREADS) gap_masksum_kernel(GapArgs a) {
     for (int t = 0; t < T; ++t) prod[t] = __dmul_rn(a.mk[i * T + t], z[t]);
     const double az = pw_sum(prod, T);
     const double yi = a.y[i];
-    const double r = gram != 0.0 ? __ddiv_rn(__dsub_rn(yi, az), gram) : 0.0;
+    // GAP: safe_div(y - Az, gram) (solvers.py:220-226, rho = 0);
+    // ADMM: (y - Am) / (rho + gram) (solvers.py:329)
+    const double den = a.rho != 0.0 ? __dadd_rn(a.rho, gram) : gram;
+    const double r = den != 0.0 ? __ddiv_rn(__dsub_rn(yi, az), den) : 0.0;
     for (int t = 0; t < T; ++t) {
       const double m = a.mk[i * T + t];
       double v = __dadd_rn(z[t], __dmul_rn(m, r));
@@ -155,6 +158,22 @@ __global__ void sq_err_kernel(const double* __restrict__ x, const double* __rest
 
 constexpr int kGapBlocks = 2 * kNumSMs;
 
+// out = clip((a x + b y) + c z) elementwise (z optional), evaluated in that
+// order so ADMM's m = z - u, v = x + u, u' = (u + x) - z match numpy bitwise
+// (solvers.py:327, 332, 334).
+__global__ void lincomb_kernel(const double* __restrict__ x, double a, const double* __restrict__ y,
+                               double b, const double* __restrict__ z, double c, int64_t n,
+                               int clip, double lo, double hi, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = __dmul_rn(a, x[i]);
+    if (y) v = __dadd_rn(v, __dmul_rn(b, y[i]));
+    if (z) v = __dadd_rn(v, __dmul_rn(c, z[i]));
+    if (clip) v = fmin(fmax(v, lo), hi);
+    out[i] = v;
+  }
+}
+
 }  // namespace glr
 
 using namespace glr;
@@ -181,10 +200,13 @@ extern "C" size_t glr_gap_workspace(int H, int W) { return (kGapBlocks + 8) * si
 extern "C" int glr_gap_masksum(const int64_t* acc_d, const int32_t* cnt_d, int frac_bits,
                                const double* x_in_d, const double* masks_d, const double* y_d,
                                const double* gram_d, int H, int W, int T, double lo, double hi,
-                               double* x_out_d, double* resid_d, void* ws_d, void* stream) {
+                               double rho, double* x_out_d, double* resid_d, void* ws_d,
+                               void* stream) {
   GLR_REQUIRE(T >= 1 && T <= gap::TMAX, GLR_ERR_UNSUPPORTED, "gap_masksum: T=%d", T);
+  GLR_REQUIRE(rho >= 0, GLR_ERR_INVALID, "rho must be nonnegative");
   cudaStream_t st = (cudaStream_t)stream;
   GapArgs a;
+  a.rho = rho;
   a.acc = acc_d;
   a.cnt = acc_d ? cnt_d : nullptr;
   a.inv_scale = ldexp(1.0, -frac_bits);
@@ -202,6 +224,15 @@ extern "C" int glr_gap_masksum(const int64_t* acc_d, const int32_t* cnt_d, int f
   GLR_CUDA(cudaGetLastError());
   final_sum_kernel<<<1, 256, 0, st>>>(a.part, kGapBlocks, resid_d);
   return check_launch("final_sum_kernel");
+}
+
+extern "C" int glr_lincomb(const double* x_d, double a, const double* y_d, double b,
+                           const double* z_d, double c, int64_t n, int clip, double lo, double hi,
+                           double* out_d, void* stream) {
+  lincomb_kernel<<<kGapBlocks * 4, gap::THREADS, 0, (cudaStream_t)stream>>>(x_d, a, y_d, b, z_d,
+                                                                            c, n, clip, lo, hi,
+                                                                            out_d);
+  return check_launch("lincomb_kernel");
 }
 
 extern "C" int glr_sq_err(const double* x_d, const double* ref_d, int n, double peak,

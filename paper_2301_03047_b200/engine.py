@@ -75,7 +75,7 @@ class DeviceOperator:
             N.call("glr_masksum_adjoint", y_d.data_ptr(), self.masks.data_ptr(), h, w, c,
                    x_d.data_ptr(), D.stream())
 
-    def gap_update(self, acc, cnt, frac, x_in, y_d, lo, hi, x_out, resid_out, ws):
+    def gap_update(self, acc, cnt, frac, x_in, y_d, lo, hi, x_out, resid_out, ws, rho=0.0):
         """x_out = clip(z + A^T safe_div(y - A z, gram)); resid_out = ||y - A x_out||^2,
         z = acc/cnt where covered else x_in (acc None: z = x_in)."""
         h, w, c = self.shape
@@ -83,12 +83,12 @@ class DeviceOperator:
         cp = cnt.data_ptr() if cnt is not None else None
         if self.kind == "fourier":
             N.call("glr_gap_fourier", ap, cp, frac, x_in.data_ptr(), self.mask.data_ptr(),
-                   y_d.data_ptr(), h, w, c, 1 if self.clip else 0, lo, hi, x_out.data_ptr(),
-                   resid_out.data_ptr(), self.fft_ws.data_ptr(), D.stream())
+                   y_d.data_ptr(), h, w, c, 1 if self.clip else 0, lo, hi, float(rho),
+                   x_out.data_ptr(), resid_out.data_ptr(), self.fft_ws.data_ptr(), D.stream())
         else:
             N.call("glr_gap_masksum", ap, cp, frac, x_in.data_ptr(), self.masks.data_ptr(),
-                   y_d.data_ptr(), self.gram.data_ptr(), h, w, c, lo, hi, x_out.data_ptr(),
-                   resid_out.data_ptr(), ws.data_ptr(), D.stream())
+                   y_d.data_ptr(), self.gram.data_ptr(), h, w, c, lo, hi, float(rho),
+                   x_out.data_ptr(), resid_out.data_ptr(), ws.data_ptr(), D.stream())
 
 
 class GlrEngine:

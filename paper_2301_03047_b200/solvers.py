@@ -277,8 +277,6 @@ def gap_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = Non
     across ranks; ``positions_override`` (list of (anchors, positions) per
     refresh) locks matching for positions-locked parity; ``trace`` (a list)
     receives (anchors, positions) of every refresh."""
-    if cfg.algorithm != "gap":
-        raise NotImplementedError("ADMM is the 'next' row f1 (SURVEY §8f); use algorithm='gap'")
     _require_glr(cfg)
     y = np.asarray(y)
     _check_measurement(op, y)
@@ -325,9 +323,125 @@ def gap_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = Non
     return out, report
 
 
-def admm_solve(op, y, cfg, ref=None):
-    """solvers.py:311-341 — the 'next' row f1."""
-    raise NotImplementedError("admm_solve is the 'next' row f1 (SURVEY §8f), not yet on B200")
+class AdmmRunner(GapRunner):
+    """Scaled-form ADMM (solvers.py:311-341) on the same device operator and
+    GLR engine; the x-update is the fused projection kernel with the divisor
+    rho + gram, the bookkeeping is glr_lincomb in numpy's evaluation order."""
+
+    def __init__(self, op, cfg: SolverConfig, process_group=None):
+        super().__init__(op, cfg, process_group)
+        t = D.torch()
+        self.z = D.empty(self.dop.shape, t.float64)
+        self.u = D.empty(self.dop.shape, t.float64)
+        self.v = D.empty(self.dop.shape, t.float64)
+
+    def _lincomb(self, out, x, a, y=None, b=0.0, z=None, c=0.0, clip=False):
+        lo, hi = -0.5 * self.cfg.peak, 1.5 * self.cfg.peak
+        N.call("glr_lincomb", x.data_ptr(), float(a), y.data_ptr() if y is not None else None,
+               float(b), z.data_ptr() if z is not None else None, float(c), int(x.numel()),
+               1 if clip else 0, lo, hi, out.data_ptr(), D.stream())
+
+    def run(self, y_d, positions_override=None, trace=None, on_iter=None, events=False):
+        t = D.torch()
+        cfg, dop, eng = self.cfg, self.dop, self.eng
+        iters = cfg.max_iters
+        h, w, c = dop.shape
+        if cfg.init == "interp":
+            raise NotImplementedError("init='interp' (Gaussian inpainting start) is not on the "
+                                      "B200 path yet; use init='adjoint' (DESIGN.md)")
+        z, u, x, m, v = self.z, self.u, self.xa, self.xb, self.v
+        if cfg.init == "zero":
+            z.zero_()
+        else:
+            dop.adjoint(y_d, z)
+        u.zero_()
+        eng.has_positions = False
+        lo, hi = -0.5 * cfg.peak, 1.5 * cfg.peak
+        clip = dop.clip
+        self.events = ([[t.cuda.Event(enable_timing=True) for _ in range(4)]
+                        for _ in range(iters)] if events else None)
+        last, refresh_no = -1, 0
+        for it in range(iters):
+            ev = self.events[it] if events else None
+            if ev:
+                ev[0].record()
+            self._lincomb(m, z, 1.0, u, -1.0)                                  # m = z - u
+            dop.gap_update(None, None, eng.frac, m, y_d, lo, hi, x, self.resid_sq[it:it + 1],
+                           eng.gap_ws, rho=cfg.admm_rho)                         # x-update + clip
+            if ev:
+                ev[1].record()
+            self._lincomb(v, x, 1.0, u, 1.0)                                   # v = x + u
+            if (not eng.has_positions) or it - last >= cfg.match_refresh_interval:
+                if positions_override is not None:
+                    anc, pos = positions_override[refresh_no]
+                    eng.set_positions(np.asarray(anc), np.asarray(pos))
+                else:
+                    eng.refresh(v)
+                if trace is not None:
+                    a, pz, _ = eng.positions_host()
+                    trace.append((a.tolist(), pz.tolist()))
+                last = it
+                refresh_no += 1
+            if ev:
+                ev[2].record()
+            if eng.regularize(v, cfg.sigma_at(it)):
+                N.call("glr_normalize", eng.acc.data_ptr(), eng.cnt.data_ptr(), v.data_ptr(),
+                       h, w, c, eng.frac, z.data_ptr(), D.stream())
+                self._lincomb(z, z, 1.0, clip=clip)                            # z = clip(z)
+            else:
+                self._lincomb(z, v, 1.0, clip=clip)
+            self._lincomb(u, u, 1.0, x, 1.0, z, -1.0)                          # u = (u + x) - z
+            if ev:
+                ev[3].record()
+            if on_iter is not None:
+                on_iter(it, x)
+        return x
+
+
+def admm_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = None,
+               process_group=None):
+    """solvers.py:311-341 — scaled-form ADMM; the x-update uses the Woodbury
+    identity through the measurement-domain diagonal (divisor rho + gram)."""
+    _require_glr(cfg)
+    y = np.asarray(y)
+    _check_measurement(op, y)
+    t = D.torch()
+    t_start = time.perf_counter()
+    report = ReconReport()
+    runner = AdmmRunner(op, cfg, process_group=process_group)
+    y_d = runner.dop.upload_y(y)
+    ref_d = D.f64(ref) if ref is not None else None
+    ssims = []
+
+    def on_iter(it, x):
+        if ref_d is not None:
+            runner.sq_err(x, ref_d, it)
+            ssims.append(ssim(ref, np.clip(D.host(x), 0.0, cfg.peak), cfg.peak))
+
+    x = runner.run(y_d, on_iter=on_iter, events=True)
+    t.cuda.synchronize()
+    res = np.sqrt(D.host(runner.resid_sq)).tolist()
+    sqh = D.host(runner.sq) if ref_d is not None else None
+    n_el = float(np.prod(runner.dop.shape))
+    for it, (e0, e1, e2, e3) in enumerate(runner.events):
+        row = {"iteration": it, "residual": float(res[it]),
+               "match_ms": round(e1.elapsed_time(e2), 3),
+               "lowrank_ms": round(e2.elapsed_time(e3), 3),
+               "projection_ms": round(e0.elapsed_time(e1), 3)}
+        if sqh is not None:
+            mse = sqh[it] / n_el
+            row["psnr_db"] = PSNR_CAP_DB if mse == 0.0 else \
+                min(10.0 * np.log10(cfg.peak ** 2 / mse), PSNR_CAP_DB)
+            row["ssim"] = ssims[it]
+        report.add(**row)
+    report.total_ms = (time.perf_counter() - t_start) * 1e3
+    y_norm = float(np.linalg.norm(y.ravel()))
+    for k in range(21, cfg.max_iters + 1):
+        _check_divergence(res[:k], y_norm)
+    out = D.host(x).copy()
+    if runner.dop.clip:
+        out = np.clip(out, 0.0, cfg.peak)
+    return out, report
 
 
 def solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = None):

@@ -220,7 +220,42 @@ def gen_solves():
         ref_solvers.global_match = orig
 
 
+def gen_admm():
+    """A small ADMM-GLR run (solvers.py:311-341), refresh positions captured."""
+    rng = np.random.default_rng(707)
+    captured = []
+    orig = ref_solvers.global_match
+
+    def spy(x, exemplars, cfg, edge):
+        groups = orig(x, exemplars, cfg, edge)
+        captured.append((list(exemplars.anchors), [g.positions for g in groups]))
+        return groups
+
+    ref_solvers.global_match = spy
+    try:
+        h, w, c = 32, 36, 4
+        scene = blob_texture(rng, h, w, c)
+        masks = glr.bernoulli_masks(h, w, c, seed=21)
+        op = glr.cacti_operator(masks)
+        y = op.forward(scene)
+        mc = glr.MatchConfig(patch_size=4, group_size=8, max_corners=24, exemplar_stride=4)
+        cfg = glr.SolverConfig(algorithm="admm", regularizer="glr", max_iters=7, match=mc,
+                               admm_rho=0.01)
+        xr, rep = glr.admm_solve(op, y, cfg, ref=scene)
+        cases = {"scene": scene, "masks": masks, "y": y, "out": xr,
+                 "resid": np.array([r["residual"] for r in rep.rows]),
+                 "psnr": np.array([r["psnr_db"] for r in rep.rows]),
+                 "nref": np.array(len(captured))}
+        for j, (anc, pos) in enumerate(captured):
+            cases[f"anchors_{j}"] = np.array(anc, dtype=np.int32)
+            cases[f"positions_{j}"] = np.array(pos, dtype=np.int32)
+        np.savez_compressed(OUT / "admm.npz", **cases)
+    finally:
+        ref_solvers.global_match = orig
+
+
 if __name__ == "__main__":
+    gen_admm()
     gen_edges()
     gen_heat_topk()
     gen_topk_slices()

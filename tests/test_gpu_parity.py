@@ -198,3 +198,19 @@ def test_gap_solve_deterministic(rng):
     b, rb = G.gap_solve(op, y, cfg)
     assert np.array_equal(a, b)
     assert [r["residual"] for r in ra.rows] == [r["residual"] for r in rb.rows]
+
+
+def test_admm_solve_vs_reference_run():
+    """ADMM-GLR (solvers.py:311-341) on device vs a recorded reference run:
+    identical refresh traces, max |x - x_ref| <= 1e-6, PSNR within 0.05 dB."""
+    g = load_golden("admm")
+    op = G.cacti_operator(g["masks"])
+    cfg = G.SolverConfig(algorithm="admm", max_iters=7, admm_rho=0.01,
+                         match=G.MatchConfig(patch_size=4, group_size=8, max_corners=24,
+                                             exemplar_stride=4))
+    x, rep = G.solve(op, g["y"], cfg, ref=g["scene"])
+    assert np.abs(x - g["out"]).max() <= 1e-6
+    assert abs(rep.rows[-1]["psnr_db"] - float(g["psnr"][-1])) <= 0.05
+    ynorm = float(np.linalg.norm(g["y"]))
+    np.testing.assert_allclose([r["residual"] for r in rep.rows], g["resid"], rtol=1e-6,
+                               atol=1e-9 * ynorm)

@@ -105,3 +105,17 @@ def test_gap_solve_matches_reference_run(i):
     np.testing.assert_allclose(x, g[f"out{i}"], atol=1e-10, rtol=0)
     np.testing.assert_allclose(res, g[f"resid{i}"], rtol=1e-9)
     np.testing.assert_allclose(ps, g[f"psnr{i}"], atol=1e-8)
+
+
+def test_admm_solve_matches_reference_run():
+    g = load_golden("admm")
+    op = O.Operator("cacti", masks=g["masks"])
+    trace = []
+    x, res, ps = O.admm_solve(op, g["y"], 7, patch_size=4, group_size=8, max_corners=24,
+                              exemplar_stride=4, rho=0.01, ref=g["scene"], trace=trace)
+    assert len(trace) == int(g["nref"])
+    for j, (anc, pos) in enumerate(trace):
+        assert np.array_equal(np.array(anc, dtype=np.int32), g[f"anchors_{j}"])
+        assert np.array_equal(np.array(pos, dtype=np.int32), g[f"positions_{j}"])
+    np.testing.assert_allclose(x, g["out"], atol=1e-10, rtol=0)
+    np.testing.assert_allclose(ps, g["psnr"], atol=1e-8)

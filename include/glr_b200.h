@@ -210,6 +210,16 @@ int glr_gap_fourier(const int64_t* acc_d, const int32_t* cnt_d, int frac_bits,
                     int C, int clip, double lo, double hi, double rho, double* x_out_d,
                     double* resid_d, void* ws_d, void* stream);
 
+/* init="interp" (solvers.py:237-254). glr_interp_msfa: per channel
+ * gaussian_filter(xt) / gaussian_filter(mask) (0 where the latter <= 1e-12),
+ * bit-identical to scipy's symmetric correlate1d with mode "reflect";
+ * weights: the 2*radius+1 host-computed taps (HOST pointer), ws: 4*H*W*C
+ * doubles. glr_interp_cacti: xt / max(gram, 1e-12).                        */
+int glr_interp_msfa(const double* xt_d, const double* masks_d, int H, int W, int C,
+                    const double* weights, int radius, double* out_d, void* ws_d, void* stream);
+int glr_interp_cacti(const double* xt_d, const double* gram_d, int H, int W, int C,
+                     double* out_d, void* stream);
+
 /* glr_lincomb: out = clip((a*x + b*y) + c*z) elementwise, y/z optional (NULL),
  * in that evaluation order (the ADMM bookkeeping of solvers.py:327-334). */
 int glr_lincomb(const double* x_d, double a, const double* y_d, double b, const double* z_d,

@@ -402,6 +402,63 @@ def safe_div(num, den):
     return out
 
 
+def gaussian_weights(sigma=1.5, truncate=4.0):
+    """The taps scipy.ndimage.gaussian_filter builds (radius int(truncate*sigma+0.5),
+    exp(-x^2/(2 sigma^2)) normalised by its numpy sum)."""
+    r = int(truncate * float(sigma) + 0.5)
+    x = np.arange(-r, r + 1)
+    phi = np.exp(-0.5 / (sigma * sigma) * x ** 2)
+    return phi / phi.sum(), r
+
+
+def gaussian_filter_reflect(img, sigma=1.5):
+    """scipy.ndimage.gaussian_filter(img, sigma) on a 2-D float64 image, mode
+    "reflect", restated in the symmetric-kernel evaluation order scipy's
+    correlate1d uses: out = x[i] w[0] + sum_{j=-r..-1} (x[i+j] + x[i-j]) w[j],
+    axis 0 then axis 1. Bit-identical (tests/test_oracle_golden.py)."""
+    w, r = gaussian_weights(sigma)
+    a = np.asarray(img, dtype=np.float64)
+    for axis in (0, 1):
+        n = a.shape[axis]
+        idx = np.arange(n)
+
+        def refl(i):
+            i = np.mod(i, 2 * n)
+            return np.where(i < n, i, 2 * n - 1 - i)
+
+        take = lambda k: np.take(a, refl(idx + k), axis=axis)
+        acc = a * w[r]
+        for j in range(-r, 0):
+            acc = acc + (take(j) + take(-j)) * w[r + j]
+        a = acc
+    return a
+
+
+def interp_init(op: "Operator", y):
+    """solvers.py:237-254 (_interp_init): MSFA normalised-convolution
+    inpainting, CACTI adjoint / max(gram, 1e-12), plain adjoint otherwise."""
+    xt = op.adjoint(y)
+    if op.kind == "msfa":
+        out = np.zeros_like(xt)
+        for c in range(xt.shape[2]):
+            num = gaussian_filter_reflect(xt[:, :, c])
+            den = gaussian_filter_reflect(op.masks[:, :, c])
+            np.divide(num, den, out=out[:, :, c], where=den > 1e-12)
+        return out
+    if op.kind == "cacti":
+        return xt / np.maximum(op.gram, 1e-12)
+    return xt
+
+
+def init_x(op: "Operator", y, init="adjoint"):
+    """solvers.py:229-234 (_init_x)."""
+    if init == "zero":
+        return np.zeros(op.x_shape)
+    if init == "interp":
+        return interp_init(op, y)
+    return op.adjoint(y)
+
+
 def psnr(a, b, peak=1.0):
     """metrics.py:26-37 (cap 100 dB)."""
     mse = np.mean((np.asarray(a, float) - np.asarray(b, float)) ** 2)
@@ -413,7 +470,7 @@ def psnr(a, b, peak=1.0):
 def gap_solve(op: Operator, y, max_iters, patch_size=8, group_size=64, max_corners=512,
               exemplar_stride=6, edge_threshold=0.2, refresh=5, sigma0=0.10, sigma_min=0.003,
               peak=1.0, c_weight=2.0 * np.sqrt(2.0), eps=1e-16, min_separation=None,
-              clip=True, ref=None, trace=None, positions_override=None):
+              clip=True, ref=None, trace=None, positions_override=None, init="adjoint"):
     """solvers.py:284-308 with the "glr" regularizer (solvers.py:170-210).
 
     ``clip=False`` is the documented policy for complex (re, im) images
@@ -423,7 +480,7 @@ def gap_solve(op: Operator, y, max_iters, patch_size=8, group_size=64, max_corne
     Returns (x, residuals, psnrs)."""
     p = patch_size
     sep = -(-p // 4) if min_separation is None else min_separation
-    x = op.adjoint(y)
+    x = init_x(op, y, init)
     lo, hi = -0.5 * peak, 1.5 * peak
     positions, last = None, -1
     residuals, psnrs = [], []
@@ -472,13 +529,13 @@ def _glr_match(x, p, group_size, max_corners, exemplar_stride, edge_threshold, s
 def admm_solve(op: Operator, y, max_iters, patch_size=8, group_size=64, max_corners=512,
                exemplar_stride=6, edge_threshold=0.2, refresh=5, sigma0=0.10, sigma_min=0.003,
                peak=1.0, rho=0.01, c_weight=2.0 * np.sqrt(2.0), eps=1e-16, min_separation=None,
-               clip=True, ref=None, trace=None):
+               clip=True, ref=None, trace=None, init="adjoint"):
     """solvers.py:311-341 — scaled-form ADMM with the "glr" regularizer:
     m = z - u; x = clip(m + A^T((y - A m) / (rho + gram))); z = clip(R(x + u));
     u = u + x - z. Returns (x, residuals, psnrs)."""
     p = patch_size
     sep = -(-p // 4) if min_separation is None else min_separation
-    z = op.adjoint(y)
+    z = init_x(op, y, init)
     u = np.zeros_like(z)
     lo, hi = -0.5 * peak, 1.5 * peak
     positions, last = None, -1

@@ -77,6 +77,8 @@ SIGNATURES: dict[str, tuple] = {
     "glr_gap_fourier": (i32, [vp, vp, i32, vp, vp, vp, i32, i32, i32, i32, f64, f64, f64, vp, vp,
                               vp, vp]),
     "glr_lincomb": (i32, [vp, f64, vp, f64, vp, f64, i64, i32, f64, f64, vp, vp]),
+    "glr_interp_msfa": (i32, [vp, vp, i32, i32, i32, C.POINTER(C.c_double), i32, vp, vp, vp]),
+    "glr_interp_cacti": (i32, [vp, vp, i32, i32, i32, vp, vp]),
     "glr_sq_err": (i32, [vp, vp, i32, f64, vp, vp, vp]),
 }
 
@@ -137,7 +139,7 @@ KERNELS_PER_CALL = {
     "glr_scatter_add_f64": 1, "glr_normalize": 1, "glr_masksum_forward": 1,
     "glr_masksum_adjoint": 1, "glr_gap_masksum": 2, "glr_fourier_forward": 4,
     "glr_fourier_adjoint": 4, "glr_gap_fourier": 11, "glr_sq_err": 2, "glr_vcache_remap": 3,
-    "glr_lincomb": 1,
+    "glr_lincomb": 1, "glr_interp_msfa": 3, "glr_interp_cacti": 1,
 }
 launch_count = 0
 

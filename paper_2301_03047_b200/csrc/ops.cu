@@ -226,6 +226,90 @@ extern "C" int glr_gap_masksum(const int64_t* acc_d, const int32_t* cnt_d, int f
   return check_launch("final_sum_kernel");
 }
 
+// ---------------------------------------------------------------------------
+// init="interp" (solvers.py:237-254): scipy gaussian_filter(sigma=1.5) of the
+// adjoint and of the masks, per channel, mode "reflect", radius 6, evaluated
+// in scipy's symmetric correlate1d order: out = x[i] w[0] + sum over
+// j = -R..-1 of (x[i+j] + x[i-j]) w[j]; axis 0 then axis 1. Bit-identical to
+// scipy (the weights come from the host, computed with numpy like scipy).
+
+__device__ __forceinline__ int reflect_idx(int i, int n) {
+  i %= 2 * n;
+  if (i < 0) i += 2 * n;
+  return i < n ? i : 2 * n - 1 - i;
+}
+
+struct GaussW {
+  double w[16];  // w[R + j], j in [-R, R]
+  int R;
+};
+
+// one separable pass over both images (x and masks) along `axis` (0: rows, 1: cols)
+__global__ void gauss_pass_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                  int H, int W, int C, int axis, GaussW gw,
+                                  double* __restrict__ oa, double* __restrict__ ob) {
+  const int64_t total = (int64_t)H * W * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int ch = (int)(i % C);
+    const int64_t pix = i / C;
+    const int r = (int)(pix / W), c = (int)(pix % W);
+    const int n = axis == 0 ? H : W, pos = axis == 0 ? r : c;
+    auto at = [&](const double* src, int k) {
+      const int q = reflect_idx(k, n);
+      return axis == 0 ? src[((int64_t)q * W + c) * C + ch] : src[((int64_t)r * W + q) * C + ch];
+    };
+    double va = __dmul_rn(at(a, pos), gw.w[gw.R]);
+    double vb = __dmul_rn(at(b, pos), gw.w[gw.R]);
+    for (int j = -gw.R; j < 0; ++j) {
+      va = __dadd_rn(va, __dmul_rn(__dadd_rn(at(a, pos + j), at(a, pos - j)), gw.w[gw.R + j]));
+      vb = __dadd_rn(vb, __dmul_rn(__dadd_rn(at(b, pos + j), at(b, pos - j)), gw.w[gw.R + j]));
+    }
+    oa[i] = va;
+    ob[i] = vb;
+  }
+}
+
+__global__ void interp_div_kernel(const double* __restrict__ num, const double* __restrict__ den,
+                                  int64_t n, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = den[i] > 1e-12 ? __ddiv_rn(num[i], den[i]) : 0.0;
+}
+
+// CACTI interp: xt / max(gram, 1e-12) (solvers.py:252-253)
+__global__ void gram_div_kernel(const double* __restrict__ xt, const double* __restrict__ gram,
+                                int64_t npix, int C, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npix * C;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __ddiv_rn(xt[i], fmax(gram[i / C], 1e-12));
+}
+
+extern "C" int glr_interp_msfa(const double* xt_d, const double* masks_d, int H, int W, int C,
+                               const double* weights, int radius, double* out_d, void* ws_d,
+                               void* stream) {
+  GLR_REQUIRE(radius >= 0 && radius <= 7, GLR_ERR_UNSUPPORTED, "interp: radius %d", radius);
+  cudaStream_t st = (cudaStream_t)stream;
+  GaussW gw;
+  gw.R = radius;
+  for (int i = 0; i <= 2 * radius; ++i) gw.w[i] = weights[i];
+  const int64_t n = (int64_t)H * W * C;
+  double* t = reinterpret_cast<double*>(ws_d);  // 4 x n doubles
+  gauss_pass_kernel<<<kGapBlocks * 4, gap::THREADS, 0, st>>>(xt_d, masks_d, H, W, C, 0, gw, t,
+                                                             t + n);
+  gauss_pass_kernel<<<kGapBlocks * 4, gap::THREADS, 0, st>>>(t, t + n, H, W, C, 1, gw, t + 2 * n,
+                                                             t + 3 * n);
+  interp_div_kernel<<<kGapBlocks * 4, gap::THREADS, 0, st>>>(t + 2 * n, t + 3 * n, n, out_d);
+  return check_launch("interp_msfa");
+}
+
+extern "C" int glr_interp_cacti(const double* xt_d, const double* gram_d, int H, int W, int C,
+                                double* out_d, void* stream) {
+  gram_div_kernel<<<kGapBlocks * 4, gap::THREADS, 0, (cudaStream_t)stream>>>(
+      xt_d, gram_d, (int64_t)H * W, C, out_d);
+  return check_launch("interp_cacti");
+}
+
 extern "C" int glr_lincomb(const double* x_d, double a, const double* y_d, double b,
                            const double* z_d, double c, int64_t n, int clip, double lo, double hi,
                            double* out_d, void* stream) {

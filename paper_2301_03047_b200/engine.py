@@ -75,6 +75,42 @@ class DeviceOperator:
             N.call("glr_masksum_adjoint", y_d.data_ptr(), self.masks.data_ptr(), h, w, c,
                    x_d.data_ptr(), D.stream())
 
+    def init_x(self, y_d, x_d, init: str = "adjoint"):
+        """solvers.py:229-254 (_init_x / _interp_init) into x_d. "interp":
+        MSFA normalised Gaussian inpainting (bit-identical to scipy's
+        gaussian_filter(sigma=1.5)), CACTI adjoint / max(gram, 1e-12),
+        plain adjoint otherwise."""
+        if init == "zero":
+            x_d.zero_()
+            return
+        if init == "interp" and self.kind == "msfa":
+            t = D.torch()
+            h, w, c = self.shape
+            if getattr(self, "_xt", None) is None:
+                self._xt = D.empty((h, w, c), t.float64)
+                self._interp_ws = D.empty((4 * h * w * c,), t.float64)
+                # scipy.ndimage _gaussian_kernel1d(sigma=1.5, radius=int(4*1.5+0.5))
+                radius = int(4.0 * 1.5 + 0.5)
+                xs = np.arange(-radius, radius + 1)
+                phi = np.exp(-0.5 / (1.5 * 1.5) * xs ** 2)
+                self._gauss = np.ascontiguousarray(phi / phi.sum(), dtype=np.float64)
+                self._gauss_r = radius
+            self.adjoint(y_d, self._xt)
+            wts = self._gauss.ctypes.data_as(N.C.POINTER(N.C.c_double))
+            N.call("glr_interp_msfa", self._xt.data_ptr(), self.masks.data_ptr(), h, w, c, wts,
+                   self._gauss_r, x_d.data_ptr(), self._interp_ws.data_ptr(), D.stream())
+            return
+        if init == "interp" and self.kind == "cacti":
+            t = D.torch()
+            h, w, c = self.shape
+            if getattr(self, "_xt", None) is None:
+                self._xt = D.empty((h, w, c), t.float64)
+            self.adjoint(y_d, self._xt)
+            N.call("glr_interp_cacti", self._xt.data_ptr(), self.gram.data_ptr(), h, w, c,
+                   x_d.data_ptr(), D.stream())
+            return
+        self.adjoint(y_d, x_d)
+
     def gap_update(self, acc, cnt, frac, x_in, y_d, lo, hi, x_out, resid_out, ws, rho=0.0):
         """x_out = clip(z + A^T safe_div(y - A z, gram)); resid_out = ||y - A x_out||^2,
         z = acc/cnt where covered else x_in (acc None: z = x_in)."""

@@ -148,12 +148,7 @@ def _check_divergence(residuals: list[float], y_norm: float) -> None:
 def _init_device(dop: DeviceOperator, y_d, cfg: SolverConfig):
     t = D.torch()
     x = D.zeros(dop.shape, t.float64)
-    if cfg.init == "zero":
-        return x
-    if cfg.init == "interp":
-        raise NotImplementedError("init='interp' (Gaussian inpainting start) is not on the B200 "
-                                  "path yet; use init='adjoint' (DESIGN.md)")
-    dop.adjoint(y_d, x)
+    dop.init_x(y_d, x, cfg.init)
     return x
 
 
@@ -224,13 +219,7 @@ class GapRunner:
         cfg, dop, eng = self.cfg, self.dop, self.eng
         iters = cfg.max_iters
         x, x_next = self.xa, self.xb
-        if cfg.init == "interp":
-            raise NotImplementedError("init='interp' (Gaussian inpainting start) is not on the "
-                                      "B200 path yet; use init='adjoint' (DESIGN.md)")
-        if cfg.init == "zero":
-            x.zero_()
-        else:
-            dop.adjoint(y_d, x)
+        dop.init_x(y_d, x, cfg.init)
         eng.has_positions = False
         lo, hi = -0.5 * cfg.peak, 1.5 * cfg.peak
         self.events = ([[t.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -346,14 +335,8 @@ class AdmmRunner(GapRunner):
         cfg, dop, eng = self.cfg, self.dop, self.eng
         iters = cfg.max_iters
         h, w, c = dop.shape
-        if cfg.init == "interp":
-            raise NotImplementedError("init='interp' (Gaussian inpainting start) is not on the "
-                                      "B200 path yet; use init='adjoint' (DESIGN.md)")
         z, u, x, m, v = self.z, self.u, self.xa, self.xb, self.v
-        if cfg.init == "zero":
-            z.zero_()
-        else:
-            dop.adjoint(y_d, z)
+        dop.init_x(y_d, z, cfg.init)
         u.zero_()
         eng.has_positions = False
         lo, hi = -0.5 * cfg.peak, 1.5 * cfg.peak

@@ -254,7 +254,55 @@ def gen_admm():
         ref_solvers.global_match = orig
 
 
+def gen_interp():
+    """init="interp" (solvers.py:237-254): the reference's _interp_init on
+    MSFA / CACTI / Fourier operators, and one MSFA gap_solve started from it."""
+    rng = np.random.default_rng(808)
+    cases = {}
+    mm = glr.msfa_pattern("periodic-4x4", 16, 24, 20)
+    x16 = f32(rng.random((24, 20, 16)))
+    mop = glr.msfa_operator(mm)
+    my = mop.forward(x16)
+    cases.update(msfa_masks=mm, msfa_y=my, msfa_init=ref_solvers._interp_init(mop, my))
+    masks = glr.bernoulli_masks(18, 22, 6, seed=5)
+    cop = glr.cacti_operator(masks)
+    cy = cop.forward(f32(rng.random((18, 22, 6))))
+    cases.update(cacti_masks=masks, cacti_y=cy, cacti_init=ref_solvers._interp_init(cop, cy))
+    captured = []
+    orig = ref_solvers.global_match
+
+    def spy(x, exemplars, cfg, edge):
+        groups = orig(x, exemplars, cfg, edge)
+        captured.append((list(exemplars.anchors), [g.positions for g in groups]))
+        return groups
+
+    ref_solvers.global_match = spy
+    try:
+        scene = blob_texture(rng, 32, 32, 16)
+        sm = glr.msfa_pattern("periodic-4x4", 16, 32, 32)
+        op = glr.msfa_operator(sm)
+        y = op.forward(scene)
+        mc = glr.MatchConfig(patch_size=4, group_size=8, max_corners=24, exemplar_stride=4)
+        cfg = glr.SolverConfig(regularizer="glr", max_iters=6, match=mc, init="interp")
+        xr, rep = glr.gap_solve(op, y, cfg, ref=scene)
+        cases.update(solve_scene=scene, solve_masks=sm, solve_y=y, solve_out=xr,
+                     solve_resid=np.array([r["residual"] for r in rep.rows]),
+                     solve_psnr=np.array([r["psnr_db"] for r in rep.rows]),
+                     solve_nref=np.array(len(captured)))
+        for j, (anc, pos) in enumerate(captured):
+            cases[f"solve_anchors_{j}"] = np.array(anc, dtype=np.int32)
+            cases[f"solve_positions_{j}"] = np.array(pos, dtype=np.int32)
+    finally:
+        ref_solvers.global_match = orig
+    np.savez_compressed(OUT / "interp.npz", **cases)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[f"gen_{name}"]()
+        sys.exit(0)
+    gen_interp()
     gen_admm()
     gen_edges()
     gen_heat_topk()

@@ -214,3 +214,38 @@ def test_admm_solve_vs_reference_run():
     ynorm = float(np.linalg.norm(g["y"]))
     np.testing.assert_allclose([r["residual"] for r in rep.rows], g["resid"], rtol=1e-6,
                                atol=1e-9 * ynorm)
+
+
+def test_interp_init_vs_golden():
+    """init="interp" (solvers.py:237-254) on device: the MSFA Gaussian
+    normalised convolution is bit-identical to the reference (scipy), CACTI
+    adjoint / max(gram, 1e-12) within 1e-13."""
+    from paper_2301_03047_b200.engine import DeviceOperator
+    import torch
+    g = load_golden("interp")
+    for kind, build, atol in (("msfa", G.msfa_operator, 0.0), ("cacti", G.cacti_operator, 1e-13)):
+        op = build(g[f"{kind}_masks"])
+        dop = DeviceOperator(op)
+        x = torch.empty(dop.shape, dtype=torch.float64, device="cuda")
+        dop.init_x(dop.upload_y(g[f"{kind}_y"]), x, "interp")
+        out = x.cpu().numpy()
+        if atol == 0.0:
+            assert np.array_equal(out, g[f"{kind}_init"]), kind
+        else:
+            np.testing.assert_allclose(out, g[f"{kind}_init"], atol=atol, rtol=0)
+
+
+def test_gap_solve_interp_init_vs_reference_run():
+    g = load_golden("interp")
+    op = G.msfa_operator(g["solve_masks"])
+    cfg = G.SolverConfig(regularizer="glr", max_iters=6, init="interp",
+                         match=G.MatchConfig(patch_size=4, group_size=8, max_corners=24,
+                                             exemplar_stride=4))
+    trace = []
+    x, rep = G.gap_solve(op, g["solve_y"], cfg, ref=g["solve_scene"], trace=trace)
+    assert len(trace) == int(g["solve_nref"])
+    for j, (anc, pos) in enumerate(trace):
+        assert np.array_equal(np.array(anc, dtype=np.int32), g[f"solve_anchors_{j}"]), j
+        assert np.array_equal(np.array(pos, dtype=np.int32), g[f"solve_positions_{j}"]), j
+    assert np.abs(x - g["solve_out"]).max() <= 1e-6
+    assert abs(rep.rows[-1]["psnr_db"] - float(g["solve_psnr"][-1])) <= 0.05

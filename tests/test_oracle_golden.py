@@ -119,3 +119,25 @@ def test_admm_solve_matches_reference_run():
         assert np.array_equal(np.array(pos, dtype=np.int32), g[f"positions_{j}"])
     np.testing.assert_allclose(x, g["out"], atol=1e-10, rtol=0)
     np.testing.assert_allclose(ps, g["psnr"], atol=1e-8)
+
+
+def test_interp_init_bitwise():
+    g = load_golden("interp")
+    op = O.Operator("msfa", masks=g["msfa_masks"])
+    assert np.array_equal(O.interp_init(op, g["msfa_y"]), g["msfa_init"])
+    op = O.Operator("cacti", masks=g["cacti_masks"])
+    np.testing.assert_allclose(O.interp_init(op, g["cacti_y"]), g["cacti_init"], atol=1e-13, rtol=0)
+
+
+def test_gap_solve_interp_init_matches_reference_run():
+    g = load_golden("interp")
+    op = O.Operator("msfa", masks=g["solve_masks"])
+    trace = []
+    x, res, ps = O.gap_solve(op, g["solve_y"], 6, patch_size=4, group_size=8, max_corners=24,
+                             exemplar_stride=4, ref=g["solve_scene"], trace=trace, init="interp")
+    assert len(trace) == int(g["solve_nref"])
+    for j, (anc, pos) in enumerate(trace):
+        assert np.array_equal(np.array(anc, dtype=np.int32), g[f"solve_anchors_{j}"])
+        assert np.array_equal(np.array(pos, dtype=np.int32), g[f"solve_positions_{j}"])
+    np.testing.assert_allclose(x, g["solve_out"], atol=1e-10, rtol=0)
+    np.testing.assert_allclose(ps, g["solve_psnr"], atol=1e-8)

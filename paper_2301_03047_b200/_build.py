@@ -27,6 +27,11 @@ NVCC_FLAGS = ARCH + [
 ]
 
 
+def _extra_flags() -> list[str]:
+    """Dev-only extra nvcc flags (e.g. GLR_NVCC_EXTRA=-DGLR_EIG_STATS)."""
+    return os.environ.get("GLR_NVCC_EXTRA", "").split()
+
+
 def _nvcc() -> str:
     for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
         if cand and os.path.exists(cand):
@@ -36,7 +41,7 @@ def _nvcc() -> str:
 
 def _compile(src: Path, verbose: bool) -> tuple[Path, str]:
     obj = BUILD / (src.stem + ".o")
-    cmd = [_nvcc(), *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+    cmd = [_nvcc(), *NVCC_FLAGS, *_extra_flags(), "-c", str(src), "-o", str(obj)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src.name}:\n{res.stderr}")

@@ -26,7 +26,8 @@ namespace glr {
 namespace wn {
 constexpr int KMAX = 64;
 constexpr int LD = KMAX + 4;      // row stride of Wm in the apply kernel (== 4 mod 16)
-constexpr int ELD = KMAX + 2;     // row stride of G / V in the eigen kernel
+constexpr int GLD = KMAX + 2;     // row stride of G in the eigen kernel (pair reads: distinct banks)
+constexpr int VLD = KMAX + 1;     // row stride of V^T in the eigen kernel
 constexpr int GROWS = 32;         // rows of M per Gram tile
 constexpr int GRS = GROWS + 4;    // column stride of the Gram tiles (== 4 mod 16)
 constexpr int AROWS = 32;         // rows of M per apply tile (one 8-row tile row per warp)
@@ -164,6 +165,11 @@ __global__ void __launch_bounds__(wn::GRAM_THREADS) gram_kernel(GroupSrc s, int 
 // ---------------------------------------------------------------------------
 // K2: eigen-decomposition + shrinkage -> Wm (in place over G)
 
+#ifdef GLR_EIG_STATS
+// dev statistics: groups per sweep count (cold [0, 32), warm [32, 64))
+__device__ unsigned int g_eig_hist[64];
+#endif
+
 struct EigArgs {
   double* G;  // n x 64 x 64: G in, Wm out
   int n, K;
@@ -173,66 +179,86 @@ struct EigArgs {
   const uint8_t* warm_flags;
 };
 
+// Circle-schedule pair k of round r over 64 indices (every pair meets once
+// in 63 rounds). "first" elements are consecutive in k, and so are the
+// "second" ones, which keeps the shared-memory accesses below conflict-free.
+__device__ __forceinline__ void jacobi_pair(int k, int r, int& p, int& q) {
+  p = 0;
+  if (k != 0) {
+    p = k + r;  // 1 + (k - 1 + r) mod 63
+    if (p > wn::KMAX - 1) p -= wn::KMAX - 1;
+  }
+  q = 1 + (wn::KMAX - 2 - k + r);
+  if (q > wn::KMAX - 1) q -= wn::KMAX - 1;
+}
+
+// (u, v) <- (c u - s v, s u + c v) in one fixed evaluation order, so the
+// (A, B) and (B, A) blocks of G stay exact transposes of each other.
+__device__ __forceinline__ void jrot(double c, double s, double& u, double& v) {
+  const double nu = __fma_rn(c, u, -__dmul_rn(s, v));
+  const double nv = __fma_rn(s, u, __dmul_rn(c, v));
+  u = nu;
+  v = nv;
+}
+
 __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
   using namespace wn;
-  constexpr int LD = ELD;  // row stride of G / V here (Jacobi column access pattern)
   extern __shared__ __align__(16) double sm[];
-  double* G = sm;             // KMAX x LD
-  double* V = G + KMAX * LD;  // KMAX x LD
+  double* G = sm;               // KMAX x GLD, exactly symmetric throughout
+  double* Vt = G + KMAX * GLD;  // KMAX x VLD: Vt[j][i] = V[i][j] (row j = eigenvector j)
+  __shared__ double cs_c[KMAX / 2], cs_s[KMAX / 2], cs_dp[KMAX / 2], cs_dq[KMAX / 2];
+  __shared__ unsigned cs_rot;
   __shared__ double ratio[KMAX];
   __shared__ double s_tiny;
   const int g = blockIdx.x;
   if (g >= a.n) return;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int K = a.K;
-  const int bi = tid >> 4, bj = tid & 15;  // 4x4 blocks for the small products
+  // small products: rows 4*bi + ii, columns bj + 16*jj (conflict-free operand reads)
+  const int bi = tid >> 4, bj = tid & 15;
   double* Gg = a.G + (size_t)g * GSZ;
   double* vc = a.vcache ? a.vcache + (size_t)g * GSZ : nullptr;
   const bool warm = vc && (a.warm == 1 || (a.warm == 2 && a.warm_flags[g]));
 
   for (int t = tid; t < GSZ / 2; t += EIG_THREADS) {
     const int i = (2 * t) >> 6, j = (2 * t) & 63;
-    *reinterpret_cast<double2*>(&G[i * LD + j]) = reinterpret_cast<const double2*>(Gg)[t];
-    if (warm) {
-      *reinterpret_cast<double2*>(&V[i * LD + j]) = reinterpret_cast<const double2*>(vc)[t];
-    } else {
-      V[i * LD + j] = (i == j) ? 1.0 : 0.0;
-      V[i * LD + j + 1] = (i == j + 1) ? 1.0 : 0.0;
-    }
+    *reinterpret_cast<double2*>(&G[i * GLD + j]) = reinterpret_cast<const double2*>(Gg)[t];
+  }
+  for (int t = tid; t < GSZ; t += EIG_THREADS) {
+    const int j = t >> 6, i = t & 63;
+    Vt[j * VLD + i] = warm ? vc[t] : (i == j ? 1.0 : 0.0);
   }
   __syncthreads();
   if (tid == 0) {
     double tr = 0.0;
-    for (int i = 0; i < K; ++i) tr += fabs(G[i * LD + i]);
+    for (int i = 0; i < K; ++i) tr += fabs(G[i * GLD + i]);
     s_tiny = 1e-17 * tr;
   }
   if (warm) {
     // Warm start from this group's eigenvectors of a previous iteration:
-    // G <- Vp^T G Vp (two 64^3 products through the Wm-sized scratch in
-    // global memory is avoided: Y = G Vp goes to registers, then to G's rows
-    // after a barrier), V stays Vp. The sweeps then only remove a small
-    // off-diagonal residue.
+    // G <- Vp^T G Vp (Y = G Vp to registers, then to G after a barrier),
+    // V stays Vp. The sweeps then only remove a small off-diagonal residue.
     double y[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) y[i][j] = 0.0;
     for (int k = 0; k < KMAX; ++k) {
-      const double2 v01 = *reinterpret_cast<const double2*>(&V[k * LD + 4 * bj]);
-      const double2 v23 = *reinterpret_cast<const double2*>(&V[k * LD + 4 * bj + 2]);
-      const double vv[4] = {v01.x, v01.y, v23.x, v23.y};
+      double gk[4], vk[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const double gk = G[(4 * bi + i) * LD + k];
+      for (int i = 0; i < 4; ++i) gk[i] = G[(4 * bi + i) * GLD + k];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) y[i][j] = fma(gk, vv[j], y[i][j]);
-      }
+      for (int j = 0; j < 4; ++j) vk[j] = Vt[(bj + 16 * j) * VLD + k];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) y[i][j] = fma(gk[i], vk[j], y[i][j]);
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) G[(4 * bi + i) * LD + 4 * bj + j] = y[i][j];
+      for (int j = 0; j < 4; ++j) G[(4 * bi + i) * GLD + bj + 16 * j] = y[i][j];
     __syncthreads();
     double z[4][4];  // G' = Vp^T Y
 #pragma unroll
@@ -240,42 +266,43 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) z[i][j] = 0.0;
     for (int k = 0; k < KMAX; ++k) {
-      const double2 v01 = *reinterpret_cast<const double2*>(&V[k * LD + 4 * bi]);
-      const double2 v23 = *reinterpret_cast<const double2*>(&V[k * LD + 4 * bi + 2]);
-      const double vv[4] = {v01.x, v01.y, v23.x, v23.y};
-      const double2 y01 = *reinterpret_cast<const double2*>(&G[k * LD + 4 * bj]);
-      const double2 y23 = *reinterpret_cast<const double2*>(&G[k * LD + 4 * bj + 2]);
-      const double yy[4] = {y01.x, y01.y, y23.x, y23.y};
+      double uk[4], yk[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) uk[i] = Vt[(4 * bi + i) * VLD + k];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) yk[j] = G[k * GLD + bj + 16 * j];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) z[i][j] = fma(vv[i], yy[j], z[i][j]);
+        for (int j = 0; j < 4; ++j) z[i][j] = fma(uk[i], yk[j], z[i][j]);
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) G[(4 * bi + i) * LD + 4 * bj + j] = z[i][j];
+      for (int j = 0; j < 4; ++j) G[(4 * bi + i) * GLD + bj + 16 * j] = z[i][j];
     __syncthreads();
     // symmetrise (the product is symmetric up to rounding)
     for (int t = tid; t < GSZ; t += EIG_THREADS) {
       const int i = t >> 6, j = t & 63;
       if (i < j) {
-        const double v = 0.5 * (G[i * LD + j] + G[j * LD + i]);
-        G[i * LD + j] = v;
-        G[j * LD + i] = v;
+        const double v = 0.5 * (G[i * GLD + j] + G[j * GLD + i]);
+        G[i * GLD + j] = v;
+        G[j * GLD + i] = v;
       }
     }
   }
   __syncthreads();
   const double tiny = s_tiny;
 
-  // ---- parallel cyclic Jacobi: 32 disjoint rotations per round (circle
-  // schedule over 64 indices); 8 threads per pair, 2 barriers per round. A
-  // rotation is skipped once |g_pq| is at rounding level relative to its
-  // diagonal pair (or to 1e-17 trace).
-  const int pk = tid >> 3, l = tid & 7;
-  for (int sweep = 0; sweep < MAX_SWEEPS; ++sweep) {
+  // ---- parallel cyclic Jacobi, 32 disjoint rotations per round. Phase 1
+  // (warp 0): the rotation of pair `lane`. Phase 2 (all): one pass over G in
+  // 2x2 blocks -- warp w owns row pairs 4w..4w+3, lane l column pair l, so
+  // G <- J^T G J costs one read and one write per element -- and V <- V J on
+  // the transposed V (contiguous rows). A rotation is skipped once |g_pq| is
+  // at rounding level relative to its diagonal pair (or to 1e-17 trace).
+  int sweep = 0;
+  for (; sweep < MAX_SWEEPS; ++sweep) {
     // A sweep changes G only if some pair passes the rotation test on the
     // current G (otherwise no round rotates, by induction): test all pairs
     // up front and stop without paying for a no-op sweep.
@@ -283,68 +310,81 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
     for (int t = tid; t < GSZ; t += EIG_THREADS) {
       const int i = t >> 6, j = t & 63;
       if (i < j)
-        need |= fabs(G[i * LD + j]) >
-                fmax(kRotTol * sqrt(fabs(G[i * LD + i] * G[j * LD + j])), tiny);
+        need |= fabs(G[i * GLD + j]) >
+                fmax(kRotTol * sqrt(fabs(G[i * GLD + i] * G[j * GLD + j])), tiny);
     }
     if (!__syncthreads_or(need)) break;
     for (int round = 0; round < KMAX - 1; ++round) {
-      int p = 0, q;
-      if (pk != 0) {
-        p = 1 + (pk - 1 + round);
-        if (p > KMAX - 1) p -= KMAX - 1;
-      }
-      q = 1 + (KMAX - 2 - pk + round);
-      if (q > KMAX - 1) q -= KMAX - 1;
-      if (p > q) {
-        const int t = p;
-        p = q;
-        q = t;
-      }
-      const double app = G[p * LD + p], aqq = G[q * LD + q], apq = G[p * LD + q];
-      __syncwarp();
-      const bool rot = fabs(apq) > fmax(kRotTol * sqrt(fabs(app * aqq)), tiny);
-      double c = 1.0, sn = 0.0;
-      if (rot) {
-        const double tau = (aqq - app) / (2.0 * apq);
-        const double t = fabs(tau) > 1e150
-                             ? 0.5 / tau
-                             : (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-        c = 1.0 / sqrt(1.0 + t * t);
-        sn = t * c;
-        // rows p, q: G <- J^T G (all loads issued before any store)
-        double gp[KMAX / 8], gq[KMAX / 8];
-#pragma unroll
-        for (int i = 0; i < KMAX / 8; ++i) {
-          gp[i] = G[p * LD + l + 8 * i];
-          gq[i] = G[q * LD + l + 8 * i];
+      if (warp == 0) {
+        int p, q;
+        jacobi_pair(lane, round, p, q);
+        const double app = G[p * GLD + p], aqq = G[q * GLD + q], apq = G[p * GLD + q];
+        const bool rot = fabs(apq) > fmax(kRotTol * sqrt(fabs(app * aqq)), tiny);
+        double c = 1.0, sn = 0.0, t = 0.0;
+        if (rot) {
+          const double tau = (aqq - app) / (2.0 * apq);
+          t = fabs(tau) > 1e150 ? 0.5 / tau
+                                : (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+          c = 1.0 / sqrt(1.0 + t * t);
+          sn = t * c;
         }
-#pragma unroll
-        for (int i = 0; i < KMAX / 8; ++i) {
-          G[p * LD + l + 8 * i] = c * gp[i] - sn * gq[i];
-          G[q * LD + l + 8 * i] = sn * gp[i] + c * gq[i];
-        }
+        cs_c[lane] = c;
+        cs_s[lane] = sn;
+        cs_dp[lane] = app - t * apq;
+        cs_dq[lane] = aqq + t * apq;
+        const unsigned m = __ballot_sync(0xffffffffu, rot);
+        if (lane == 0) cs_rot = m;
       }
       __syncthreads();
-      if (rot) {
-        // columns p, q: G <- G J, V <- V J
+      const unsigned mask = cs_rot;
+      if (mask) {
+        // Branch-free block update: a skipped rotation is (c, s) = (1, 0),
+        // which is exact. Blocks below the diagonal are handled transposed
+        // (x01 <-> x10, A <-> B) so both halves use the same operation order.
+        int pB, qB;
+        jacobi_pair(lane, round, pB, qB);
+        const double cB = cs_c[lane], sB = cs_s[lane];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          double gp[KMAX / 16], gq[KMAX / 16], vp[KMAX / 16], vq[KMAX / 16];
-#pragma unroll
-          for (int i = 0; i < KMAX / 16; ++i) {
-            const int r = l + 8 * (i + h * (KMAX / 16));
-            gp[i] = G[r * LD + p];
-            gq[i] = G[r * LD + q];
-            vp[i] = V[r * LD + p];
-            vq[i] = V[r * LD + q];
+        for (int ab = 0; ab < 4; ++ab) {
+          const int A = 4 * warp + ab;
+          int pA, qA;
+          jacobi_pair(A, round, pA, qA);
+          const double cA = cs_c[A], sA = cs_s[A];
+          double x00 = G[pA * GLD + pB], x01 = G[pA * GLD + qB];
+          double x10 = G[qA * GLD + pB], x11 = G[qA * GLD + qB];
+          const bool lo = A <= lane;
+          const double c1 = lo ? cA : cB, s1 = lo ? sA : sB;
+          const double c2 = lo ? cB : cA, s2 = lo ? sB : sA;
+          double y01 = lo ? x01 : x10, y10 = lo ? x10 : x01;
+          jrot(c1, s1, x00, y10);
+          jrot(c1, s1, y01, x11);
+          jrot(c2, s2, x00, y01);
+          jrot(c2, s2, y10, x11);
+          x01 = lo ? y01 : y10;
+          x10 = lo ? y10 : y01;
+          if (A == lane) {  // closed form on the rotated pair's own 2x2 block
+            x00 = cs_dp[A];
+            x11 = cs_dq[A];
+            x01 = x10 = 0.0;
           }
+          G[pA * GLD + pB] = x00;
+          G[pA * GLD + qB] = x01;
+          G[qA * GLD + pB] = x10;
+          G[qA * GLD + qB] = x11;
+        }
 #pragma unroll
-          for (int i = 0; i < KMAX / 16; ++i) {
-            const int r = l + 8 * (i + h * (KMAX / 16));
-            G[r * LD + p] = c * gp[i] - sn * gq[i];
-            G[r * LD + q] = sn * gp[i] + c * gq[i];
-            V[r * LD + p] = c * vp[i] - sn * vq[i];
-            V[r * LD + q] = sn * vp[i] + c * vq[i];
+        for (int ab = 0; ab < 4; ++ab) {
+          const int A = 4 * warp + ab;
+          int pA, qA;
+          jacobi_pair(A, round, pA, qA);
+          const double cA = cs_c[A], sA = cs_s[A];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int i = lane + 32 * h;
+            double vp = Vt[pA * VLD + i], vq = Vt[qA * VLD + i];
+            jrot(cA, sA, vp, vq);
+            Vt[pA * VLD + i] = vp;
+            Vt[qA * VLD + i] = vq;
           }
         }
       }
@@ -352,17 +392,17 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
     }
   }
 
+#ifdef GLR_EIG_STATS
+  if (tid == 0) atomicAdd(&g_eig_hist[warm ? 32 + sweep : sweep], 1u);
+#endif
   if (vc) {
-    for (int t = tid; t < GSZ / 2; t += EIG_THREADS) {
-      const int i = (2 * t) >> 6, j = (2 * t) & 63;
-      reinterpret_cast<double2*>(vc)[t] = *reinterpret_cast<const double2*>(&V[i * LD + j]);
-    }
+    for (int t = tid; t < GSZ; t += EIG_THREADS) vc[t] = Vt[(t >> 6) * VLD + (t & 63)];
   }
   // ---- shrinkage weights (lowrank.py:58-64) ----
   if (tid < KMAX) {
     double r = 0.0;
     if (tid < K) {
-      const double lam = G[tid * LD + tid];
+      const double lam = G[tid * GLD + tid];
       const double s = sqrt(fmax(lam, 0.0));
       double w;
       if (a.uniform_weight >= 0.0) {
@@ -377,7 +417,7 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
     ratio[tid] = r;
   }
   __syncthreads();
-  // Wm = V diag(ratio) V^T -> global (4x4 block per thread)
+  // Wm = V diag(ratio) V^T -> global
   double o[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -388,21 +428,18 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
     if (rk == 0.0) continue;
     double x[4], y[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      x[i] = V[(4 * bi + i) * LD + k] * rk;
-      y[i] = V[(4 * bj + i) * LD + k];
-    }
+    for (int i = 0; i < 4; ++i) x[i] = Vt[k * VLD + 4 * bi + i] * rk;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) y[j] = Vt[k * VLD + bj + 16 * j];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) o[i][j] = fma(x[i], y[j], o[i][j]);
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    double2* dst = reinterpret_cast<double2*>(Gg + (4 * bi + i) * KMAX + 4 * bj);
-    dst[0] = make_double2(o[i][0], o[i][1]);
-    dst[1] = make_double2(o[i][2], o[i][3]);
-  }
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) Gg[(4 * bi + i) * KMAX + bj + 16 * j] = o[i][j];
 }
 
 // ---------------------------------------------------------------------------
@@ -581,7 +618,7 @@ static int blocks_for(int64_t n, int threads = 256) {
 }
 
 constexpr size_t kGramSmem = 2 * wn::KMAX * wn::GRS * sizeof(double);
-constexpr size_t kEigSmem = 2 * wn::KMAX * wn::ELD * sizeof(double);
+constexpr size_t kEigSmem = wn::KMAX * (wn::GLD + wn::VLD) * sizeof(double);
 constexpr size_t kApplySmem = (wn::KMAX * wn::LD + 2 * wn::KMAX * wn::ARS) * sizeof(double);
 
 // Gram -> eigen/shrink -> apply for n groups; ws holds n x 64 x 64 doubles.
@@ -612,6 +649,17 @@ static int run_wnnm(const GroupSrc& s, int n, const EigArgs& ea_in, double scale
 }  // namespace glr
 
 using namespace glr;
+
+#ifdef GLR_EIG_STATS
+extern "C" int glr_debug_eig_hist(unsigned int* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_eig_hist, sizeof(unsigned int) * 64);
+  if (reset) {
+    unsigned int z[64] = {};
+    cudaMemcpyToSymbol(g_eig_hist, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 extern "C" size_t glr_wnnm_workspace(int G, int K) {
   return (size_t)std::max(G, 1) * wn::GSZ * sizeof(double) + 256;

@@ -257,6 +257,17 @@ class GapRunner:
         return x
 
 
+def _final_host(runner, x) -> np.ndarray:
+    """The solver's return value: clip(x, 0, peak) (solvers.py:307) computed on
+    device into the runner's spare iterate buffer, then one pinned D2H copy."""
+    if not runner.dop.clip:
+        return D.host_pinned(x)
+    spare = runner.xb if x.data_ptr() == runner.xa.data_ptr() else runner.xa
+    N.call("glr_lincomb", x.data_ptr(), 1.0, None, 0.0, None, 0.0, int(x.numel()), 1, 0.0,
+           float(runner.cfg.peak), spare.data_ptr(), D.stream())
+    return D.host_pinned(spare)
+
+
 def gap_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = None,
               process_group=None, positions_override=None, trace=None):
     """solvers.py:284-308 — regularize, then project onto the measurement-
@@ -306,10 +317,7 @@ def gap_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = Non
     y_norm = float(np.linalg.norm(y.ravel()))
     for k in range(21, iters + 1):
         _check_divergence(res[:k], y_norm)
-    out = D.host(x).copy()
-    if dop.clip:
-        out = np.clip(out, 0.0, cfg.peak)
-    return out, report
+    return _final_host(runner, x), report
 
 
 class AdmmRunner(GapRunner):
@@ -421,10 +429,7 @@ def admm_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = No
     y_norm = float(np.linalg.norm(y.ravel()))
     for k in range(21, cfg.max_iters + 1):
         _check_divergence(res[:k], y_norm)
-    out = D.host(x).copy()
-    if runner.dop.clip:
-        out = np.clip(out, 0.0, cfg.peak)
-    return out, report
+    return _final_host(runner, x), report
 
 
 def solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = None):

@@ -179,17 +179,36 @@ struct EigArgs {
   const uint8_t* warm_flags;
 };
 
-// Circle-schedule pair k of round r over 64 indices (every pair meets once
-// in 63 rounds). "first" elements are consecutive in k, and so are the
-// "second" ones, which keeps the shared-memory accesses below conflict-free.
-__device__ __forceinline__ void jacobi_pair(int k, int r, int& p, int& q) {
-  p = 0;
-  if (k != 0) {
-    p = k + r;  // 1 + (k - 1 + r) mod 63
-    if (p > wn::KMAX - 1) p -= wn::KMAX - 1;
-  }
-  q = 1 + (wn::KMAX - 2 - k + r);
-  if (q > wn::KMAX - 1) q -= wn::KMAX - 1;
+// Block-Jacobi schedule. The 63 rounds of a parallel cyclic sweep pair i
+// with i ^ r; grouped into the 21 lines {a, b, a^b} of a line spread of
+// PG(5, 2), three consecutive rounds act inside the 16 cosets ("quads") of
+// {0, a, b, a^b}, so one super-round = three rounds = one 4x4 block step:
+// G <- Q^T G Q, V <- V Q with Q block-diagonal over the quads, one read and
+// one write of G and V per three rounds. g0..g3 span a complement whose
+// low four bits are bijective: quad B's representative xor_k(bit k of B) g_k
+// lands in its own shared-memory bank. Generated and checked by
+// tools/jacobi_schedule.py (tests/test_native_abi.py re-checks the table).
+__constant__ unsigned char kJacobiSched[21][6] = {
+    {1, 59, 2, 4, 8, 17},   {2, 53, 1, 4, 8, 18},   {4, 41, 1, 2, 8, 20},
+    {8, 17, 1, 2, 4, 40},   {16, 34, 1, 2, 4, 8},   {32, 7, 1, 2, 8, 20},
+    {3, 14, 1, 4, 18, 40},  {6, 28, 1, 2, 8, 36},   {12, 56, 1, 2, 4, 24},
+    {24, 51, 1, 2, 4, 8},   {48, 37, 1, 2, 4, 8},   {35, 9, 1, 2, 4, 24},
+    {5, 18, 1, 2, 8, 36},   {10, 36, 1, 2, 4, 24},  {20, 11, 1, 2, 4, 40},
+    {40, 22, 1, 2, 4, 8},   {19, 44, 1, 2, 4, 8},   {38, 27, 1, 2, 4, 8},
+    {15, 54, 1, 2, 4, 24},  {30, 47, 1, 2, 4, 8},   {60, 29, 1, 2, 4, 8},
+};
+
+// the four indices of quad B in super-round sr: t, t^a, t^b, t^a^b
+__device__ __forceinline__ void jacobi_quad(int sr, int B, int e[4]) {
+  const int a = kJacobiSched[sr][0], b = kJacobiSched[sr][1];
+  int t = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if ((B >> k) & 1) t ^= kJacobiSched[sr][2 + k];
+  e[0] = t;
+  e[1] = t ^ a;
+  e[2] = t ^ b;
+  e[3] = t ^ a ^ b;
 }
 
 // (u, v) <- (c u - s v, s u + c v) in one fixed evaluation order, so the
@@ -206,8 +225,6 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
   extern __shared__ __align__(16) double sm[];
   double* G = sm;               // KMAX x GLD, exactly symmetric throughout
   double* Vt = G + KMAX * GLD;  // KMAX x VLD: Vt[j][i] = V[i][j] (row j = eigenvector j)
-  __shared__ double cs_c[KMAX / 2], cs_s[KMAX / 2], cs_dp[KMAX / 2], cs_dq[KMAX / 2];
-  __shared__ unsigned cs_rot;
   __shared__ double ratio[KMAX];
   __shared__ double s_tiny;
   const int g = blockIdx.x;
@@ -295,12 +312,16 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
   __syncthreads();
   const double tiny = s_tiny;
 
-  // ---- parallel cyclic Jacobi, 32 disjoint rotations per round. Phase 1
-  // (warp 0): the rotation of pair `lane`. Phase 2 (all): one pass over G in
-  // 2x2 blocks -- warp w owns row pairs 4w..4w+3, lane l column pair l, so
-  // G <- J^T G J costs one read and one write per element -- and V <- V J on
-  // the transposed V (contiguous rows). A rotation is skipped once |g_pq| is
-  // at rounding level relative to its diagonal pair (or to 1e-17 trace).
+  // ---- parallel cyclic Jacobi in 4x4 block steps (schedule above). Phase
+  // 1 (16 lanes of warp 0, one quad each): the quad's three rounds on its
+  // own 4x4 diagonal block, accumulating Q_quad. Phase 2 (all threads):
+  // thread (w, l) owns the G block (2w + l/16, l%16) -> Q_A^T X Q_B, and the
+  // V^T rows of quad l%16 at four columns. A rotation is skipped once |g_pq|
+  // is at rounding level relative to its diagonal pair (or to 1e-17 trace).
+  __shared__ double Qs[16][16];  // Qs[4*r + c][quad] = Q_quad[r][c]
+  __shared__ double Ds[16][16];  // rotated diagonal block, same layout
+  __shared__ unsigned s_qrot;
+  const int qA = 2 * warp + (lane >> 4), qB = lane & 15;
   int sweep = 0;
   for (; sweep < MAX_SWEEPS; ++sweep) {
     // A sweep changes G only if some pair passes the rotation test on the
@@ -314,77 +335,119 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
                 fmax(kRotTol * sqrt(fabs(G[i * GLD + i] * G[j * GLD + j])), tiny);
     }
     if (!__syncthreads_or(need)) break;
-    for (int round = 0; round < KMAX - 1; ++round) {
+    for (int sr = 0; sr < 21; ++sr) {
       if (warp == 0) {
-        int p, q;
-        jacobi_pair(lane, round, p, q);
-        const double app = G[p * GLD + p], aqq = G[q * GLD + q], apq = G[p * GLD + q];
-        const bool rot = fabs(apq) > fmax(kRotTol * sqrt(fabs(app * aqq)), tiny);
-        double c = 1.0, sn = 0.0, t = 0.0;
-        if (rot) {
-          const double tau = (aqq - app) / (2.0 * apq);
-          t = fabs(tau) > 1e150 ? 0.5 / tau
-                                : (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-          c = 1.0 / sqrt(1.0 + t * t);
-          sn = t * c;
+        bool any = false;
+        if (lane < 16) {
+          int e[4];
+          jacobi_quad(sr, lane, e);
+          double S[4][4], Q[4][4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              Q[i][j] = i == j ? 1.0 : 0.0;
+              if (j >= i) S[i][j] = G[e[i] * GLD + e[j]];
+            }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < i; ++j) S[i][j] = S[j][i];
+          // rounds a, b, a^b: pairs (0,1)(2,3), (0,2)(1,3), (0,3)(1,2)
+          constexpr int PI[6] = {0, 2, 0, 1, 0, 1}, PJ[6] = {1, 3, 2, 3, 3, 2};
+#pragma unroll
+          for (int r = 0; r < 6; ++r) {
+            const int p = PI[r], q = PJ[r];
+            const double app = S[p][p], aqq = S[q][q], apq = S[p][q];
+            if (fabs(apq) > fmax(kRotTol * sqrt(fabs(app * aqq)), tiny)) {
+              any = true;
+              const double tau = (aqq - app) / (2.0 * apq);
+              const double t = fabs(tau) > 1e150 ? 0.5 / tau
+                                                 : (tau >= 0 ? 1.0 : -1.0) /
+                                                       (fabs(tau) + sqrt(1.0 + tau * tau));
+              const double c = 1.0 / sqrt(1.0 + t * t), sn = t * c;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                if (k != p && k != q) {
+                  jrot(c, sn, S[k][p], S[k][q]);
+                  S[p][k] = S[k][p];
+                  S[q][k] = S[k][q];
+                }
+                jrot(c, sn, Q[k][p], Q[k][q]);
+              }
+              S[p][p] = app - t * apq;
+              S[q][q] = aqq + t * apq;
+              S[p][q] = S[q][p] = 0.0;
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              Qs[4 * i + j][lane] = Q[i][j];
+              Ds[4 * i + j][lane] = S[i][j];
+            }
         }
-        cs_c[lane] = c;
-        cs_s[lane] = sn;
-        cs_dp[lane] = app - t * apq;
-        cs_dq[lane] = aqq + t * apq;
-        const unsigned m = __ballot_sync(0xffffffffu, rot);
-        if (lane == 0) cs_rot = m;
+        const unsigned m = __ballot_sync(0xffffffffu, any);
+        if (lane == 0) s_qrot = m;
       }
       __syncthreads();
-      const unsigned mask = cs_rot;
+      const unsigned mask = s_qrot;
       if (mask) {
-        // Branch-free block update: a skipped rotation is (c, s) = (1, 0),
-        // which is exact. Blocks below the diagonal are handled transposed
-        // (x01 <-> x10, A <-> B) so both halves use the same operation order.
-        int pB, qB;
-        jacobi_pair(lane, round, pB, qB);
-        const double cB = cs_c[lane], sB = cs_s[lane];
+        const bool rA = (mask >> qA) & 1u, rB = (mask >> qB) & 1u;
+        int eA[4], eB[4];
+        jacobi_quad(sr, qA, eA);
+        jacobi_quad(sr, qB, eB);
+        double QB[4][4];
 #pragma unroll
-        for (int ab = 0; ab < 4; ++ab) {
-          const int A = 4 * warp + ab;
-          int pA, qA;
-          jacobi_pair(A, round, pA, qA);
-          const double cA = cs_c[A], sA = cs_s[A];
-          double x00 = G[pA * GLD + pB], x01 = G[pA * GLD + qB];
-          double x10 = G[qA * GLD + pB], x11 = G[qA * GLD + qB];
-          const bool lo = A <= lane;
-          const double c1 = lo ? cA : cB, s1 = lo ? sA : sB;
-          const double c2 = lo ? cB : cA, s2 = lo ? sB : sA;
-          double y01 = lo ? x01 : x10, y10 = lo ? x10 : x01;
-          jrot(c1, s1, x00, y10);
-          jrot(c1, s1, y01, x11);
-          jrot(c2, s2, x00, y01);
-          jrot(c2, s2, y10, x11);
-          x01 = lo ? y01 : y10;
-          x10 = lo ? y10 : y01;
-          if (A == lane) {  // closed form on the rotated pair's own 2x2 block
-            x00 = cs_dp[A];
-            x11 = cs_dq[A];
-            x01 = x10 = 0.0;
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) QB[i][j] = Qs[4 * i + j][qB];
+        if (rB) {
+          // V <- V Q: V^T rows eB[*], columns h + 2w + 16m
+#pragma unroll
+          for (int mm = 0; mm < 4; ++mm) {
+            const int i = (lane >> 4) + 2 * warp + 16 * mm;
+            double v[4];
+#pragma unroll
+            for (int l = 0; l < 4; ++l) v[l] = Vt[eB[l] * VLD + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              double u = 0.0;
+#pragma unroll
+              for (int l = 0; l < 4; ++l) u = fma(v[l], QB[l][j], u);
+              Vt[eB[j] * VLD + i] = u;
+            }
           }
-          G[pA * GLD + pB] = x00;
-          G[pA * GLD + qB] = x01;
-          G[qA * GLD + pB] = x10;
-          G[qA * GLD + qB] = x11;
         }
+        if (rA || rB) {
+          // U = X Q_B (rows of X streamed in), then Y = Q_A^T U row by row
+          double U[4][4];
 #pragma unroll
-        for (int ab = 0; ab < 4; ++ab) {
-          const int A = 4 * warp + ab;
-          int pA, qA;
-          jacobi_pair(A, round, pA, qA);
-          const double cA = cs_c[A], sA = cs_s[A];
+          for (int k = 0; k < 4; ++k) {
+            double xk[4];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int i = lane + 32 * h;
-            double vp = Vt[pA * VLD + i], vq = Vt[qA * VLD + i];
-            jrot(cA, sA, vp, vq);
-            Vt[pA * VLD + i] = vp;
-            Vt[qA * VLD + i] = vq;
+            for (int l = 0; l < 4; ++l) xk[l] = G[eA[k] * GLD + eB[l]];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              double u = 0.0;
+#pragma unroll
+              for (int l = 0; l < 4; ++l) u = fma(xk[l], QB[l][j], u);
+              U[k][j] = u;
+            }
+          }
+          const bool diag = qA == qB;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            double y[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const double qa = Qs[4 * k + i][qA];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) y[j] = fma(qa, U[k][j], y[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) G[eA[i] * GLD + eB[j]] = diag ? Ds[4 * i + j][qA] : y[j];
           }
         }
       }

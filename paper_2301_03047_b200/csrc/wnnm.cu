@@ -211,6 +211,24 @@ __device__ __forceinline__ void jacobi_quad(int sr, int B, int e[4]) {
   e[3] = t ^ a ^ b;
 }
 
+// Short-latency reciprocal / reciprocal square root for the Jacobi rotation
+// parameters: hardware approximation + two Newton steps (quadratic: full
+// double precision to ~1 ulp; inputs are positive and normal when used).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int i = 0; i < 2; ++i) y = fma(y, fma(-x, y, 1.0), y);
+  return y;
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int i = 0; i < 2; ++i) y = fma(0.5 * y, fma(-x * y, y, 1.0), y);
+  return y;
+}
+
 // (u, v) <- (c u - s v, s u + c v) in one fixed evaluation order, so the
 // (A, B) and (B, A) blocks of G stay exact transposes of each other.
 __device__ __forceinline__ void jrot(double c, double s, double& u, double& v) {
@@ -312,16 +330,44 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
   __syncthreads();
   const double tiny = s_tiny;
 
-  // ---- parallel cyclic Jacobi in 4x4 block steps (schedule above). Phase
-  // 1 (16 lanes of warp 0, one quad each): the quad's three rounds on its
-  // own 4x4 diagonal block, accumulating Q_quad. Phase 2 (all threads):
-  // thread (w, l) owns the G block (2w + l/16, l%16) -> Q_A^T X Q_B, and the
-  // V^T rows of quad l%16 at four columns. A rotation is skipped once |g_pq|
-  // is at rounding level relative to its diagonal pair (or to 1e-17 trace).
-  __shared__ double Qs[16][16];  // Qs[4*r + c][quad] = Q_quad[r][c]
-  __shared__ double Ds[16][16];  // rotated diagonal block, same layout
-  __shared__ unsigned s_qrot;
+  // ---- parallel cyclic Jacobi in 4x4 block steps (schedule above). Per
+  // super-round: phase 1 -- warp 0 lanes 0..15, one quad each, run the
+  // quad's three rounds on its own 4x4 diagonal block (accumulating
+  // Q_quad) while warps 1..7 apply the PREVIOUS super-round's V <- V Q
+  // (double-buffered Q); phase 2 -- thread (w, l) rotates the G block
+  // (2w + l/16, l%16): Q_A^T X Q_B. A rotation is skipped once |g_pq| is at
+  // rounding level relative to its diagonal pair (or to 1e-17 trace).
+  __shared__ double Qs[2][16][16];  // Qs[buf][4*r + c][quad] = Q_quad[r][c]
+  __shared__ double Ds[16][16];     // rotated diagonal block, same layout
+  __shared__ unsigned s_qrot[2];
   const int qA = 2 * warp + (lane >> 4), qB = lane & 15;
+  int gsr = 0, prev_sr = -1;  // running super-round count; pending V step
+  auto v_step = [&](int buf, int srv, int t0, int nthreads) {
+    // V <- V Q_srv: V^T rows of quad B at 64 columns; unit u = (column, quad)
+    const unsigned m = s_qrot[buf];
+    const int B = t0 & 15;
+    if (!((m >> B) & 1u)) return;
+    int e[4];
+    jacobi_quad(srv, B, e);
+    double QB[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) QB[i][j] = Qs[buf][4 * i + j][B];
+    for (int u = t0; u < 16 * KMAX; u += nthreads) {
+      const int i = u >> 4;
+      double v[4];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) v[l] = Vt[e[l] * VLD + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        double o = 0.0;
+#pragma unroll
+        for (int l = 0; l < 4; ++l) o = fma(v[l], QB[l][j], o);
+        Vt[e[j] * VLD + i] = o;
+      }
+    }
+  };
   int sweep = 0;
   for (; sweep < MAX_SWEEPS; ++sweep) {
     // A sweep changes G only if some pair passes the rotation test on the
@@ -335,7 +381,8 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
                 fmax(kRotTol * sqrt(fabs(G[i * GLD + i] * G[j * GLD + j])), tiny);
     }
     if (!__syncthreads_or(need)) break;
-    for (int sr = 0; sr < 21; ++sr) {
+    for (int sr = 0; sr < 21; ++sr, ++gsr) {
+      const int buf = gsr & 1;
       if (warp == 0) {
         bool any = false;
         if (lane < 16) {
@@ -353,30 +400,45 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
           for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < i; ++j) S[i][j] = S[j][i];
-          // rounds a, b, a^b: pairs (0,1)(2,3), (0,2)(1,3), (0,3)(1,2)
+          // rounds a, b, a^b: pairs (0,1)(2,3), (0,2)(1,3), (0,3)(1,2); the
+          // two rotations of a round are independent (branch-free, so their
+          // latency chains overlap); a skipped rotation is the identity.
           constexpr int PI[6] = {0, 2, 0, 1, 0, 1}, PJ[6] = {1, 3, 2, 3, 3, 2};
 #pragma unroll
-          for (int r = 0; r < 6; ++r) {
-            const int p = PI[r], q = PJ[r];
-            const double app = S[p][p], aqq = S[q][q], apq = S[p][q];
-            if (fabs(apq) > fmax(kRotTol * sqrt(fabs(app * aqq)), tiny)) {
-              any = true;
-              const double tau = (aqq - app) / (2.0 * apq);
-              const double t = fabs(tau) > 1e150 ? 0.5 / tau
-                                                 : (tau >= 0 ? 1.0 : -1.0) /
-                                                       (fabs(tau) + sqrt(1.0 + tau * tau));
-              const double c = 1.0 / sqrt(1.0 + t * t), sn = t * c;
+          for (int rr = 0; rr < 3; ++rr) {
+            double c[2], sn[2], t[2], app[2], aqq[2], apq[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int p = PI[2 * rr + h], q = PJ[2 * rr + h];
+              app[h] = S[p][p];
+              aqq[h] = S[q][q];
+              apq[h] = S[p][q];
+              const bool rot = fabs(apq[h]) > fmax(kRotTol * sqrt(fabs(app[h] * aqq[h])), tiny);
+              any |= rot;
+              // t = sign(tau) / (|tau| + sqrt(1 + tau^2)), tau = d / g, as
+              // sign(d) g / (|d| + hypot(d, g)): one sqrt, one division, one
+              // rsqrt on the latency chain (|t| <= 1)
+              const double d = aqq[h] - app[h], g = 2.0 * apq[h];
+              const double hh = fma(d, d, g * g);
+              const double tt = (d >= 0.0 ? g : -g) * rcp_nr(fabs(d) + hh * rsqrt_nr(hh));
+              t[h] = rot ? tt : 0.0;
+              c[h] = rot ? rsqrt_nr(fma(tt, tt, 1.0)) : 1.0;
+              sn[h] = rot ? t[h] * c[h] : 0.0;
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int p = PI[2 * rr + h], q = PJ[2 * rr + h];
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
                 if (k != p && k != q) {
-                  jrot(c, sn, S[k][p], S[k][q]);
+                  jrot(c[h], sn[h], S[k][p], S[k][q]);
                   S[p][k] = S[k][p];
                   S[q][k] = S[k][q];
                 }
-                jrot(c, sn, Q[k][p], Q[k][q]);
+                jrot(c[h], sn[h], Q[k][p], Q[k][q]);
               }
-              S[p][p] = app - t * apq;
-              S[q][q] = aqq + t * apq;
+              S[p][p] = app[h] - t[h] * apq[h];
+              S[q][q] = aqq[h] + t[h] * apq[h];
               S[p][q] = S[q][p] = 0.0;
             }
           }
@@ -384,75 +446,58 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
           for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              Qs[4 * i + j][lane] = Q[i][j];
+              Qs[buf][4 * i + j][lane] = Q[i][j];
               Ds[4 * i + j][lane] = S[i][j];
             }
         }
         const unsigned m = __ballot_sync(0xffffffffu, any);
-        if (lane == 0) s_qrot = m;
+        if (lane == 0) s_qrot[buf] = m;
+      } else if (prev_sr >= 0) {
+        v_step(buf ^ 1, prev_sr, tid - 32, EIG_THREADS - 32);
       }
       __syncthreads();
-      const unsigned mask = s_qrot;
-      if (mask) {
-        const bool rA = (mask >> qA) & 1u, rB = (mask >> qB) & 1u;
+      const unsigned mask = s_qrot[buf];
+      prev_sr = mask ? sr : -1;
+      const bool rA = (mask >> qA) & 1u, rB = (mask >> qB) & 1u;
+      if (rA || rB) {
         int eA[4], eB[4];
         jacobi_quad(sr, qA, eA);
         jacobi_quad(sr, qB, eB);
-        double QB[4][4];
+        // U = X Q_B (rows of X streamed in), then Y = Q_A^T U row by row
+        double U[4][4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int k = 0; k < 4; ++k) {
+          double xk[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) QB[i][j] = Qs[4 * i + j][qB];
-        if (rB) {
-          // V <- V Q: V^T rows eB[*], columns h + 2w + 16m
+          for (int l = 0; l < 4; ++l) xk[l] = G[eA[k] * GLD + eB[l]];
 #pragma unroll
-          for (int mm = 0; mm < 4; ++mm) {
-            const int i = (lane >> 4) + 2 * warp + 16 * mm;
-            double v[4];
+          for (int j = 0; j < 4; ++j) {
+            double u = 0.0;
 #pragma unroll
-            for (int l = 0; l < 4; ++l) v[l] = Vt[eB[l] * VLD + i];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              double u = 0.0;
-#pragma unroll
-              for (int l = 0; l < 4; ++l) u = fma(v[l], QB[l][j], u);
-              Vt[eB[j] * VLD + i] = u;
-            }
+            for (int l = 0; l < 4; ++l) u = fma(xk[l], Qs[buf][4 * l + j][qB], u);
+            U[k][j] = u;
           }
         }
-        if (rA || rB) {
-          // U = X Q_B (rows of X streamed in), then Y = Q_A^T U row by row
-          double U[4][4];
+        const bool diag = qA == qB;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          double y[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            double xk[4];
+            const double qa = Qs[buf][4 * k + i][qA];
 #pragma unroll
-            for (int l = 0; l < 4; ++l) xk[l] = G[eA[k] * GLD + eB[l]];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              double u = 0.0;
-#pragma unroll
-              for (int l = 0; l < 4; ++l) u = fma(xk[l], QB[l][j], u);
-              U[k][j] = u;
-            }
+            for (int j = 0; j < 4; ++j) y[j] = fma(qa, U[k][j], y[j]);
           }
-          const bool diag = qA == qB;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            double y[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const double qa = Qs[4 * k + i][qA];
-#pragma unroll
-              for (int j = 0; j < 4; ++j) y[j] = fma(qa, U[k][j], y[j]);
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) G[eA[i] * GLD + eB[j]] = diag ? Ds[4 * i + j][qA] : y[j];
-          }
+          for (int j = 0; j < 4; ++j) G[eA[i] * GLD + eB[j]] = diag ? Ds[4 * i + j][qA] : y[j];
         }
       }
       __syncthreads();
     }
+  }
+  if (prev_sr >= 0) {  // the last super-round's V step
+    v_step((gsr - 1) & 1, prev_sr, tid, EIG_THREADS);
+    __syncthreads();
   }
 
 #ifdef GLR_EIG_STATS

@@ -57,9 +57,11 @@ int glr_sobel(const double* x_d, int H, int W, int C, double* gh_d, double* gv_d
 /* glr_edge_stack: sign-split thresholding (edges.py:67-85) of gh/gv into
  *  - maps_d  (optional, may be NULL): u8 {0,1} (4,H,W,C) in the order
  *            h_pos, h_neg, v_pos, v_neg (EdgeMaps.as_tuple, edges.py:33-34);
- *  - stack_d (optional): the u8 im2col-friendly "expanded" stack used by the
- *            heat-map GEMM, (H,W,e*4C) with stack[r][c][p*4C+m*C+ch] =
- *            map_m[r+p][c][ch] for p<e (0 past the last row).
+ *  - stack_d (optional): the im2col-friendly "expanded" stack used by the
+ *            heat-map GEMM: (H,W,e*4C) elements with element p*4C+m*C+ch of
+ *            pixel (r,c) = map_m[r+p][c][ch] for p<e (0 past the last row),
+ *            each an E2M1 (fp4) 1.0 / 0.0 code packed two per byte (element
+ *            2j in the low nibble of byte j): H*W*e*2C bytes.
  * th is relative to max|g| when relative != 0 (edges.py:79-80).
  * ws_d: 2 doubles of scratch (the two maxima).                              */
 int glr_edge_stack(const double* gh_d, const double* gv_d, int H, int W, int C, double th,
@@ -98,7 +100,8 @@ int glr_select_anchors(const int32_t* corners_rc_d, const int32_t* n_corners_d, 
 
 /* ---- (2) global similarity heat map: glr/matching.py:140-167 ---------------
  * heat[n][u*ow+v] = sum_{p,q,ch<4C} E[u+p][v+q][ch] * E[r_n+p][c_n+q][ch],
- * exact integer overlap counts on tcgen05 tensor cores (kind::i8, s32 accum).
+ * exact integer overlap counts on tcgen05 tensor cores (kind::mxf4: packed
+ * fp4 0/1 operands, unit UE8M0 scale factors, f32 accumulation).
  * Exemplar-major u16 output heat[n*stride + u*ow + v], stride =
  * glr_heat_stride(H,W,P) (oh = H-P+1, ow = W-P+1). n_dev_d (optional) caps the exemplar count on device.
  * ws: glr_heat_workspace (the packed exemplar operand).                     */

@@ -169,6 +169,21 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// D[tmem] (+)= (A * SFA)[smem] * (B * SFB)[smem]^T, packed E2M1 (fp4) operands
+// with UE8M0 scale factors per 32 K-elements read from TMEM, f32 accumulate
+// (kind::mxf4, K = 64 per instruction), one CTA.
+__device__ __forceinline__ void umma_mxf4(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate, uint32_t tmem_sfa,
+                                          uint32_t tmem_sfb) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t"
+      "}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tmem_sfa), "r"(tmem_sfb));
+}
+
 // Arrive on an mbarrier once every previously issued tcgen05.mma has completed.
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile(
@@ -189,6 +204,24 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)
         "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
         "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
+}
+
+// 32 registers per thread -> 32 lanes x 32 consecutive 32-bit TMEM columns.
+__device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+      "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st_wait() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
 __device__ __forceinline__ void tmem_ld_wait() {
@@ -216,5 +249,19 @@ __host__ __device__ constexpr uint32_t idesc_u8_s32(uint32_t m, uint32_t n) {
          | ((n >> 3) << 17)    // N / 8
          | ((m >> 4) << 24);   // M / 16
 }
+
+// Instruction descriptor, kind::mxf4 block32: E2M1 A/B (K-major), UE8M0 scale
+// factors (scale-factor ids 0), f32 accumulate, dense K = 64.
+__host__ __device__ constexpr uint32_t idesc_mxf4(uint32_t m, uint32_t n) {
+  return (1u << 7)             // A: E2M1
+         | (1u << 10)          // B: E2M1
+         | ((n >> 3) << 17)    // N / 8
+         | (1u << 23)          // scale factors: UE8M0
+         | ((m >> 4) << 24);   // M / 16
+}
+
+// E2M1 code of 1.0 (sign 0, exponent 01, mantissa 0); 0.0 is code 0. Binary
+// edge maps are stored two per byte (element 2j in the low nibble).
+constexpr uint8_t kFp4One = 0x2;
 
 }  // namespace glr

@@ -162,42 +162,53 @@ __global__ void edge_maps_kernel(const double* __restrict__ gh, const double* __
   }
 }
 
+// Stack layout (heat_gemm.cu): (H, W, Ce) binary elements, Ce = e*4C, stored
+// as packed E2M1 nibbles (1.0 / 0.0), element 2j in the low nibble of byte j.
 __global__ void edge_stack_kernel(const double* __restrict__ gh, const double* __restrict__ gv,
                                   int H, int W, int C, int e, EdgeTh t,
                                   const unsigned long long* mx, uint8_t* __restrict__ stack) {
   double th_h, th_v;
   edge_thresholds(mx, t, th_h, th_v);
-  const int C4 = 4 * C, Ce = e * C4;
-  const int64_t total = (int64_t)H * W * Ce;
+  const int C4 = 4 * C, Ce = e * C4, Cb = Ce / 2;
+  const int64_t total = (int64_t)H * W * Cb;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int ce = (int)(i % Ce);
-    const int64_t pix = i / Ce;
+    const int cb = (int)(i % Cb);
+    const int64_t pix = i / Cb;
     const int r = (int)(pix / W), c = (int)(pix % W);
-    const int p = ce / C4, k = ce % C4, m = k / C, ch = k % C;
-    uint8_t v = 0;
-    if (r + p < H) {
-      const int64_t j = ((int64_t)(r + p) * W + c) * C + ch;
-      v = edge_bit((m < 2) ? gh[j] : gv[j], m, th_h, th_v);
+    uint8_t byte = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int ce = 2 * cb + h;
+      const int p = ce / C4, k = ce % C4, m = k / C, ch = k % C;
+      if (r + p < H) {
+        const int64_t j = ((int64_t)(r + p) * W + c) * C + ch;
+        if (edge_bit((m < 2) ? gh[j] : gv[j], m, th_h, th_v)) byte |= kFp4One << (4 * h);
+      }
     }
-    stack[i] = v;
+    stack[i] = byte;
   }
 }
 
 __global__ void stack_from_maps_kernel(const uint8_t* __restrict__ maps, int H, int W, int C,
                                        int e, uint8_t* __restrict__ stack) {
-  const int C4 = 4 * C, Ce = e * C4;
+  const int C4 = 4 * C, Ce = e * C4, Cb = Ce / 2;
   const int64_t plane = (int64_t)H * W * C;
-  const int64_t total = (int64_t)H * W * Ce;
+  const int64_t total = (int64_t)H * W * Cb;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int ce = (int)(i % Ce);
-    const int64_t pix = i / Ce;
+    const int cb = (int)(i % Cb);
+    const int64_t pix = i / Cb;
     const int r = (int)(pix / W), c = (int)(pix % W);
-    const int p = ce / C4, k = ce % C4, m = k / C, ch = k % C;
-    uint8_t v = 0;
-    if (r + p < H) v = maps[m * plane + ((int64_t)(r + p) * W + c) * C + ch] ? 1 : 0;
-    stack[i] = v;
+    uint8_t byte = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int ce = 2 * cb + h;
+      const int p = ce / C4, k = ce % C4, m = k / C, ch = k % C;
+      if (r + p < H && maps[m * plane + ((int64_t)(r + p) * W + c) * C + ch])
+        byte |= kFp4One << (4 * h);
+    }
+    stack[i] = byte;
   }
 }
 
@@ -504,7 +515,7 @@ extern "C" int glr_edge_stack(const double* gh_d, const double* gv_d, int H, int
     GLR_CUDA(cudaGetLastError());
   }
   if (stack_d) {
-    edge_stack_kernel<<<grid_for(n * 4 * expand), 256, 0, st>>>(gh_d, gv_d, H, W, C, expand, t, mx,
+    edge_stack_kernel<<<grid_for(n * 2 * expand), 256, 0, st>>>(gh_d, gv_d, H, W, C, expand, t, mx,
                                                                  stack_d);
     GLR_CUDA(cudaGetLastError());
   }
@@ -515,7 +526,8 @@ extern "C" int glr_stack_from_maps(const uint8_t* maps_d, int H, int W, int C, i
                                    uint8_t* stack_d, void* stream) {
   GLR_REQUIRE(H >= 1 && W >= 1 && C >= 1 && expand >= 1, GLR_ERR_INVALID,
               "stack_from_maps: bad shape");
-  int64_t n = (int64_t)H * W * C * 4 * expand;
+  GLR_REQUIRE((4 * C * expand) % 2 == 0, GLR_ERR_INVALID, "stack_from_maps: odd stack width");
+  int64_t n = (int64_t)H * W * C * 2 * expand;
   stack_from_maps_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(maps_d, H, W, C, expand,
                                                                        stack_d);
   return check_launch("stack_from_maps_kernel");

@@ -6,17 +6,24 @@
 // reference runs this as an OpenBLAS sgemm on an explicit im2col copy; here
 // the im2col is never materialised:
 //
-//   * The edge stack is stored u8 {0,1} as (H, W, Ce) with Ce = e*4C ("e-row
-//     expanded": channel p*4C+k of pixel (r,c) holds map_k(r+p, c)). For a
-//     fixed output row u and slab s, the K-run of position v is the
-//     contiguous byte range stack[u+s*e][v .. v+P-1][0..Ce-1] of length
-//     L = P*Ce, and consecutive v are Ce bytes apart. A 3-D TMA map with
-//     dims {L, ow, H} and strides {Ce, W*Ce} therefore addresses the
-//     overlapping im2col rows directly; one TMA box = 128 positions x 128 K.
-//   * The exemplar operand B (Npad x Kp, K-major, zero-padded) is gathered
-//     once per refresh from the same stack (exemplar_pack_kernel).
-//   * u8 x u8 -> s32 on tcgen05.mma kind::i8 is exact for every count
-//     (max 4*C*P^2); the accumulator lives in TMEM (128 lanes x 256 cols).
+//   * The edge stack holds the binary maps as (H, W, Ce) elements with
+//     Ce = e*4C ("e-row expanded": channel p*4C+k of pixel (r,c) holds
+//     map_k(r+p, c)), each element an E2M1 (fp4) 1.0 or 0.0 packed two per
+//     byte, so a pixel is Cb = Ce/2 bytes. For a fixed output row u and slab
+//     s, the K-run of position v is the contiguous byte range
+//     stack[u+s*e][v .. v+P-1][*] of length L = P*Cb, and consecutive v are
+//     Cb bytes apart. A 3-D TMA map with dims {L, ow, H} and strides
+//     {Cb, W*Cb} therefore addresses the overlapping im2col rows directly;
+//     one TMA box = 128 positions x 128 bytes (256 K-elements).
+//   * The exemplar operand B (Npad x Kp bytes, K-major, zero-padded) is
+//     gathered once per refresh from the same stack (exemplar_pack_kernel).
+//   * tcgen05.mma kind::mxf4 (block-scaled fp4, f32 accumulate) with every
+//     UE8M0 scale factor = 2^0: products of 0/1 are exact and the f32 sums
+//     are exact integers (max 4*C*P^2 < 2^24). fp4 halves the operand bytes
+//     per multiply-add of the u8 formulation (this kernel is bound by the
+//     L2 -> shared-memory operand stream) and runs at twice the i8 rate.
+//     Accumulators live in TMEM (2 x 128 lanes x 224 columns), the constant
+//     scale factors in the remaining 64 columns.
 //   * Output: exemplar-major u16 heat[n][u*ow+v] (flat index = the
 //     reference's row-major slice index, matching.py:177-178), rows padded
 //     to a multiple of 8 entries (glr_heat_stride) for 16-byte loads.
@@ -25,6 +32,7 @@
 //   warp 0 (one lane)  TMA producer, 4-stage smem ring (full/empty mbarriers);
 //   warp 1 (one lane)  tcgen05.mma issuer into one of two TMEM accumulators;
 //   warp 2             owns the 512-column TMEM allocation;
+//   warps 4-7          also write the constant scale factors at start-up;
 //   warps 4-7          epilogue: tcgen05.ld -> u16 stores, then release the
 //                      accumulator, so tile i's epilogue overlaps tile i+1's
 //                      MMAs (accumulator handoff via tmem_full/tmem_empty).
@@ -37,21 +45,23 @@ namespace glr {
 
 namespace heat {
 constexpr int BM = 128;      // positions per tile (UMMA M)
-constexpr int BN = 256;      // exemplars per tile (UMMA N)
-constexpr int BK = 128;      // bytes of K per stage (one 128B swizzle row)
-constexpr int UK = 32;       // K per tcgen05.mma kind::i8
+constexpr int BN = 224;      // exemplars per tile (UMMA N)
+constexpr int BK = 128;      // bytes of K per stage (one 128B swizzle row = 256 fp4)
+constexpr int UK = 32;       // bytes of K per tcgen05.mma kind::mxf4 (64 fp4)
 constexpr int STAGES = 4;
-constexpr int ACC = 2;       // TMEM accumulators (2 x 256 columns)
+constexpr int ACC = 2;       // TMEM accumulators (2 x 224 columns)
 constexpr int THREADS = 256;
 constexpr int A_BYTES = BM * BK;
 constexpr int B_BYTES = BN * BK;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t SFA_COL = 448;  // 32 columns of scale factors for A
+constexpr uint32_t SFB_COL = 480;  // 32 columns of scale factors for B
 }  // namespace heat
 
 struct HeatGeom {
-  int H, W, C4, P, e, Ce, S, L, kchunks, Kp, oh, ow;
+  int H, W, C4, P, e, Ce, Cb, S, L, kchunks, Kp, oh, ow;
 };
 
 static HeatGeom heat_geom(int H, int W, int C, int P, int e) {
@@ -62,8 +72,9 @@ static HeatGeom heat_geom(int H, int W, int C, int P, int e) {
   g.P = P;
   g.e = e;
   g.Ce = e * 4 * C;
+  g.Cb = g.Ce / 2;
   g.S = (int)cdiv(P, e);
-  g.L = P * g.Ce;
+  g.L = P * g.Cb;
   g.kchunks = (int)cdiv(g.L, heat::BK);
   g.Kp = g.S * g.kchunks * heat::BK;
   g.oh = H - P + 1;
@@ -119,6 +130,19 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (warp >= 4) {
+    // every scale-factor byte = UE8M0 127 = 2^0, whatever the layout the MMA reads
+    uint32_t ones[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) ones[j] = 0x7F7F7F7Fu;
+    const uint32_t lanes = (uint32_t)((warp - 4) * 32) << 16;
+    tmem_st_32x32b_x32(tmem + lanes + SFA_COL, ones);
+    tmem_st_32x32b_x32(tmem + lanes + SFB_COL, ones);
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -144,7 +168,7 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       // ---- MMA issuer ----
-      constexpr uint32_t idesc = idesc_u8_s32(BM, BN);
+      constexpr uint32_t idesc = idesc_mxf4(BM, BN);
       int it = 0, lt = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
         const int acc = lt & 1, use = lt >> 1;
@@ -160,8 +184,8 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
           const uint64_t bd = smem_desc_k_sw128(sB + s * B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / UK; ++k)  // +32 bytes inside the 128B swizzle atom
-            umma_i8(d, ad + (uint64_t)((k * UK) >> 4), bd + (uint64_t)((k * UK) >> 4), idesc,
-                    (kb | k) != 0);
+            umma_mxf4(d, ad + (uint64_t)((k * UK) >> 4), bd + (uint64_t)((k * UK) >> 4), idesc,
+                      (kb | k) != 0, tmem + SFA_COL, tmem + SFB_COL);
           umma_commit(&empty[s]);
         }
         umma_commit(&tfull[acc]);
@@ -190,7 +214,7 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int n = nb + j;
-          if (v_ok && n < N) out[(size_t)n * p.Mpad] = (uint16_t)r[j];
+          if (v_ok && n < N) out[(size_t)n * p.Mpad] = (uint16_t)__float2uint_rn(__uint_as_float(r[j]));
         }
       }
       tc_fence_before();
@@ -204,8 +228,8 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
   if (warp == 2) tmem_dealloc<TMEM_COLS>(tmem);
 }
 
-// B operand: bmat[n][s*kchunks*BK + k'] = stack[r_n + s*e][c_n + k'/Ce][k' % Ce] for
-// k' < L, zero for the K padding, for the padded exemplars and past row H.
+// B operand (bytes): bmat[n][s*kchunks*BK + k'] = stack[r_n + s*e][c_n + k'/Cb][k' % Cb]
+// for k' < L, zero for the K padding, for the padded exemplars and past row H.
 __global__ void exemplar_pack_kernel(const uint8_t* __restrict__ stack, HeatGeom g,
                                      const int32_t* __restrict__ anchors, int n_max,
                                      const int32_t* n_dev, int n_pad, uint8_t* __restrict__ bmat) {
@@ -219,13 +243,14 @@ __global__ void exemplar_pack_kernel(const uint8_t* __restrict__ stack, HeatGeom
     const int kk = k - slab * g.kchunks * heat::BK;
     uint8_t val = 0;
     if (n < N && kk < g.L) {
-      const int ch = kk % g.Ce;
-      // expanded channel ch holds map row (anchor row + slab*e + ch / 4C); rows
-      // at or past P belong to no patch and stay zero
-      if (slab * g.e + ch / g.C4 < g.P) {
+      const int cb = kk % g.Cb;
+      // the byte's two expanded channels 2cb, 2cb+1 (same row: 4C is even) hold
+      // map row (anchor row + slab*e + 2cb / 4C); rows at or past P belong to
+      // no patch and stay zero
+      if (slab * g.e + (2 * cb) / g.C4 < g.P) {
         const int r = anchors[2 * n] + slab * g.e;
-        const int c = anchors[2 * n + 1] + kk / g.Ce;
-        val = stack[((size_t)r * g.W + c) * g.Ce + ch];
+        const int c = anchors[2 * n + 1] + kk / g.Cb;
+        val = stack[((size_t)r * g.W + c) * g.Cb + cb];
       }
     }
     bmat[i] = val;
@@ -250,13 +275,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 using namespace glr;
 
 extern "C" int glr_heat_expand_factor(int C, int P) {
-  // Smallest padded K (then the smallest expansion) among e in [1, max(P,4)]
-  // whose pixel stride e*4C is a multiple of 16 bytes (TMA stride rule);
-  // e = 4 always qualifies. Expanded rows at or past P are zero in B.
+  // Smallest padded K (then the smallest expansion) among e in [1, max(P,8)]
+  // whose pixel stride e*4C/2 bytes is a multiple of 16 (TMA stride rule);
+  // e = 8 always qualifies. Expanded rows at or past P are zero in B.
   int best_e = -1;
   int64_t best_k = 0;
-  for (int e = 1; e <= (P > 4 ? P : 4); ++e) {
-    if ((4 * C * e) % 16 != 0) continue;
+  for (int e = 1; e <= (P > 8 ? P : 8); ++e) {
+    if ((4 * C * e) % 32 != 0) continue;
     HeatGeom g = heat_geom(P, P, C, P, e);
     if (best_e < 0 || g.Kp < best_k) {
       best_e = e;
@@ -283,7 +308,7 @@ extern "C" int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, 
                             uint16_t* heat_d, void* ws_d, size_t ws_bytes, void* stream) {
   GLR_REQUIRE(P >= 1 && P <= H && P <= W && C >= 1, GLR_ERR_INVALID,
               "heat_map: bad shape H=%d W=%d C=%d P=%d", H, W, C, P);
-  GLR_REQUIRE(expand >= 1 && expand <= (P > 4 ? P : 4) && (4 * C * expand) % 16 == 0,
+  GLR_REQUIRE(expand >= 1 && expand <= (P > 8 ? P : 8) && (4 * C * expand) % 32 == 0,
               GLR_ERR_INVALID,
               "heat_map: expand factor %d invalid for C=%d", expand, C);
   if (n_max <= 0) return GLR_OK;
@@ -309,7 +334,7 @@ extern "C" int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, 
   CUtensorMap tmA, tmB;
   {
     cuuint64_t dims[3] = {(cuuint64_t)g.L, (cuuint64_t)g.ow, (cuuint64_t)H};
-    cuuint64_t strides[2] = {(cuuint64_t)g.Ce, (cuuint64_t)W * g.Ce};
+    cuuint64_t strides[2] = {(cuuint64_t)g.Cb, (cuuint64_t)W * g.Cb};
     cuuint32_t box[3] = {heat::BK, heat::BM, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = encode(&tmA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)stack_d, dims, strides, box,

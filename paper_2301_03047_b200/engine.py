@@ -163,7 +163,7 @@ class GlrEngine:
         self.resp = D.empty((h, w), t.float64)
         self.gh = D.empty((h, w, c), t.float64)
         self.gv = D.empty((h, w, c), t.float64)
-        self.stack = D.empty((h * w * 4 * c * self.expand,), t.uint8)
+        self.stack = D.empty((h * w * 2 * c * self.expand,), t.uint8)  # packed fp4
         self.corners = D.empty((match.max_corners, 2), t.int32)
         self.n_corners = D.zeros((1,), t.int32)
         self.anchors = D.empty((self.max_anchors, 2), t.int32)

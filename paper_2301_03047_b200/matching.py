@@ -88,7 +88,7 @@ def heat_device(maps_d, h, w, c, p, anchors_d, n):
     """Device heat map from binary maps (4,H,W,C) u8: returns u16 (n, stride)."""
     t = D.torch()
     e = N.query("glr_heat_expand_factor", c, p)
-    stack = D.empty((h * w * 4 * c * e,), t.uint8)
+    stack = D.empty((h * w * 2 * c * e,), t.uint8)  # packed fp4 (two elements per byte)
     N.call("glr_stack_from_maps", maps_d.data_ptr(), h, w, c, e, stack.data_ptr(), D.stream())
     stride = N.query("glr_heat_stride", h, w, p)
     heat = D.empty((n, stride), t.int16)

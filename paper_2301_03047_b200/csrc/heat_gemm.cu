@@ -29,12 +29,12 @@
 //     to a multiple of 8 entries (glr_heat_stride) for 16-byte loads.
 //
 // Persistent, warp-specialised kernel (256 threads, one CTA per SM), launched
-// as clusters of two CTAs that work on vertically adjacent position tiles of
-// the same exemplar tile: each CTA loads its own A box and HALF of the B box,
-// multicast into both CTAs' shared memory, so the L2 -> SM operand stream (the
-// bound) carries 16 + 14 KB per stage instead of 16 + 28 KB.
+// as clusters of CL CTAs that work on adjacent position tiles of the same
+// exemplar tile: each CTA loads its own A box and 1/CL of the B box,
+// multicast into every CTA's shared memory, so the L2 -> SM operand stream
+// (the bound) carries 16 + 28/CL KB per stage instead of 16 + 28 KB.
 //   warp 0 (one lane)  TMA producer, 5-stage smem ring (full/empty mbarriers;
-//                      a stage is refilled once BOTH CTAs' MMAs released it);
+//                      a stage is refilled once ALL CTAs' MMAs released it);
 //   warp 1 (one lane)  tcgen05.mma issuer into one of two TMEM accumulators;
 //   warp 2             owns the 512-column TMEM allocation;
 //   warps 4-7          also write the constant scale factors at start-up;
@@ -54,6 +54,7 @@ constexpr int BN = 224;      // exemplars per tile (UMMA N)
 constexpr int BK = 128;      // bytes of K per stage (one 128B swizzle row = 256 fp4)
 constexpr int UK = 32;       // bytes of K per tcgen05.mma kind::mxf4 (64 fp4)
 constexpr int STAGES = 5;
+constexpr int CL = 2;        // CTAs per cluster sharing one exemplar tile (multicast)
 constexpr int ACC = 2;       // TMEM accumulators (2 x 224 columns)
 constexpr int THREADS = 256;
 constexpr int A_BYTES = BM * BK;
@@ -111,17 +112,18 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
   const int N = p.n_dev ? min(*p.n_dev, p.n_max) : p.n_max;
   const int n_tiles = (N + BN - 1) / BN;
   // tile pairs (two m tiles, one n tile), n fastest: clusters share A tiles in L2
-  const int total = p.oh * (p.m_tiles_per_row / 2) * n_tiles;
+  const int total = p.oh * (p.m_tiles_per_row / CL) * n_tiles;
   const int num_k = p.S * p.kchunks;
   const int rank = (int)cluster_ctarank();
-  const int cl = blockIdx.x >> 1, n_cl = gridDim.x >> 1;
+  const int cl = blockIdx.x / CL, n_cl = gridDim.x / CL;
+  constexpr uint16_t kAll = (1u << CL) - 1;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 2);  // both CTAs' MMA commits
+      mbar_init(&empty[s], CL);  // every CTA's MMA commit
     }
     for (int a = 0; a < ACC; ++a) {
       mbar_init(&tfull[a], 1);
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
       int it = 0;
       for (int t = cl; t < total; t += n_cl) {
         const int n0 = (t % n_tiles) * BN;
-        const int m_tile = 2 * (t / n_tiles) + rank;
+        const int m_tile = CL * (t / n_tiles) + rank;
         const int u = m_tile / p.m_tiles_per_row;
         const int v0 = (m_tile % p.m_tiles_per_row) * BM;
         for (int kb = 0; kb < num_k; ++kb, ++it) {
@@ -170,8 +172,8 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
           const int slab = kb / p.kchunks;
           const int kc = kb - slab * p.kchunks;
           tma_load_3d(sA + s * A_BYTES, &tmA, &full[s], kc * BK, v0, u + slab * p.e);
-          tma_load_2d_mc(sB + s * B_BYTES + rank * (B_BYTES / 2), &tmB, &full[s], kb * BK,
-                         n0 + rank * (BN / 2), 0x3);
+          tma_load_2d_mc(sB + s * B_BYTES + rank * (B_BYTES / CL), &tmB, &full[s], kb * BK,
+                         n0 + rank * (BN / CL), kAll);
         }
       }
     }
@@ -196,7 +198,7 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
           for (int k = 0; k < BK / UK; ++k)  // +32 bytes inside the 128B swizzle atom
             umma_mxf4(d, ad + (uint64_t)((k * UK) >> 4), bd + (uint64_t)((k * UK) >> 4), idesc,
                       (kb | k) != 0, tmem + SFA_COL, tmem + SFB_COL);
-          umma_commit_mc(&empty[s], 0x3);  // frees stage s in both CTAs
+          umma_commit_mc(&empty[s], kAll);  // frees stage s in every CTA
         }
         umma_commit(&tfull[acc]);
       }
@@ -208,7 +210,7 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
     for (int t = cl; t < total; t += n_cl, ++lt) {
       const int acc = lt & 1, use = lt >> 1;
       const int n0 = (t % n_tiles) * BN;
-      const int m_tile = 2 * (t / n_tiles) + rank;
+      const int m_tile = CL * (t / n_tiles) + rank;
       const int u = m_tile / p.m_tiles_per_row;
       const int v = (m_tile % p.m_tiles_per_row) * BM + ew * 32 + lane;
       mbar_wait(&tfull[acc], use & 1);
@@ -356,7 +358,7 @@ extern "C" int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, 
   {
     cuuint64_t dims[2] = {(cuuint64_t)g.Kp, (cuuint64_t)n_pad};
     cuuint64_t strides[1] = {(cuuint64_t)g.Kp};
-    cuuint32_t box[2] = {heat::BK, heat::BN / 2};  // each CTA of a pair loads half
+    cuuint32_t box[2] = {heat::BK, heat::BN / heat::CL};  // each CTA loads its slice
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)bmat, dims, strides, box,
                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -369,7 +371,7 @@ extern "C" int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, 
   hp.ow = g.ow;
   hp.Mpad = (int)glr_heat_stride(H, W, P);
   hp.n_max = n_max;
-  hp.m_tiles_per_row = (int)cdiv(g.ow, 2 * heat::BM) * 2;  // even: tiles go in pairs
+  hp.m_tiles_per_row = (int)cdiv(g.ow, heat::CL * heat::BM) * heat::CL;  // tiles go in clusters
   hp.S = g.S;
   hp.kchunks = g.kchunks;
   hp.e = g.e;
@@ -381,7 +383,7 @@ extern "C" int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, 
                                   heat::SMEM_BYTES));
     attr_set = true;
   }
-  const int64_t pairs = (int64_t)g.oh * (hp.m_tiles_per_row / 2) * (n_pad / heat::BN);
+  const int64_t pairs = (int64_t)g.oh * (hp.m_tiles_per_row / heat::CL) * (n_pad / heat::BN);
   GLR_REQUIRE(pairs < (1ll << 31), GLR_ERR_UNSUPPORTED, "heat_map: too many tiles");
   int sms = kNumSMs;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -391,7 +393,7 @@ extern "C" int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, 
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = heat::CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -400,13 +402,13 @@ extern "C" int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, 
   // be co-resident (the GPCs need not split into pairs evenly)
   static int max_clusters = 0;
   if (max_clusters == 0) {
-    cfg.gridDim = dim3(2 * (sms / 2));
+    cfg.gridDim = dim3(heat::CL * (sms / heat::CL));
     if (cudaOccupancyMaxActiveClusters(&max_clusters, heat_gemm_kernel, &cfg) != cudaSuccess ||
         max_clusters < 1)
-      max_clusters = sms / 2;
+      max_clusters = sms / heat::CL;
     cudaGetLastError();
   }
-  cfg.gridDim = dim3(2 * (unsigned)std::min<int64_t>(pairs, max_clusters));
+  cfg.gridDim = dim3(heat::CL * (unsigned)std::min<int64_t>(pairs, max_clusters));
   GLR_CUDA(cudaLaunchKernelEx(&cfg, heat_gemm_kernel, tmA, tmB, hp));
   return GLR_OK;
 }

@@ -102,41 +102,79 @@ struct GapArgs {
   double* part;
 };
 
-__global__ void __launch_bounds__(gap::THREADS) gap_masksum_kernel(GapArgs a) {
-  double z[gap::TMAX], prod[gap::TMAX];
+// TT > 0: channel count fixed at compile time (arrays in registers, 16-byte
+// loads); TT = 0: any T <= TMAX (arrays in local memory).
+template <int TT>
+__global__ void __launch_bounds__(gap::THREADS, 2) gap_masksum_kernel(GapArgs a) {
+  constexpr int TA = TT > 0 ? TT : gap::TMAX;
+  const int T = TT > 0 ? TT : a.T;
+  double z[TA], mk[TA], prod[TA];
   double acc_sq = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.npix;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int T = a.T;
     const int n = a.cnt ? a.cnt[i] : 0;
-    for (int t = 0; t < T; ++t) {
-      const int64_t k = i * T + t;
-      z[t] = n > 0 ? ((double)a.acc[k] * a.inv_scale) / (double)n : a.x_in[k];
+    if constexpr (TT > 0 && TT % 2 == 0) {
+      const double2* mk2 = reinterpret_cast<const double2*>(a.mk + i * TT);
+#pragma unroll
+      for (int t = 0; t < TT / 2; ++t) {
+        const double2 m = mk2[t];
+        mk[2 * t] = m.x;
+        mk[2 * t + 1] = m.y;
+      }
+      if (n > 0) {
+        const longlong2* ac2 = reinterpret_cast<const longlong2*>(a.acc + i * TT);
+#pragma unroll
+        for (int t = 0; t < TT / 2; ++t) {
+          const longlong2 v = ac2[t];
+          z[2 * t] = ((double)v.x * a.inv_scale) / (double)n;
+          z[2 * t + 1] = ((double)v.y * a.inv_scale) / (double)n;
+        }
+      } else {
+        const double2* x2 = reinterpret_cast<const double2*>(a.x_in + i * TT);
+#pragma unroll
+        for (int t = 0; t < TT / 2; ++t) {
+          const double2 v = x2[t];
+          z[2 * t] = v.x;
+          z[2 * t + 1] = v.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const int64_t k = i * T + t;
+        mk[t] = a.mk[k];
+        z[t] = n > 0 ? ((double)a.acc[k] * a.inv_scale) / (double)n : a.x_in[k];
+      }
     }
     double gram;
     if (a.gram) {
       gram = a.gram[i];
     } else {
-      for (int t = 0; t < T; ++t) {
-        const double m = a.mk[i * T + t];
-        prod[t] = __dmul_rn(m, m);
-      }
+#pragma unroll
+      for (int t = 0; t < T; ++t) prod[t] = __dmul_rn(mk[t], mk[t]);
       gram = pw_sum(prod, T);
     }
-    for (int t = 0; t < T; ++t) prod[t] = __dmul_rn(a.mk[i * T + t], z[t]);
+#pragma unroll
+    for (int t = 0; t < T; ++t) prod[t] = __dmul_rn(mk[t], z[t]);
     const double az = pw_sum(prod, T);
     const double yi = a.y[i];
     // GAP: safe_div(y - Az, gram) (solvers.py:220-226, rho = 0);
     // ADMM: (y - Am) / (rho + gram) (solvers.py:329)
     const double den = a.rho != 0.0 ? __dadd_rn(a.rho, gram) : gram;
     const double r = den != 0.0 ? __ddiv_rn(__dsub_rn(yi, az), den) : 0.0;
+#pragma unroll
     for (int t = 0; t < T; ++t) {
-      const double m = a.mk[i * T + t];
-      double v = __dadd_rn(z[t], __dmul_rn(m, r));
-      v = fmin(fmax(v, a.lo), a.hi);
-      z[t] = v;
-      a.x_out[i * T + t] = v;
-      prod[t] = __dmul_rn(m, v);
+      double v = __dadd_rn(z[t], __dmul_rn(mk[t], r));
+      z[t] = fmin(fmax(v, a.lo), a.hi);
+      prod[t] = __dmul_rn(mk[t], z[t]);
+    }
+    if constexpr (TT > 0 && TT % 2 == 0) {
+      double2* o2 = reinterpret_cast<double2*>(a.x_out + i * TT);
+#pragma unroll
+      for (int t = 0; t < TT / 2; ++t) o2[t] = make_double2(z[2 * t], z[2 * t + 1]);
+    } else {
+#pragma unroll
+      for (int t = 0; t < T; ++t) a.x_out[i * T + t] = z[t];
     }
     const double d = __dsub_rn(yi, pw_sum(prod, T));
     acc_sq = fma(d, d, acc_sq);
@@ -156,7 +194,7 @@ __global__ void sq_err_kernel(const double* __restrict__ x, const double* __rest
   block_sum_store(s, part);
 }
 
-constexpr int kGapBlocks = 2 * kNumSMs;
+constexpr int kGapBlocks = 8 * kNumSMs;
 
 // out = clip((a x + b y) + c z) elementwise (z optional), evaluated in that
 // order so ADMM's m = z - u, v = x + u, u' = (u + x) - z match numpy bitwise
@@ -220,7 +258,13 @@ extern "C" int glr_gap_masksum(const int64_t* acc_d, const int32_t* cnt_d, int f
   a.hi = hi;
   a.x_out = x_out_d;
   a.part = reinterpret_cast<double*>(ws_d);
-  gap_masksum_kernel<<<kGapBlocks, gap::THREADS, 0, st>>>(a);
+  switch (T) {
+    case 8: gap_masksum_kernel<8><<<kGapBlocks, gap::THREADS, 0, st>>>(a); break;
+    case 16: gap_masksum_kernel<16><<<kGapBlocks, gap::THREADS, 0, st>>>(a); break;
+    case 24: gap_masksum_kernel<24><<<kGapBlocks, gap::THREADS, 0, st>>>(a); break;
+    case 32: gap_masksum_kernel<32><<<kGapBlocks, gap::THREADS, 0, st>>>(a); break;
+    default: gap_masksum_kernel<0><<<kGapBlocks, gap::THREADS, 0, st>>>(a); break;
+  }
   GLR_CUDA(cudaGetLastError());
   final_sum_kernel<<<1, 256, 0, st>>>(a.part, kGapBlocks, resid_d);
   return check_launch("final_sum_kernel");

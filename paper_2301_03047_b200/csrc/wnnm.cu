@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(wn::GRAM_THREADS) gram_kernel(GroupSrc s, int 
 #ifdef GLR_EIG_STATS
 // dev statistics: groups per sweep count (cold [0, 32), warm [32, 64))
 __device__ unsigned int g_eig_hist[64];
+__device__ unsigned int g_rank_hist[65];  // groups by number of kept components
 #endif
 
 struct EigArgs {
@@ -525,6 +526,13 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
     ratio[tid] = r;
   }
   __syncthreads();
+#ifdef GLR_EIG_STATS
+  if (tid == 0) {
+    int kept = 0;
+    for (int k = 0; k < KMAX; ++k) kept += ratio[k] != 0.0;
+    atomicAdd(&g_rank_hist[kept], 1u);
+  }
+#endif
   // Wm = V diag(ratio) V^T -> global
   double o[4][4];
 #pragma unroll
@@ -761,9 +769,11 @@ using namespace glr;
 #ifdef GLR_EIG_STATS
 extern "C" int glr_debug_eig_hist(unsigned int* out, int reset) {
   cudaMemcpyFromSymbol(out, g_eig_hist, sizeof(unsigned int) * 64);
+  cudaMemcpyFromSymbol(out + 64, g_rank_hist, sizeof(unsigned int) * 65);
   if (reset) {
-    unsigned int z[64] = {};
-    cudaMemcpyToSymbol(g_eig_hist, z, sizeof(z));
+    unsigned int z[65] = {};
+    cudaMemcpyToSymbol(g_eig_hist, z, sizeof(unsigned int) * 64);
+    cudaMemcpyToSymbol(g_rank_hist, z, sizeof(unsigned int) * 65);
   }
   return 0;
 }

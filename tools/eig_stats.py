@@ -19,18 +19,22 @@ y = r.dop.upload_y(wl.y)
 lib = N.load()
 fn = lib.glr_debug_eig_hist
 fn.argtypes = [C.c_void_p, C.c_int]
-buf = (C.c_uint * 64)()
+buf = (C.c_uint * 129)()
 fn(buf, 1)
 
 
 def on_iter(it, x):
     torch.cuda.synchronize()
     fn(buf, 1)
-    h = np.array(buf[:])
+    h = np.array(buf[:64])
     cold = {i: int(v) for i, v in enumerate(h[:32]) if v}
     warm = {i: int(v) for i, v in enumerate(h[32:]) if v}
     tot = h[:32] @ np.arange(32) + h[32:] @ np.arange(32)
-    print(f"it {it:2d} mean sweeps {tot / max(h.sum(), 1):.2f} cold {cold} warm {warm}")
+    rk = np.array(buf[64:129])
+    cum = np.cumsum(rk) / max(rk.sum(), 1)
+    q = [int(np.searchsorted(cum, f)) for f in (0.1, 0.5, 0.9, 0.99)]
+    print(f"it {it:2d} mean sweeps {tot / max(h.sum(), 1):.2f} cold {cold} warm {warm} "
+          f"kept-rank mean {rk @ np.arange(65) / max(rk.sum(), 1):.1f} p10/50/90/99 {q}")
 
 
 r.run(y, on_iter=on_iter)

@@ -410,6 +410,69 @@ __global__ void __launch_bounds__(1024) nms_kernel(const uint64_t* __restrict__ 
   if (tid == 0) *out_n = s_picked;
 }
 
+// Same greedy NMS with the blocked set as a shared-memory BITMAP (one bit per
+// pixel: 128 KB for 1024 x 1024): one warp walks the ranked candidates 32 at
+// a time; the first unblocked lane is the next pick (exactly the sequential
+// rule), its (2R+1)-row neighbourhood is or-ed into the bitmap by 2R+1 lanes,
+// and the remaining lanes are re-tested. Cost ~ picks + candidates / 32 warp
+// steps instead of a per-survivor conflict scan.
+__global__ void __launch_bounds__(1024) nms_bitmap_kernel(const uint64_t* __restrict__ keys,
+                                                          const int32_t* __restrict__ idx,
+                                                          int64_t total, int H, int W, int max_n,
+                                                          int R, int32_t* __restrict__ out_rc,
+                                                          int32_t* __restrict__ out_n) {
+  extern __shared__ uint32_t bm[];
+  const int nw = (int)(((int64_t)H * W + 31) / 32);
+  for (int i = threadIdx.x; i < nw; i += blockDim.x) bm[i] = 0u;
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const unsigned full = 0xffffffffu;
+  int picked = 0;
+  for (int64_t base = 0; base < total && picked < max_n; base += 32) {
+    const int64_t i = base + lane;
+    const uint64_t key = i < total ? keys[i] : 0ull;
+    if (__ballot_sync(full, key != 0ull) == 0u) break;  // descending: the rest are zero
+    const int cand = key != 0ull ? idx[i] : 0;
+    const int r = cand / W, c = cand - (cand / W) * W;
+    bool live = key != 0ull;
+    while (true) {
+      const bool free_px = live && !((bm[cand >> 5] >> (cand & 31)) & 1u);
+      const unsigned m = __ballot_sync(full, free_px);
+      if (m == 0u) break;
+      const int first = __ffs(m) - 1;
+      const int pr = __shfl_sync(full, r, first), pc = __shfl_sync(full, c, first);
+      if (lane == 0) {
+        out_rc[2 * picked] = pr;
+        out_rc[2 * picked + 1] = pc;
+      }
+      ++picked;
+      if (lane <= 2 * R) {
+        const int rr = pr - R + lane;
+        if (rr >= 0 && rr < H) {
+          const int64_t b0 = (int64_t)rr * W + max(pc - R, 0);
+          const int64_t b1 = (int64_t)rr * W + min(pc + R, W - 1);
+          const int w0 = (int)(b0 >> 5), w1 = (int)(b1 >> 5);
+          const unsigned lo = ~0u << (b0 & 31);
+          const unsigned hi = (b1 & 31) == 31 ? ~0u : ((1u << ((b1 & 31) + 1)) - 1u);
+          if (w0 == w1) {
+            atomicOr(&bm[w0], lo & hi);
+          } else {
+            atomicOr(&bm[w0], lo);
+            atomicOr(&bm[w1], hi);
+          }
+        }
+      }
+      __syncwarp();
+      if (picked >= max_n) break;
+      live = live && lane > first;
+    }
+  }
+  if (lane == 0) *out_n = picked;
+}
+
+constexpr int kNmsBitmapMaxBytes = 200 * 1024;
+
 // ---------------------------------------------------------------------------
 // A4: anchors (edges.py:131-162)
 
@@ -609,6 +672,19 @@ extern "C" int glr_corners(const double* resp_d, int H, int W, int max_n, int nm
   GLR_CUDA(cudaGetLastError());
   GLR_CUDA(cub::DeviceRadixSort::SortPairsDescending(p, temp_bytes, k_in, k_out, v_in, v_out,
                                                      (int)n, 0, 64, st));
+  const size_t bm_bytes = (size_t)((n + 31) / 32) * sizeof(uint32_t);
+  if (bm_bytes <= (size_t)kNmsBitmapMaxBytes && nms_radius <= 15) {
+    static bool attr = false;
+    if (!attr) {
+      GLR_CUDA(cudaFuncSetAttribute(nms_bitmap_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kNmsBitmapMaxBytes));
+      attr = true;
+    }
+    nms_bitmap_kernel<<<1, 1024, bm_bytes, st>>>(k_out, v_out, n, H, W, max_n, nms_radius,
+                                                 out_rc_d, out_n_d);
+    return check_launch("nms_bitmap_kernel");
+  }
   nms_kernel<<<1, 1024, 0, st>>>(k_out, v_out, n, H, W, max_n, nms_radius, blocked, out_rc_d,
                                  out_n_d);
   return check_launch("nms_kernel");

@@ -10,13 +10,14 @@
 //   a second walk with sep = 0; missing slots repeat the anchor ("padded").
 //
 // One CTA per exemplar over its u16 heat-map row:
-//   1. shared-memory histogram of the integer scores;
+//   1. shared-memory histogram of the integer scores (only the top range
+//      unless the cut falls below it);
 //   2. the cut T = largest score with count(>= T) >= need, need = min(pool, M)
 //      where pool = K(2 sep + 1)^2 + 1 (the reference's bound: the first pool
 //      entries of the ordered walk always fill the group, matching.py:219-225);
-//   3. one ordered pass compacting A = {score > T} (all, < need entries) and
-//      the first need-|A| entries of B = {score == T} in index order — this
-//      is exactly the first `need` entries of the reference's ordered walk;
+//   3. one pass collecting A = {score > T} (all, < need entries) and the ties
+//      B = {score == T}, of which the first need-|A| in index order are kept
+//      — exactly the first `need` entries of the reference's ordered walk;
 //   4. bitonic sort of A by (score desc, index asc) in shared memory;
 //   5. one warp runs the greedy walk, 32 candidates per step: lanes test
 //      their candidate against the chosen set in parallel, then accepted
@@ -41,6 +42,7 @@ struct TopkParams {
   int bins;  // max_score + 1
   const int32_t* anchors;
   int K, sep, pool, a_cap;  // a_cap: power of two >= pool
+  int b_cap;                // tie buffer: power of two >= max(pool, 4096)
   int32_t* positions;
   int32_t* padded;
 };
@@ -49,15 +51,16 @@ __device__ __forceinline__ int cheb(int r0, int c0, int r1, int c1) {
   return max(abs(r0 - r1), abs(c0 - c1));
 }
 
-__global__ void __launch_bounds__(topk::THREADS) topk_kernel(TopkParams p) {
+__global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   using namespace topk;
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* sA = reinterpret_cast<uint64_t*>(smem);                   // a_cap
-  int32_t* sB = reinterpret_cast<int32_t*>(sA + p.a_cap);              // pool
-  int32_t* hist = sB + p.pool;                                         // bins
+  int32_t* sB = reinterpret_cast<int32_t*>(sA + p.a_cap);              // b_cap
+  int32_t* hist = sB + p.b_cap;                                        // bins
   int32_t* chosen = hist + p.bins;                                     // 2*K
   __shared__ int warp_tot[32];
-  __shared__ int s_total, s_T, s_cntA, s_baseA, s_baseB;
+  __shared__ int s_total, s_T, s_cntA, s_baseA, s_baseB, s_na, s_nb, s_found;
+  const int BCAP = p.b_cap;
 
   const int n = blockIdx.x;
   const int N = p.n_dev ? min(*p.n_dev, p.n_max) : p.n_max;
@@ -67,39 +70,57 @@ __global__ void __launch_bounds__(topk::THREADS) topk_kernel(TopkParams p) {
   const int64_t M = p.M;
   const int need = (int)(M < (int64_t)p.pool ? M : (int64_t)p.pool);
 
-  // 1. histogram
-  for (int b = tid; b < p.bins; b += THREADS) hist[b] = 0;
-  __syncthreads();
-  for (int64_t base = (int64_t)tid * VEC; base < M; base += (int64_t)THREADS * VEC * 2) {
-    // two independent 16-byte loads in flight per thread
-    const int64_t b1 = base + (int64_t)THREADS * VEC;
-    const uint4 v0 = *reinterpret_cast<const uint4*>(row + base);
-    const uint4 v1 = b1 < M ? *reinterpret_cast<const uint4*>(row + b1) : make_uint4(0, 0, 0, 0);
-    const uint16_t* s0 = reinterpret_cast<const uint16_t*>(&v0);
-    const uint16_t* s1 = reinterpret_cast<const uint16_t*>(&v1);
-#pragma unroll
-    for (int j = 0; j < VEC; ++j)
-      if (base + j < M) atomicAdd(&hist[min((int)s0[j], p.bins - 1)], 1);
-#pragma unroll
-    for (int j = 0; j < VEC; ++j)
-      if (b1 + j < M) atomicAdd(&hist[min((int)s1[j], p.bins - 1)], 1);
+  // 1. histogram of the scores >= L, L = a quarter of the anchor's own score
+  //    (for a heat map the row maximum: |E_u ∩ E_n| <= |E_n|), so the bulk of
+  //    low scores costs no shared-memory atomics. If fewer than `need`
+  //    positions reach L (or the row is not a heat map), a second pass adds
+  //    the bins below L -- the cut is exact either way.
+  const int64_t aidx = (int64_t)p.anchors[2 * n] * p.ow + p.anchors[2 * n + 1];
+  const int L = min((int)row[aidx] >> 2, p.bins - 1);
+  for (int b = L + tid; b < p.bins; b += THREADS) hist[b] = 0;
+  if (tid == 0) {
+    s_na = 0;
+    s_nb = 0;
   }
   __syncthreads();
+  auto hist_pass = [&](int lo, int hi) {  // add the scores in [lo, hi)
+    constexpr int U = 4;  // 16-byte loads in flight per thread
+    for (int64_t tile = 0; tile < M; tile += (int64_t)THREADS * VEC * U) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t base = tile + ((int64_t)u * THREADS + tid) * VEC;
+        v[u] = base < M ? *reinterpret_cast<const uint4*>(row + base) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t base = tile + ((int64_t)u * THREADS + tid) * VEC;
+        const uint16_t* sv = reinterpret_cast<const uint16_t*>(&v[u]);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          const int val = min((int)sv[j], p.bins - 1);
+          if (base + j < M && val >= lo && val < hi) atomicAdd(&hist[val], 1);
+        }
+      }
+    }
+  };
+  hist_pass(L, p.bins);
+  __syncthreads();
 
-  // 2. cut score T: walk bins from the top, 32 at a time
-  if (warp == 0) {
+  // 2. cut score T: walk bins from the top down to `lo`, 32 at a time
+  auto cut_search = [&](int lo) {
     int running = 0;
     int T = 0, cntA = 0;
     bool found = false;
-    for (int top = p.bins - 1; top >= 0 && !found; top -= 32) {
+    for (int top = p.bins - 1; top >= lo && !found; top -= 32) {
       const int b = top - lane;
-      const int c = b >= 0 ? hist[b] : 0;
+      const int c = b >= lo ? hist[b] : 0;
       int incl = c;  // inclusive prefix from the top (lane 0 = highest bin)
       for (int o = 1; o < 32; o <<= 1) {
         int y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += y;
       }
-      const unsigned hit = __ballot_sync(0xffffffffu, b >= 0 && running + incl >= need);
+      const unsigned hit = __ballot_sync(0xffffffffu, b >= lo && running + incl >= need);
       if (hit) {
         const int l = __ffs(hit) - 1;
         T = top - l;
@@ -111,51 +132,133 @@ __global__ void __launch_bounds__(topk::THREADS) topk_kernel(TopkParams p) {
     if (lane == 0) {
       s_T = T;
       s_cntA = cntA;
-      s_baseA = 0;
-      s_baseB = 0;
+      s_found = found ? 1 : 0;
     }
-  }
+  };
+  if (warp == 0) cut_search(L);
   __syncthreads();
+  if (!s_found) {
+    for (int b = tid; b < L; b += THREADS) hist[b] = 0;
+    __syncthreads();
+    hist_pass(0, L);
+    __syncthreads();
+    if (warp == 0) cut_search(0);
+    __syncthreads();
+  }
   const int T = s_T, cntA = s_cntA, capB = need - cntA;
 
-  // 3. ordered compaction of A (score > T) and the first capB of B (score == T)
-  for (int64_t tile = 0; tile < M; tile += (int64_t)THREADS * VEC) {
-    if (s_baseA >= cntA && s_baseB >= capB) break;  // block-uniform
-    const int64_t base = tile + (int64_t)tid * VEC;
-    uint16_t s[VEC];
-    int a = 0, b = 0;
-    if (base < M) {
-      const uint4 v = *reinterpret_cast<const uint4*>(row + base);
-      const uint16_t* sv = reinterpret_cast<const uint16_t*>(&v);
+  // 3. collect A = {score > T} (cntA < need entries) and the ties {score == T};
+  //    unordered warp-aggregated appends when the ties fit the buffer (they are
+  //    then sorted by index), else an ordered block-scan compaction.
+  if (hist[T] <= BCAP) {
+    constexpr int U = 4;  // 16-byte loads in flight per thread
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t tile = 0; tile < M; tile += (int64_t)THREADS * VEC * U) {
+      uint4 v[U];
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) {
-        s[j] = (base + j < M) ? sv[j] : 0;
-        const bool valid = base + j < M;
-        a += valid && s[j] > T;
-        b += valid && s[j] == T;
+      for (int u = 0; u < U; ++u) {
+        const int64_t base = tile + ((int64_t)u * THREADS + tid) * VEC;
+        v[u] = base < M ? *reinterpret_cast<const uint4*>(row + base) : make_uint4(0, 0, 0, 0);
       }
-    }
-    const int pre = block_excl_scan_1024(a | (b << 16), warp_tot, &s_total);
-    int ia = s_baseA + (pre & 0xFFFF);
-    int ib = s_baseB + (pre >> 16);
-    if (a | b) {
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) {
-        if (base + j >= M) break;
-        if (s[j] > T) {
-          sA[ia++] = ((uint64_t)(65535 - s[j]) << 32) | (uint32_t)(base + j);
-        } else if (s[j] == T) {
-          if (ib < capB) sB[ib] = (int32_t)(base + j);
-          ++ib;
+      for (int u = 0; u < U; ++u) {
+        const int64_t base = tile + ((int64_t)u * THREADS + tid) * VEC;
+        const uint16_t* sv = reinterpret_cast<const uint16_t*>(&v[u]);
+        // warp-uniform skip of chunks holding no candidate (the common case)
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) any |= base + j < M && sv[j] >= T;
+        if (!__any_sync(0xffffffffu, any)) continue;
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          const bool ok = base + j < M;
+          const bool isA = ok && sv[j] > T, isB = ok && sv[j] == T;
+          const unsigned mA = __ballot_sync(0xffffffffu, isA);
+          const unsigned mB = __ballot_sync(0xffffffffu, isB);
+          if (mA) {
+            int off = 0;
+            if (lane == __ffs(mA) - 1) off = atomicAdd(&s_na, __popc(mA));
+            off = __shfl_sync(0xffffffffu, off, __ffs(mA) - 1);
+            if (isA)
+              sA[off + __popc(mA & lt)] =
+                  ((uint64_t)(65535 - sv[j]) << 32) | (uint32_t)(base + j);
+          }
+          if (mB) {
+            int off = 0;
+            if (lane == __ffs(mB) - 1) off = atomicAdd(&s_nb, __popc(mB));
+            off = __shfl_sync(0xffffffffu, off, __ffs(mB) - 1);
+            if (isB) sB[off + __popc(mB & lt)] = (int32_t)(base + j);
+          }
         }
       }
     }
     __syncthreads();
+    // ties in index order (bitonic, padded to a power of two)
+    const int nB = s_nb;
+    int szb = 1;
+    while (szb < nB) szb <<= 1;
+    for (int i = nB + tid; i < szb; i += THREADS) sB[i] = 0x7fffffff;
+    __syncthreads();
+    for (int k = 2; k <= szb; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = tid; i < szb; i += THREADS) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const int32_t x = sB[i], y = sB[ixj];
+            const bool up = (i & k) == 0;
+            if ((x > y) == up) {
+              sB[i] = y;
+              sB[ixj] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+  } else {
     if (tid == 0) {
-      s_baseA += s_total & 0xFFFF;
-      s_baseB += s_total >> 16;
+      s_baseA = 0;
+      s_baseB = 0;
     }
     __syncthreads();
+    for (int64_t tile = 0; tile < M; tile += (int64_t)THREADS * VEC) {
+      if (s_baseA >= cntA && s_baseB >= capB) break;  // block-uniform
+      const int64_t base = tile + (int64_t)tid * VEC;
+      uint16_t s[VEC];
+      int a = 0, b = 0;
+      if (base < M) {
+        const uint4 v = *reinterpret_cast<const uint4*>(row + base);
+        const uint16_t* sv = reinterpret_cast<const uint16_t*>(&v);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          s[j] = (base + j < M) ? sv[j] : 0;
+          const bool valid = base + j < M;
+          a += valid && s[j] > T;
+          b += valid && s[j] == T;
+        }
+      }
+      const int pre = block_excl_scan_1024(a | (b << 16), warp_tot, &s_total);
+      int ia = s_baseA + (pre & 0xFFFF);
+      int ib = s_baseB + (pre >> 16);
+      if (a | b) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          if (base + j >= M) break;
+          if (s[j] > T) {
+            sA[ia++] = ((uint64_t)(65535 - s[j]) << 32) | (uint32_t)(base + j);
+          } else if (s[j] == T) {
+            if (ib < capB) sB[ib] = (int32_t)(base + j);
+            ++ib;
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        s_baseA += s_total & 0xFFFF;
+        s_baseB += s_total >> 16;
+      }
+      __syncthreads();
+    }
   }
 
   // 4. bitonic sort of A (padded to the next power of two >= cntA)
@@ -246,10 +349,15 @@ __global__ void gather_kernel(const double* __restrict__ x, int H, int W, int C,
 
 static int topk_pool(int K, int sep) { return K * (2 * sep + 1) * (2 * sep + 1) + 1; }
 
+static int pow2_at_least(int v) {
+  int c = 1;
+  while (c < v) c <<= 1;
+  return c;
+}
+
 static size_t topk_smem(int pool, int bins, int K) {
-  int a_cap = 1;
-  while (a_cap < pool) a_cap <<= 1;
-  return (size_t)a_cap * 8 + (size_t)pool * 4 + (size_t)bins * 4 + (size_t)K * 8 + 16;
+  return (size_t)pow2_at_least(pool) * 8 + (size_t)pow2_at_least(std::max(pool, 4096)) * 4 +
+         (size_t)bins * 4 + (size_t)K * 8 + 16;
 }
 
 }  // namespace glr
@@ -287,8 +395,8 @@ extern "C" int glr_topk(const uint16_t* heat_d, int n_max, const int32_t* n_dev_
   p.K = K;
   p.sep = sep;
   p.pool = pool;
-  p.a_cap = 1;
-  while (p.a_cap < pool) p.a_cap <<= 1;
+  p.a_cap = pow2_at_least(pool);
+  p.b_cap = pow2_at_least(std::max(pool, 4096));
   p.positions = positions_d;
   p.padded = padded_d;
   GLR_CUDA(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -222,11 +222,15 @@ class GlrEngine:
         h, w, c = self.shape
         mc = self.mc
         s = D.stream()
+        e = self._ev()
         N.call("glr_corner_response", x_d.data_ptr(), h, w, c, self.resp.data_ptr(),
                self.ws_corner.data_ptr(), s)
+        self._log(("corner_response", 1), e)
+        e = self._ev()
         N.call("glr_corners", self.resp.data_ptr(), h, w, mc.max_corners, mc.nms,
                float(mc.corner_quality), self.corners.data_ptr(), self.n_corners.data_ptr(),
                self.ws_nms.data_ptr(), self.ws_nms.numel(), s)
+        self._log(("corners_nms", 1), e)
         old_anchors, old_n, old_lo, old_hi = self.anchors, self.n, self.lo, self.hi
         self._acur ^= 1
         self.anchors = self._anc[self._acur]
@@ -251,10 +255,12 @@ class GlrEngine:
         self.vcache_valid = False
         if n == 0:
             return 0
+        e = self._ev()
         N.call("glr_sobel", x_d.data_ptr(), h, w, c, self.gh.data_ptr(), self.gv.data_ptr(), s)
         N.call("glr_edge_stack", self.gh.data_ptr(), self.gv.data_ptr(), h, w, c,
                float(mc.edge_threshold), 1, self.expand, None, self.stack.data_ptr(),
                self.ws_edge.data_ptr(), s)
+        self._log(("edge_stack", 1), e)
         self.match_shard()
         self.count()
         return n

@@ -41,6 +41,19 @@ def test_edges_corners_anchors_bitwise_vs_golden():
         assert [t == "uniform" for t in ex.tags] == g[f"tags{i}"].astype(bool).tolist()
 
 
+@pytest.mark.parametrize("shape,max_n,radius", [((300, 280, 3), 500, 4), ((1300, 1300, 1), 60, 4),
+                                              ((97, 131, 2), 5000, 2), ((64, 64, 1), 10, 17)])
+def test_detect_corners_vs_oracle(shape, max_n, radius, rng):
+    """Greedy NMS (edges.py:100-128): the shared-memory bitmap walk, and the
+    global-memory fallback (over 1.6 MPixel or radius > 15), vs the oracle."""
+    h, w, c = shape
+    base = rng.random((h // 4 + 2, w // 4 + 2, c))
+    x = np.kron(base, np.ones((4, 4, 1)))[:h, :w] + 0.05 * rng.random((h, w, c))
+    got = G.detect_corners(x, max_n=max_n, nms_radius=radius)
+    want = O.detect_corners(x, max_n=max_n, nms_radius=radius)
+    assert [tuple(p) for p in got] == [tuple(p) for p in want]
+
+
 def test_corner_response_bitwise_vs_oracle(rng):
     from paper_2301_03047_b200 import _device as D, _native as N
     import torch

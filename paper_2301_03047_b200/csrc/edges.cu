@@ -269,9 +269,23 @@ __device__ __forceinline__ void box3_line(const double* __restrict__ in, double*
   };
   double t = __dadd_rn(__dadd_rn(P(0), P(1)), P(2));
   out[0] = __ddiv_rn(t, 3.0);
-  for (int i = 1; i < n; ++i) {
-    t = __dadd_rn(t, __dsub_rn(P(i + 2), P(i - 1)));
-    out[i * step] = __ddiv_rn(t, 3.0);
+  // the recurrence is sequential (bitwise scipy order); the loads are not:
+  // fetch CH samples ahead so only the two adds sit on the dependency chain
+  constexpr int CH = 16;
+  for (int i0 = 1; i0 < n; i0 += CH) {
+    double nx[CH], pv[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      nx[c] = P(i0 + c + 2);
+      pv[c] = P(i0 + c - 1);
+    }
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if (i0 + c < n) {
+        t = __dadd_rn(t, __dsub_rn(nx[c], pv[c]));
+        out[(int64_t)(i0 + c) * step] = __ddiv_rn(t, 3.0);
+      }
+    }
   }
 }
 
@@ -331,16 +345,21 @@ __global__ void resp_max_kernel(const double* __restrict__ resp, int64_t n,
 // quality * max, only when max > 0), 0 otherwise; values = flat index.
 __global__ void cand_keys_kernel(const double* __restrict__ resp, int64_t n, double quality,
                                  const unsigned long long* mx, uint64_t* __restrict__ keys,
-                                 int32_t* __restrict__ idx) {
+                                 int32_t* __restrict__ idx, int* __restrict__ n_cand) {
   const double rmax = unord64(*mx);
   const double thr = __dmul_rn(quality, rmax);
   const bool any = rmax > 0.0;
+  int cnt = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const double v = resp[i];
-    keys[i] = (any && v >= thr) ? ord64(v) : 0ull;
+    const bool c = any && v >= thr;
+    keys[i] = c ? ord64(v) : 0ull;
     idx[i] = (int32_t)i;
+    cnt += c;
   }
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(n_cand, cnt);
 }
 
 __global__ void __launch_bounds__(1024) nms_kernel(const uint64_t* __restrict__ keys,
@@ -412,14 +431,13 @@ __global__ void __launch_bounds__(1024) nms_kernel(const uint64_t* __restrict__ 
 
 // Same greedy NMS with the blocked set as a shared-memory BITMAP (one bit per
 // pixel: 128 KB for 1024 x 1024): one warp walks the ranked candidates 32 at
-// a time; the first unblocked lane is the next pick (exactly the sequential
-// rule), its (2R+1)-row neighbourhood is or-ed into the bitmap by 2R+1 lanes,
-// and the remaining lanes are re-tested. Cost ~ picks + candidates / 32 warp
-// steps instead of a per-survivor conflict scan.
-__global__ void __launch_bounds__(1024) nms_bitmap_kernel(const uint64_t* __restrict__ keys,
-                                                          const int32_t* __restrict__ idx,
-                                                          int64_t total, int H, int W, int max_n,
-                                                          int R, int32_t* __restrict__ out_rc,
+// a time (prefetched 256 ahead); the first unblocked lane is the next pick
+// (exactly the sequential rule), its (2R+1)-row neighbourhood is or-ed into
+// the bitmap by 2R+1 lanes, and the remaining lanes are re-tested.
+__global__ void __launch_bounds__(1024) nms_bitmap_kernel(const int32_t* __restrict__ idx,
+                                                          const int* __restrict__ n_cand, int H,
+                                                          int W, int max_n, int R,
+                                                          int32_t* __restrict__ out_rc,
                                                           int32_t* __restrict__ out_n) {
   extern __shared__ uint32_t bm[];
   const int nw = (int)(((int64_t)H * W + 31) / 32);
@@ -428,45 +446,61 @@ __global__ void __launch_bounds__(1024) nms_bitmap_kernel(const uint64_t* __rest
   if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
   const unsigned full = 0xffffffffu;
+  const int total = *n_cand;  // ranked candidates idx[0 .. total)
+  constexpr int U = 8;        // batches of 32 fetched per round trip (double-buffered)
+  int cur[U], nxt[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int i = u * 32 + lane;
+    cur[u] = i < total ? idx[i] : -1;
+  }
   int picked = 0;
-  for (int64_t base = 0; base < total && picked < max_n; base += 32) {
-    const int64_t i = base + lane;
-    const uint64_t key = i < total ? keys[i] : 0ull;
-    if (__ballot_sync(full, key != 0ull) == 0u) break;  // descending: the rest are zero
-    const int cand = key != 0ull ? idx[i] : 0;
-    const int r = cand / W, c = cand - (cand / W) * W;
-    bool live = key != 0ull;
-    while (true) {
-      const bool free_px = live && !((bm[cand >> 5] >> (cand & 31)) & 1u);
-      const unsigned m = __ballot_sync(full, free_px);
-      if (m == 0u) break;
-      const int first = __ffs(m) - 1;
-      const int pr = __shfl_sync(full, r, first), pc = __shfl_sync(full, c, first);
-      if (lane == 0) {
-        out_rc[2 * picked] = pr;
-        out_rc[2 * picked + 1] = pc;
-      }
-      ++picked;
-      if (lane <= 2 * R) {
-        const int rr = pr - R + lane;
-        if (rr >= 0 && rr < H) {
-          const int64_t b0 = (int64_t)rr * W + max(pc - R, 0);
-          const int64_t b1 = (int64_t)rr * W + min(pc + R, W - 1);
-          const int w0 = (int)(b0 >> 5), w1 = (int)(b1 >> 5);
-          const unsigned lo = ~0u << (b0 & 31);
-          const unsigned hi = (b1 & 31) == 31 ? ~0u : ((1u << ((b1 & 31) + 1)) - 1u);
-          if (w0 == w1) {
-            atomicOr(&bm[w0], lo & hi);
-          } else {
-            atomicOr(&bm[w0], lo);
-            atomicOr(&bm[w1], hi);
+  for (int base = 0; base < total && picked < max_n; base += 32 * U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + 32 * U + u * 32 + lane;
+      nxt[u] = i < total ? idx[i] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int cand = cur[u];
+      if (__ballot_sync(full, cand >= 0) == 0u || picked >= max_n) break;
+      const int r = cand >= 0 ? cand / W : 0, c = cand >= 0 ? cand - (cand / W) * W : 0;
+      bool live = cand >= 0;
+      while (true) {
+        const bool free_px = live && !((bm[cand >> 5] >> (cand & 31)) & 1u);
+        const unsigned m = __ballot_sync(full, free_px);
+        if (m == 0u) break;
+        const int first = __ffs(m) - 1;
+        const int pr = __shfl_sync(full, r, first), pc = __shfl_sync(full, c, first);
+        if (lane == 0) {
+          out_rc[2 * picked] = pr;
+          out_rc[2 * picked + 1] = pc;
+        }
+        ++picked;
+        if (lane <= 2 * R) {
+          const int rr = pr - R + lane;
+          if (rr >= 0 && rr < H) {
+            const int64_t b0 = (int64_t)rr * W + max(pc - R, 0);
+            const int64_t b1 = (int64_t)rr * W + min(pc + R, W - 1);
+            const int w0 = (int)(b0 >> 5), w1 = (int)(b1 >> 5);
+            const unsigned lo = ~0u << (b0 & 31);
+            const unsigned hi = (b1 & 31) == 31 ? ~0u : ((1u << ((b1 & 31) + 1)) - 1u);
+            if (w0 == w1) {
+              atomicOr(&bm[w0], lo & hi);
+            } else {
+              atomicOr(&bm[w0], lo);
+              atomicOr(&bm[w1], hi);
+            }
           }
         }
+        __syncwarp();
+        if (picked >= max_n) break;
+        live = live && lane > first;
       }
-      __syncwarp();
-      if (picked >= max_n) break;
-      live = live && lane > first;
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u) cur[u] = nxt[u];
   }
   if (lane == 0) *out_n = picked;
 }
@@ -665,10 +699,10 @@ extern "C" int glr_corners(const double* resp_d, int H, int W, int max_n, int nm
   uint8_t* blocked = p;
   p = align256(p + n);
   size_t temp_bytes = nms_sort_temp(n);
-  GLR_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned long long), st));
-  GLR_CUDA(cudaMemsetAsync(blocked, 0, n, st));
+  int* n_cand = reinterpret_cast<int*>(mx + 1);
+  GLR_CUDA(cudaMemsetAsync(mx, 0, 2 * sizeof(unsigned long long), st));
   resp_max_kernel<<<grid_for(n), 256, 0, st>>>(resp_d, n, mx);
-  cand_keys_kernel<<<grid_for(n), 256, 0, st>>>(resp_d, n, quality, mx, k_in, v_in);
+  cand_keys_kernel<<<grid_for(n), 256, 0, st>>>(resp_d, n, quality, mx, k_in, v_in, n_cand);
   GLR_CUDA(cudaGetLastError());
   GLR_CUDA(cub::DeviceRadixSort::SortPairsDescending(p, temp_bytes, k_in, k_out, v_in, v_out,
                                                      (int)n, 0, 64, st));
@@ -681,10 +715,11 @@ extern "C" int glr_corners(const double* resp_d, int H, int W, int max_n, int nm
                                     kNmsBitmapMaxBytes));
       attr = true;
     }
-    nms_bitmap_kernel<<<1, 1024, bm_bytes, st>>>(k_out, v_out, n, H, W, max_n, nms_radius,
+    nms_bitmap_kernel<<<1, 1024, bm_bytes, st>>>(v_out, n_cand, H, W, max_n, nms_radius,
                                                  out_rc_d, out_n_d);
     return check_launch("nms_bitmap_kernel");
   }
+  GLR_CUDA(cudaMemsetAsync(blocked, 0, n, st));
   nms_kernel<<<1, 1024, 0, st>>>(k_out, v_out, n, H, W, max_n, nms_radius, blocked, out_rc_d,
                                  out_n_d);
   return check_launch("nms_kernel");

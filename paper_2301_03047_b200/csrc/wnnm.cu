@@ -30,11 +30,11 @@ constexpr int GLD = KMAX + 2;     // row stride of G in the eigen kernel (pair r
 constexpr int VLD = KMAX + 1;     // row stride of V^T in the eigen kernel
 constexpr int GROWS = 32;         // rows of M per Gram tile
 constexpr int GRS = GROWS + 4;    // column stride of the Gram tiles (== 4 mod 16)
-constexpr int AROWS = 32;         // rows of M per apply tile (one 8-row tile row per warp)
+constexpr int AROWS = 64;         // rows of M per apply tile (one 8-row tile row per warp)
 constexpr int ARS = AROWS + 8;    // column stride of the apply tiles (== 8 mod 16)
 constexpr int GRAM_THREADS = 96;  // three warps: super-blocks (0,0), (0,1), (1,1)
 constexpr int EIG_THREADS = 256;
-constexpr int APPLY_THREADS = 128;
+constexpr int APPLY_THREADS = 256;
 constexpr int MAX_SWEEPS = 24;
 constexpr int GSZ = KMAX * KMAX;  // doubles per group in the G / Wm / V buffers
 // Jacobi rotation threshold: skip (p,q) once |g_pq| <= kRotTol sqrt(|g_pp g_qq|).
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// K3: out = M Wm on DMMA over 32-row tiles (column stride ARS = 40 == 8 mod
+// K3: out = M Wm on DMMA over 64-row tiles (column stride ARS = 72 == 8 mod
 // 16 doubles), Wm in shared memory (row stride LD = 68 == 4 mod 16). Warp w
 // owns tile row w (8 rows) x all 8 column tiles: per k-step one A fragment
 // and eight B fragments feed eight DMMAs. The denoised patch entries go to

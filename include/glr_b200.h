@@ -155,12 +155,15 @@ int glr_wnnm_scatter(const double* x_d, int H, int W, int C, int P, const int32_
 /* glr_vcache_remap: carry cached eigenvectors across a matching refresh —
  * new group g in [new_lo, new_hi) whose anchor was old group i in
  * [old_lo, old_hi) gets vc_new[g] = vc_old[i] and flags[g] = 1 (else 0), for
- * warm = 2 in glr_wnnm_scatter. map_d: H*W int32 scratch that must hold -1
- * everywhere on entry (it is restored on exit).                            */
+ * warm = 2 in glr_wnnm_scatter. With old_pos_d / new_pos_d ((n, K, 2) group
+ * positions, both or neither) the eigenvector coordinates are re-indexed so
+ * each kept patch position keeps its coordinate (an orthogonal row
+ * permutation). map_d: H*W int32 scratch that must hold -1 everywhere on
+ * entry (it is restored on exit).                                          */
 int glr_vcache_remap(const int32_t* old_anchors_d, int old_lo, int old_hi,
                      const int32_t* new_anchors_d, int new_lo, int new_hi, int H, int W,
                      const double* vc_old_d, double* vc_new_d, uint8_t* flags_d, int32_t* map_d,
-                     void* stream);
+                     const int32_t* old_pos_d, const int32_t* new_pos_d, int K, void* stream);
 
 /* glr_scatter_count: cnt[r][c] += 1 for every pixel covered by every patch
  * (channel-invariant form of scatter_group's counter, patches.py:70).      */

@@ -60,7 +60,8 @@ SIGNATURES: dict[str, tuple] = {
     "glr_wnnm": (i32, [vp, i32, i32, i32, f64, f64, f64, f64, vp, vp, vp, sz, vp]),
     "glr_wnnm_scatter": (i32, [vp, i32, i32, i32, i32, vp, i32, vp, i32, f64, f64, f64, i32, vp,
                                vp, i32, vp, vp, sz, vp]),
-    "glr_vcache_remap": (i32, [vp, i32, i32, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp]),
+    "glr_vcache_remap": (i32, [vp, i32, i32, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, i32,
+                               vp]),
     "glr_scatter_count": (i32, [vp, i32, vp, i32, i32, i32, i32, vp, vp]),
     "glr_scatter_add_f64": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, vp, vp, vp]),
     "glr_scatter_fixed": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, vp]),

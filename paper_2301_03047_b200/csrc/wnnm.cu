@@ -644,17 +644,78 @@ __global__ void anchor_map_kernel(const int32_t* __restrict__ anchors, int lo, i
     map[anchors[2 * i] * W + anchors[2 * i + 1]] = set ? i : -1;
 }
 
+// With both position lists given, the cached V^T rows are also re-indexed
+// by group column: new column j takes the coordinate of the old column that
+// holds the same patch position (t-th occurrence matched to t-th occurrence),
+// unmatched new columns take the unmatched old coordinates in order. Any
+// such coordinate permutation of an orthogonal V is orthogonal, and a good
+// warm start whenever the refreshed group keeps most of its patches.
 __global__ void vcache_remap_kernel(const int32_t* __restrict__ new_anchors, int lo, int W,
                                     const int32_t* __restrict__ map,
                                     const double* __restrict__ vc_old, double* __restrict__ vc_new,
-                                    uint8_t* __restrict__ flags) {
+                                    uint8_t* __restrict__ flags,
+                                    const int32_t* __restrict__ old_pos,
+                                    const int32_t* __restrict__ new_pos, int K) {
+  __shared__ int perm[wn::KMAX], inv[wn::KMAX], used[wn::KMAX], key_o[wn::KMAX],
+      key_n[wn::KMAX];
   const int g = lo + blockIdx.x;
   const int old = map[new_anchors[2 * g] * W + new_anchors[2 * g + 1]];
-  if (threadIdx.x == 0) flags[g] = old >= 0 ? 1 : 0;
+  const int tid = threadIdx.x;
+  if (tid == 0) flags[g] = old >= 0 ? 1 : 0;
   if (old < 0) return;
-  const double2* src = reinterpret_cast<const double2*>(vc_old + (size_t)old * wn::GSZ);
-  double2* dst = reinterpret_cast<double2*>(vc_new + (size_t)g * wn::GSZ);
-  for (int t = threadIdx.x; t < wn::GSZ / 2; t += blockDim.x) dst[t] = src[t];
+  if (tid < wn::KMAX) {
+    perm[tid] = tid;
+    used[tid] = 0;
+  }
+  if (old_pos && new_pos) {
+    if (tid < K) {
+      const int32_t* op = old_pos + ((size_t)old * K + tid) * 2;
+      const int32_t* np = new_pos + ((size_t)g * K + tid) * 2;
+      key_o[tid] = op[0] * W + op[1];
+      key_n[tid] = np[0] * W + np[1];
+    }
+    __syncthreads();
+    int match = -1;
+    if (tid < K) {
+      const int v = key_n[tid];
+      int t = 0;  // occurrence rank of v among the new columns before tid
+      for (int j = 0; j < tid; ++j) t += key_n[j] == v;
+      for (int i = 0; i < K && match < 0; ++i)
+        if (key_o[i] == v && t-- == 0) match = i;
+      if (match >= 0) used[match] = 1;
+    }
+    __syncthreads();
+    if (tid < K) {
+      if (!used[tid]) {  // rank among the unmatched old coordinates
+        int r = 0;
+        for (int i = 0; i < tid; ++i) r += !used[i];
+        inv[r] = tid;
+      }
+    }
+    __syncthreads();
+    if (tid < K) {
+      if (match < 0) {  // rank among the unmatched new columns
+        int r = 0;
+        for (int j = 0; j < tid; ++j) {
+          const int v = key_n[j];
+          int t = 0, m = -1;
+          for (int q = 0; q < j; ++q) t += key_n[q] == v;
+          for (int i = 0; i < K && m < 0; ++i)
+            if (key_o[i] == v && t-- == 0) m = i;
+          r += m < 0;
+        }
+        match = inv[r];
+      }
+      perm[tid] = match;
+    }
+  }
+  __syncthreads();
+  const double* src = vc_old + (size_t)old * wn::GSZ;
+  double* dst = vc_new + (size_t)g * wn::GSZ;
+  for (int t = tid; t < wn::GSZ; t += blockDim.x) {  // Vt[e][j] = Vt_old[e][perm[j]]
+    const int e = t >> 6, j = t & 63;
+    dst[t] = src[e * wn::KMAX + perm[j]];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -850,7 +911,12 @@ extern "C" int glr_wnnm_scatter(const double* x_d, int H, int W, int C, int P,
 extern "C" int glr_vcache_remap(const int32_t* old_anchors_d, int old_lo, int old_hi,
                                 const int32_t* new_anchors_d, int new_lo, int new_hi, int H,
                                 int W, const double* vc_old_d, double* vc_new_d,
-                                uint8_t* flags_d, int32_t* map_d, void* stream) {
+                                uint8_t* flags_d, int32_t* map_d, const int32_t* old_pos_d,
+                                const int32_t* new_pos_d, int K, void* stream) {
+  GLR_REQUIRE((old_pos_d == nullptr) == (new_pos_d == nullptr), GLR_ERR_INVALID,
+              "vcache_remap: give both position lists or neither");
+  GLR_REQUIRE(old_pos_d == nullptr || (K >= 1 && K <= wn::KMAX), GLR_ERR_INVALID,
+              "vcache_remap: K=%d", K);
   cudaStream_t st = (cudaStream_t)stream;
   if (old_hi > old_lo) {
     anchor_map_kernel<<<blocks_for(old_hi - old_lo), 256, 0, st>>>(old_anchors_d, old_lo, old_hi,
@@ -859,7 +925,8 @@ extern "C" int glr_vcache_remap(const int32_t* old_anchors_d, int old_lo, int ol
   }
   if (new_hi > new_lo) {
     vcache_remap_kernel<<<new_hi - new_lo, 256, 0, st>>>(new_anchors_d, new_lo, W, map_d,
-                                                        vc_old_d, vc_new_d, flags_d);
+                                                        vc_old_d, vc_new_d, flags_d, old_pos_d,
+                                                        new_pos_d, K);
     GLR_CUDA(cudaGetLastError());
   }
   if (old_hi > old_lo) {

@@ -169,7 +169,11 @@ class GlrEngine:
         self.anchors = D.empty((self.max_anchors, 2), t.int32)
         self.tags = D.empty((self.max_anchors,), t.uint8)
         self.n_anchors = D.zeros((1,), t.int32)
-        self.positions = D.empty((self.max_anchors, self.k, 2), t.int32)
+        # match positions, double-buffered so a refresh can re-index the cached
+        # eigenvectors of groups that keep their anchor (glr_vcache_remap)
+        self._pos = [D.empty((self.max_anchors, self.k, 2), t.int32) for _ in range(2)]
+        self._pcur = 0
+        self.positions = self._pos[0]
         self.padded = D.empty((self.max_anchors,), t.int32)
         self.acc = D.zeros((h, w, c), t.int64)
         self.cnt = D.zeros((h, w), t.int32)
@@ -243,16 +247,11 @@ class GlrEngine:
         self.lo, self.hi = shard_bounds(n, self.rank, self.world)
         self.has_positions = True
         self.warm = 0
-        if n and old_n and self.vcache_valid:
-            # groups keeping their anchor start from their old eigenvectors
-            vc_old = self._vc[self._vcur]
-            self._vcur ^= 1
-            N.call("glr_vcache_remap", old_anchors.data_ptr(), old_lo, old_hi,
-                   self.anchors.data_ptr(), self.lo, self.hi, h, w, vc_old.data_ptr(),
-                   self.vcache.data_ptr(), self.warm_flags.data_ptr(),
-                   self.anchor_map.data_ptr(), s)
-            self.warm = 2
+        carry = bool(n and old_n and self.vcache_valid)
         self.vcache_valid = False
+        old_positions = self.positions
+        self._pcur ^= 1
+        self.positions = self._pos[self._pcur]
         if n == 0:
             return 0
         e = self._ev()
@@ -262,6 +261,17 @@ class GlrEngine:
                self.ws_edge.data_ptr(), s)
         self._log(("edge_stack", 1), e)
         self.match_shard()
+        if carry:
+            # groups keeping their anchor start from their old eigenvectors,
+            # coordinates re-indexed to the refreshed positions
+            vc_old = self._vc[self._vcur]
+            self._vcur ^= 1
+            N.call("glr_vcache_remap", old_anchors.data_ptr(), old_lo, old_hi,
+                   self.anchors.data_ptr(), self.lo, self.hi, h, w, vc_old.data_ptr(),
+                   self.vcache.data_ptr(), self.warm_flags.data_ptr(),
+                   self.anchor_map.data_ptr(), old_positions.data_ptr(),
+                   self.positions.data_ptr(), self.k, s)
+            self.warm = 2
         self.count()
         return n
 

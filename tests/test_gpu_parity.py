@@ -262,3 +262,50 @@ def test_gap_solve_interp_init_vs_reference_run():
         assert np.array_equal(np.array(pos, dtype=np.int32), g[f"solve_positions_{j}"]), j
     assert np.abs(x - g["solve_out"]).max() <= 1e-6
     assert abs(rep.rows[-1]["psnr_db"] - float(g["solve_psnr"][-1])) <= 0.05
+
+
+def test_vcache_remap_reindexes_kept_positions(rng):
+    """glr_vcache_remap: a group keeping its anchor gets its cached V^T with the
+    coordinates permuted so every kept patch position keeps its coordinate
+    (t-th occurrence to t-th occurrence), the rest in order: an orthogonal
+    row permutation of V."""
+    import torch
+    from paper_2301_03047_b200 import _device as D, _native as N
+    H, W, K = 40, 50, 12
+    old_anc = np.array([[3, 4], [10, 20], [30, 5]], np.int32)
+    new_anc = np.array([[10, 20], [7, 7], [3, 4]], np.int32)
+    old_pos = rng.integers(0, 30, (3, K, 2)).astype(np.int32)
+    old_pos[0, 5] = old_pos[0, 2]                      # a duplicated position
+    new_pos = rng.integers(0, 30, (3, K, 2)).astype(np.int32)
+    new_pos[0, [0, 3, 7]] = old_pos[1, [4, 0, 9]]      # kept by the second old group
+    new_pos[2, [1, 2, 6]] = old_pos[0, [2, 5, 11]]     # includes the duplicate twice
+    vc_old = np.zeros((3, 64, 64))
+    for g in range(3):
+        q, _ = np.linalg.qr(rng.standard_normal((64, 64)))
+        vc_old[g] = q
+    vo, vn = D.f64(vc_old), D.f64(np.zeros_like(vc_old))
+    flags = D.zeros((3,), torch.uint8)
+    amap = D.empty((H * W,), torch.int32).fill_(-1)
+    oa, na, op, npd = D.i32(old_anc), D.i32(new_anc), D.i32(old_pos), D.i32(new_pos)
+    N.call("glr_vcache_remap", oa.data_ptr(), 0, 3, na.data_ptr(), 0, 3, H, W, vo.data_ptr(),
+           vn.data_ptr(), flags.data_ptr(), amap.data_ptr(), op.data_ptr(), npd.data_ptr(), K,
+           D.stream())
+    got, fl = D.host(vn), D.host(flags)
+    assert fl.tolist() == [1, 0, 1]
+    assert (D.host(amap) == -1).all()
+    for g_new, g_old in ((0, 1), (2, 0)):
+        perm = []
+        for j in range(64):
+            hits = [i for i in range(64) if np.array_equal(got[g_new][:, j], vc_old[g_old][:, i])]
+            assert len(hits) == 1
+            perm.append(hits[0])
+        assert sorted(perm) == list(range(64)) and perm[K:] == list(range(K, 64))
+        key = lambda p: (int(p[0]), int(p[1]))  # noqa: E731
+        seen = {}
+        for j in range(K):
+            v = key(new_pos[g_new, j])
+            t = seen.get(v, 0)
+            seen[v] = t + 1
+            occ = [i for i in range(K) if key(old_pos[g_old, i]) == v]
+            if t < len(occ):
+                assert perm[j] == occ[t], (g_new, j)

@@ -113,6 +113,20 @@ int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, int expand,
                  const int32_t* anchors_d, int n_max, const int32_t* n_dev_d, uint16_t* heat_d,
                  void* ws_d, size_t ws_bytes, void* stream);
 
+/* glr_heat_topk: heat map + top-K fused (matching.py:140-231) without
+ * materialising the heat map: the GEMM epilogue appends, per exemplar n, every
+ * position whose score reaches |E_n|/4 (a quarter of the exemplar's
+ * self-score, the row maximum) to a list of capacity `cap`; the exact top-K
+ * (same semantics as glr_topk) then runs on the lists. An exemplar whose cut
+ * falls below that floor, whose list overflows, or with more than 4096 ties
+ * at the cut gets fallback_d[n] = 1 and untouched positions/padded: the
+ * caller runs glr_heat_map + glr_topk for it. ws: glr_heat_topk_workspace.  */
+size_t glr_heat_topk_workspace(int C, int P, int n_max, int cap);
+int glr_heat_topk(const uint8_t* stack_d, int H, int W, int C, int P, int expand,
+                  const int32_t* anchors_d, int n_max, int K, int sep, int cap,
+                  int32_t* positions_d, int32_t* padded_d, uint8_t* fallback_d, void* ws_d,
+                  size_t ws_bytes, void* stream);
+
 /* ---- (3) top-K selection: glr/matching.py:170-231 ---------------------------
  * Exact tie-ordered greedy selection per exemplar: slot 0 = anchor, then
  * (score desc, flat index asc) skipping Chebyshev <= sep of any chosen,

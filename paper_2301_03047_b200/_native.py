@@ -54,6 +54,9 @@ SIGNATURES: dict[str, tuple] = {
     "glr_heat_workspace": (sz, [i32, i32, i32]),
     "glr_heat_map": (i32, [vp, i32, i32, i32, i32, i32, vp, i32, vp, vp, vp, sz, vp]),
     "glr_topk_workspace": (sz, [i32, i32, i32]),
+    "glr_heat_topk_workspace": (sz, [i32, i32, i32, i32]),
+    "glr_heat_topk": (i32, [vp, i32, i32, i32, i32, i32, vp, i32, i32, i32, i32, vp, vp, vp, vp, sz,
+                            vp]),
     "glr_topk": (i32, [vp, i32, vp, i32, i32, i32, vp, i32, i32, vp, vp, vp, sz, vp]),
     "glr_gather": (i32, [vp, i32, i32, i32, i32, vp, i32, i32, vp, vp]),
     "glr_wnnm_workspace": (sz, [i32, i32]),
@@ -140,7 +143,7 @@ KERNELS_PER_CALL = {
     "glr_scatter_add_f64": 1, "glr_normalize": 1, "glr_masksum_forward": 1,
     "glr_masksum_adjoint": 1, "glr_gap_masksum": 2, "glr_fourier_forward": 4,
     "glr_fourier_adjoint": 4, "glr_gap_fourier": 11, "glr_sq_err": 2, "glr_vcache_remap": 3,
-    "glr_lincomb": 1, "glr_interp_msfa": 3, "glr_interp_cacti": 1,
+    "glr_lincomb": 1, "glr_interp_msfa": 3, "glr_interp_cacti": 1, "glr_heat_topk": 4,
 }
 launch_count = 0
 

@@ -45,20 +45,22 @@
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
+#include "internal.cuh"
 
 namespace glr {
 
 namespace heat {
-constexpr int BM = 128;      // positions per tile (UMMA M)
-constexpr int BN = 224;      // exemplars per tile (UMMA N)
+constexpr int BM = 128;      // positions per CTA tile (the pair's UMMA M = 256)
+constexpr int BN = 224;      // exemplars per pair tile (UMMA N)
+constexpr int BNH = BN / 2;  // exemplar rows of B held by each CTA of the pair
 constexpr int BK = 128;      // bytes of K per stage (one 128B swizzle row = 256 fp4)
 constexpr int UK = 32;       // bytes of K per tcgen05.mma kind::mxf4 (64 fp4)
-constexpr int STAGES = 5;
-constexpr int CL = 2;        // CTAs per cluster sharing one exemplar tile (multicast)
+constexpr int STAGES = 7;
 constexpr int ACC = 2;       // TMEM accumulators (2 x 224 columns)
-constexpr int THREADS = 256;
+constexpr int THREADS = 384;  // warps 4-11: epilogue (lane quadrant w%4, column half)
+constexpr int EPI_WARPS = 8;
 constexpr int A_BYTES = BM * BK;
-constexpr int B_BYTES = BN * BK;
+constexpr int B_BYTES = BNH * BK;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr uint32_t TMEM_COLS = 512;
@@ -92,6 +94,12 @@ struct HeatParams {
   int oh, ow, Mpad, n_max, m_tiles_per_row, S, kchunks, e;
   const int32_t* n_dev;
   uint16_t* heat;
+  // candidate mode (cand != nullptr): instead of the dense u16 map, append
+  // (score << 32) | position for every score >= thr[n] to cand[n][0 .. cap)
+  const uint16_t* thr;
+  uint32_t* cnt;
+  uint64_t* cand;
+  int cap;
 };
 
 __global__ void __launch_bounds__(heat::THREADS, 1)
@@ -111,23 +119,23 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
 
   const int N = p.n_dev ? min(*p.n_dev, p.n_max) : p.n_max;
   const int n_tiles = (N + BN - 1) / BN;
-  // tile pairs (two m tiles, one n tile), n fastest: clusters share A tiles in L2
-  const int total = p.oh * (p.m_tiles_per_row / CL) * n_tiles;
+  // pair tiles (two m tiles, one n tile), n fastest: pairs share A tiles in L2
+  const int total = p.oh * (p.m_tiles_per_row / 2) * n_tiles;
   const int num_k = p.S * p.kchunks;
   const int rank = (int)cluster_ctarank();
-  const int cl = blockIdx.x / CL, n_cl = gridDim.x / CL;
-  constexpr uint16_t kAll = (1u << CL) - 1;
+  const bool leader = rank == 0;
+  const int cl = blockIdx.x >> 1, n_cl = gridDim.x >> 1;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL);  // every CTA's MMA commit
+      mbar_init(&full[s], 1);   // leader: its expect_tx; both CTAs' TMA bytes land here
+      mbar_init(&empty[s], 1);  // the leader's MMA commit (multicast to both CTAs)
     }
     for (int a = 0; a < ACC; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+      mbar_init(&tfull[a], 1);   // the leader's MMA commit (multicast)
+      mbar_init(&tempty[a], 2 * EPI_WARPS);  // leader: one arrive per epilogue warp, both CTAs
     }
     fence_barrier_init();
   }
@@ -135,13 +143,13 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
   }
-  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  if (warp == 2) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
-  cluster_sync();  // peers' barriers initialised before any multicast lands
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (warp >= 4) {
+  if (warp >= 4 && warp < 8) {
     // every scale-factor byte = UE8M0 127 = 2^0, whatever the layout the MMA reads
     uint32_t ones[32];
 #pragma unroll
@@ -153,38 +161,39 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync();  // both CTAs' scale factors written before the leader's first MMA
   tc_fence_after();
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---- TMA producer ----
+      // ---- TMA producer (both CTAs): own A tile + own half of the B tile ----
       int it = 0;
       for (int t = cl; t < total; t += n_cl) {
         const int n0 = (t % n_tiles) * BN;
-        const int m_tile = CL * (t / n_tiles) + rank;
+        const int m_tile = 2 * (t / n_tiles) + rank;
         const int u = m_tile / p.m_tiles_per_row;
         const int v0 = (m_tile % p.m_tiles_per_row) * BM;
         for (int kb = 0; kb < num_k; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           if (it >= STAGES) mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+          if (leader) mbar_arrive_expect_tx(&full[s], 2 * STAGE_BYTES);
+          const uint32_t fb = cluster_addr(&full[s], 0);
           const int slab = kb / p.kchunks;
           const int kc = kb - slab * p.kchunks;
-          tma_load_3d(sA + s * A_BYTES, &tmA, &full[s], kc * BK, v0, u + slab * p.e);
-          tma_load_2d_mc(sB + s * B_BYTES + rank * (B_BYTES / CL), &tmB, &full[s], kb * BK,
-                         n0 + rank * (BN / CL), kAll);
+          tma_load_3d_pair(sA + s * A_BYTES, &tmA, fb, kc * BK, v0, u + slab * p.e);
+          tma_load_2d_pair(sB + s * B_BYTES, &tmB, fb, kb * BK, n0 + rank * BNH);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---- MMA issuer ----
-      constexpr uint32_t idesc = idesc_mxf4(BM, BN);
+    if (lane == 0 && leader) {
+      // ---- MMA issuer (pair leader): 256 x 224 x 64 fp4 per instruction ----
+      constexpr uint32_t idesc = idesc_mxf4(2 * BM, BN);
       int it = 0, lt = 0;
       for (int t = cl; t < total; t += n_cl, ++lt) {
         const int acc = lt & 1, use = lt >> 1;
-        if (use > 0) mbar_wait(&tempty[acc], (use - 1) & 1);  // epilogue drained it
+        if (use > 0) mbar_wait_cluster(&tempty[acc], (use - 1) & 1);  // both epilogues drained it
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(acc * BN);
         for (int kb = 0; kb < num_k; ++kb, ++it) {
@@ -196,21 +205,23 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
           const uint64_t bd = smem_desc_k_sw128(sB + s * B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / UK; ++k)  // +32 bytes inside the 128B swizzle atom
-            umma_mxf4(d, ad + (uint64_t)((k * UK) >> 4), bd + (uint64_t)((k * UK) >> 4), idesc,
-                      (kb | k) != 0, tmem + SFA_COL, tmem + SFB_COL);
-          umma_commit_mc(&empty[s], kAll);  // frees stage s in every CTA
+            umma_mxf4_pair(d, ad + (uint64_t)((k * UK) >> 4), bd + (uint64_t)((k * UK) >> 4),
+                           idesc, (kb | k) != 0, tmem + SFA_COL, tmem + SFB_COL);
+          umma_commit_pair_mc(&empty[s], 0x3);  // frees stage s in both CTAs
         }
-        umma_commit(&tfull[acc]);
+        umma_commit_pair_mc(&tfull[acc], 0x3);
       }
     }
   } else if (warp >= 4) {
-    // ---- epilogue: TMEM -> registers -> u16 exemplar-major rows ----
-    const int ew = warp - 4;  // TMEM lanes 32*ew .. 32*ew+31 (warp id % 4)
+    // ---- epilogue (both CTAs): own 128 TMEM lanes -> u16 exemplar-major rows ----
+    const int ew = warp & 3;           // TMEM lanes 32*ew .. 32*ew+31 (warp id % 4)
+    const int ch = (warp - 4) >> 2;    // column half: chunks ch*4 .. (BN/32 chunks total)
+    const uint32_t te_leader[ACC] = {cluster_addr(&tempty[0], 0), cluster_addr(&tempty[1], 0)};
     int lt = 0;
     for (int t = cl; t < total; t += n_cl, ++lt) {
       const int acc = lt & 1, use = lt >> 1;
       const int n0 = (t % n_tiles) * BN;
-      const int m_tile = CL * (t / n_tiles) + rank;
+      const int m_tile = 2 * (t / n_tiles) + rank;
       const int u = m_tile / p.m_tiles_per_row;
       const int v = (m_tile % p.m_tiles_per_row) * BM + ew * 32 + lane;
       mbar_wait(&tfull[acc], use & 1);
@@ -218,11 +229,34 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
       const bool v_ok = v < p.ow;
       uint16_t* out = p.heat + (size_t)u * p.ow + v;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = ch * 4; c < min(ch * 4 + 4, BN / 32); ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * BN + c * 32), r);
         tmem_ld_wait();
         const int nb = n0 + c * 32;
+        if (p.cand) {
+          // candidate lists: warp-aggregated appends per exemplar column
+          const int tl = nb + lane < N ? (int)p.thr[nb + lane] : 0x10000;
+          const uint32_t pos = (uint32_t)(u * p.ow + v);
+          const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int sc = (int)__float2uint_rn(__uint_as_float(r[j]));
+            const int tj = __shfl_sync(0xffffffffu, tl, j);  // all lanes (no short-circuit)
+            const bool hit = v_ok && sc >= tj;
+            const unsigned m = __ballot_sync(0xffffffffu, hit);
+            if (m) {
+              const int n = nb + j;
+              const int ld = __ffs(m) - 1;
+              uint32_t base = 0;
+              if (lane == ld) base = atomicAdd(&p.cnt[n], (uint32_t)__popc(m));
+              base = __shfl_sync(0xffffffffu, base, ld) + __popc(m & lt);
+              if (hit && base < (uint32_t)p.cap)
+                p.cand[(size_t)n * p.cap + base] = ((uint64_t)sc << 32) | pos;
+            }
+          }
+          continue;
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int n = nb + j;
@@ -231,14 +265,14 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) mbar_arrive_cluster(te_leader[acc]);
     }
   }
   __syncwarp();
   tc_fence_before();
   __syncthreads();
-  cluster_sync();  // no CTA leaves while its peer may still multicast into it
-  if (warp == 2) tmem_dealloc<TMEM_COLS>(tmem);
+  cluster_sync();  // no CTA leaves while its peer may still use its smem / TMEM
+  if (warp == 2) tmem_dealloc_pair<TMEM_COLS>(tmem);
 }
 
 // B operand (bytes): bmat[n][s*kchunks*BK + k'] = stack[r_n + s*e][c_n + k'/Cb][k' % Cb]
@@ -268,6 +302,23 @@ __global__ void exemplar_pack_kernel(const uint8_t* __restrict__ stack, HeatGeom
     }
     bmat[i] = val;
   }
+}
+
+// thr[n] = |E_n| / 4: a quarter of the exemplar's self-score (the number of
+// 1.0 nibbles of its packed operand row = the maximum of its heat row)
+__global__ void exemplar_thr_kernel(const uint8_t* __restrict__ bmat, int Kp, int n_max,
+                                    uint16_t* __restrict__ thr) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= n_max) return;
+  const uint32_t* row = reinterpret_cast<const uint32_t*>(bmat + (size_t)w * Kp);
+  int cnt = 0;
+  for (int i = lane; i < Kp / 4; i += 32) {
+    const uint32_t v = row[i];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) cnt += ((v >> (4 * k)) & 0xFu) == kFp4One;
+  }
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0) thr[w] = (uint16_t)(cnt >> 2);
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
@@ -316,32 +367,27 @@ extern "C" size_t glr_heat_workspace(int C, int P, int n_max) {
   return n_pad * (size_t)g.Kp + 256;
 }
 
-extern "C" int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, int expand,
-                            const int32_t* anchors_d, int n_max, const int32_t* n_dev_d,
-                            uint16_t* heat_d, void* ws_d, size_t ws_bytes, void* stream) {
-  GLR_REQUIRE(P >= 1 && P <= H && P <= W && C >= 1, GLR_ERR_INVALID,
-              "heat_map: bad shape H=%d W=%d C=%d P=%d", H, W, C, P);
-  GLR_REQUIRE(expand >= 1 && expand <= (P > 8 ? P : 8) && (4 * C * expand) % 32 == 0,
-              GLR_ERR_INVALID,
-              "heat_map: expand factor %d invalid for C=%d", expand, C);
-  if (n_max <= 0) return GLR_OK;
-  HeatGeom g = heat_geom(H, W, C, P, expand);
-  GLR_REQUIRE(4 * C * P * P <= 65535, GLR_ERR_UNSUPPORTED,
-              "heat_map: max score %d does not fit u16", 4 * C * P * P);
+// pack B (+ thresholds in candidate mode) and launch the GEMM; shared by
+// glr_heat_map (dense map) and glr_heat_topk (candidate lists)
+static int run_heat(const uint8_t* stack_d, int H, int W, int P, const HeatGeom& g,
+                    const int32_t* anchors_d, int n_max, const int32_t* n_dev_d,
+                    uint16_t* heat_d, uint8_t* bmat, uint16_t* thr_d, uint32_t* cnt_d,
+                    uint64_t* cand_d, int cap, cudaStream_t st) {
   const int n_pad = (int)cdiv(n_max, heat::BN) * heat::BN;
-  GLR_REQUIRE(ws_bytes >= (size_t)n_pad * g.Kp, GLR_ERR_WORKSPACE,
-              "heat_map: workspace %zu < %zu", ws_bytes, (size_t)n_pad * g.Kp);
   auto encode = get_encode_fn();
   GLR_REQUIRE(encode != nullptr, GLR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  uint8_t* bmat = reinterpret_cast<uint8_t*>(ws_d);
-
   {
     int64_t total = (int64_t)n_pad * g.Kp;
     int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
     exemplar_pack_kernel<<<blocks, 256, 0, st>>>(stack_d, g, anchors_d, n_max, n_dev_d, n_pad,
                                                  bmat);
     GLR_CUDA(cudaGetLastError());
+  }
+  if (cand_d) {
+    exemplar_thr_kernel<<<(unsigned)cdiv((int64_t)n_max * 32, 256), 256, 0, st>>>(bmat, g.Kp,
+                                                                                  n_max, thr_d);
+    GLR_CUDA(cudaGetLastError());
+    GLR_CUDA(cudaMemsetAsync(cnt_d, 0, (size_t)n_max * sizeof(uint32_t), st));
   }
 
   CUtensorMap tmA, tmB;
@@ -358,7 +404,7 @@ extern "C" int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, 
   {
     cuuint64_t dims[2] = {(cuuint64_t)g.Kp, (cuuint64_t)n_pad};
     cuuint64_t strides[1] = {(cuuint64_t)g.Kp};
-    cuuint32_t box[2] = {heat::BK, heat::BN / heat::CL};  // each CTA loads its slice
+    cuuint32_t box[2] = {heat::BK, heat::BNH};  // each CTA of a pair loads its half
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode(&tmB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)bmat, dims, strides, box,
                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -371,19 +417,23 @@ extern "C" int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, 
   hp.ow = g.ow;
   hp.Mpad = (int)glr_heat_stride(H, W, P);
   hp.n_max = n_max;
-  hp.m_tiles_per_row = (int)cdiv(g.ow, heat::CL * heat::BM) * heat::CL;  // tiles go in clusters
+  hp.m_tiles_per_row = (int)cdiv(g.ow, 2 * heat::BM) * 2;  // even: tiles go in pairs
   hp.S = g.S;
   hp.kchunks = g.kchunks;
   hp.e = g.e;
   hp.n_dev = n_dev_d;
   hp.heat = heat_d;
+  hp.thr = thr_d;
+  hp.cnt = cnt_d;
+  hp.cand = cand_d;
+  hp.cap = cap;
   static bool attr_set = false;
   if (!attr_set) {
     GLR_CUDA(cudaFuncSetAttribute(heat_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   heat::SMEM_BYTES));
     attr_set = true;
   }
-  const int64_t pairs = (int64_t)g.oh * (hp.m_tiles_per_row / heat::CL) * (n_pad / heat::BN);
+  const int64_t pairs = (int64_t)g.oh * (hp.m_tiles_per_row / 2) * (n_pad / heat::BN);
   GLR_REQUIRE(pairs < (1ll << 31), GLR_ERR_UNSUPPORTED, "heat_map: too many tiles");
   int sms = kNumSMs;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -393,7 +443,7 @@ extern "C" int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, 
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = heat::CL;
+  attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -402,13 +452,84 @@ extern "C" int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, 
   // be co-resident (the GPCs need not split into pairs evenly)
   static int max_clusters = 0;
   if (max_clusters == 0) {
-    cfg.gridDim = dim3(heat::CL * (sms / heat::CL));
+    cfg.gridDim = dim3(2 * (sms / 2));
     if (cudaOccupancyMaxActiveClusters(&max_clusters, heat_gemm_kernel, &cfg) != cudaSuccess ||
         max_clusters < 1)
-      max_clusters = sms / heat::CL;
+      max_clusters = sms / 2;
     cudaGetLastError();
   }
-  cfg.gridDim = dim3(heat::CL * (unsigned)std::min<int64_t>(pairs, max_clusters));
+  cfg.gridDim = dim3(2 * (unsigned)std::min<int64_t>(pairs, max_clusters));
   GLR_CUDA(cudaLaunchKernelEx(&cfg, heat_gemm_kernel, tmA, tmB, hp));
   return GLR_OK;
+}
+
+extern "C" int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, int expand,
+                            const int32_t* anchors_d, int n_max, const int32_t* n_dev_d,
+                            uint16_t* heat_d, void* ws_d, size_t ws_bytes, void* stream) {
+  GLR_REQUIRE(P >= 1 && P <= H && P <= W && C >= 1, GLR_ERR_INVALID,
+              "heat_map: bad shape H=%d W=%d C=%d P=%d", H, W, C, P);
+  GLR_REQUIRE(expand >= 1 && expand <= (P > 8 ? P : 8) && (4 * C * expand) % 32 == 0,
+              GLR_ERR_INVALID,
+              "heat_map: expand factor %d invalid for C=%d", expand, C);
+  if (n_max <= 0) return GLR_OK;
+  HeatGeom g = heat_geom(H, W, C, P, expand);
+  GLR_REQUIRE(4 * C * P * P <= 65535, GLR_ERR_UNSUPPORTED,
+              "heat_map: max score %d does not fit u16", 4 * C * P * P);
+  const int n_pad = (int)cdiv(n_max, heat::BN) * heat::BN;
+  GLR_REQUIRE(ws_bytes >= (size_t)n_pad * g.Kp, GLR_ERR_WORKSPACE,
+              "heat_map: workspace %zu < %zu", ws_bytes, (size_t)n_pad * g.Kp);
+  return run_heat(stack_d, H, W, P, g, anchors_d, n_max, n_dev_d, heat_d,
+                  reinterpret_cast<uint8_t*>(ws_d), nullptr, nullptr, nullptr, 0,
+                  reinterpret_cast<cudaStream_t>(stream));
+}
+
+// workspace of glr_heat_topk: packed B | thresholds | counts | candidate lists
+static size_t heat_topk_layout(int C, int P, int n_max, int cap, size_t off[4]) {
+  int e = glr_heat_expand_factor(C, P);
+  HeatGeom g = heat_geom(P, P, C, P, e < 1 ? 1 : e);
+  const size_t n_pad = (size_t)cdiv(std::max(n_max, 1), heat::BN) * heat::BN;
+  auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+  off[0] = 0;
+  off[1] = al(off[0] + n_pad * (size_t)g.Kp);
+  off[2] = al(off[1] + n_pad * sizeof(uint16_t));
+  off[3] = al(off[2] + n_pad * sizeof(uint32_t));
+  return off[3] + (size_t)std::max(n_max, 1) * cap * sizeof(uint64_t) + 256;
+}
+
+extern "C" size_t glr_heat_topk_workspace(int C, int P, int n_max, int cap) {
+  size_t off[4];
+  return heat_topk_layout(C, P, n_max, cap, off);
+}
+
+extern "C" int glr_heat_topk(const uint8_t* stack_d, int H, int W, int C, int P, int expand,
+                             const int32_t* anchors_d, int n_max, int K, int sep, int cap,
+                             int32_t* positions_d, int32_t* padded_d, uint8_t* fallback_d,
+                             void* ws_d, size_t ws_bytes, void* stream) {
+  GLR_REQUIRE(P >= 1 && P <= H && P <= W && C >= 1, GLR_ERR_INVALID,
+              "heat_topk: bad shape H=%d W=%d C=%d P=%d", H, W, C, P);
+  GLR_REQUIRE(expand >= 1 && expand <= (P > 8 ? P : 8) && (4 * C * expand) % 32 == 0,
+              GLR_ERR_INVALID, "heat_topk: expand factor %d invalid for C=%d", expand, C);
+  GLR_REQUIRE(cap >= 1, GLR_ERR_INVALID, "heat_topk: cap %d", cap);
+  if (n_max <= 0) return GLR_OK;
+  HeatGeom g = heat_geom(H, W, C, P, expand);
+  GLR_REQUIRE(4 * C * P * P <= 65535, GLR_ERR_UNSUPPORTED,
+              "heat_topk: max score %d does not fit u16", 4 * C * P * P);
+  size_t off[4];
+  const size_t need = heat_topk_layout(C, P, n_max, cap, off);
+  GLR_REQUIRE(ws_bytes >= need, GLR_ERR_WORKSPACE, "heat_topk: workspace %zu < %zu", ws_bytes,
+              need);
+  uint8_t* base = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(ws_d) + 255) & ~uintptr_t(255));
+  GLR_REQUIRE(ws_bytes - (size_t)(base - reinterpret_cast<uint8_t*>(ws_d)) >= need - 256,
+              GLR_ERR_WORKSPACE, "heat_topk: workspace alignment");
+  uint8_t* bmat = base + off[0];
+  uint16_t* thr = reinterpret_cast<uint16_t*>(base + off[1]);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(base + off[2]);
+  uint64_t* cand = reinterpret_cast<uint64_t*>(base + off[3]);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int r = run_heat(stack_d, H, W, P, g, anchors_d, n_max, nullptr, nullptr, bmat, thr, cnt,
+                         cand, cap, st);
+  if (r != GLR_OK) return r;
+  return topk_cand_launch(cand, cnt, thr, cap, n_max, g.oh, g.ow, 4 * C * P * P, anchors_d, K,
+                          sep, positions_d, padded_d, fallback_d, stream);
 }

@@ -23,6 +23,7 @@
 //      their candidate against the chosen set in parallel, then accepted
 //      candidates are committed in lane order with an in-warp re-check.
 #include "common.cuh"
+#include "internal.cuh"
 
 namespace glr {
 
@@ -31,6 +32,10 @@ constexpr int THREADS = 512;
 constexpr int VEC = 8;  // u16 scores per 16-byte load
 constexpr int MAX_BINS = 12288;
 }  // namespace topk
+
+#ifdef GLR_TOPK_STATS
+__device__ unsigned int g_topk_stats[4];  // rows, fallbacks below L, sum / max of count(>= L)
+#endif
 
 struct TopkParams {
   const uint16_t* heat;
@@ -51,216 +56,13 @@ __device__ __forceinline__ int cheb(int r0, int c0, int r1, int c1) {
   return max(abs(r0 - r1), abs(c0 - c1));
 }
 
-__global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
+// Steps 4-5, shared by both top-K kernels: bitonic sort of A (score desc,
+// index asc), then the greedy walk over the first `need` entries of A ++ B.
+__device__ __forceinline__ void topk_finish(const TopkParams& p, int n, int64_t M, int need,
+                                            int cntA, uint64_t* sA, const int32_t* sB,
+                                            int32_t* chosen) {
   using namespace topk;
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint64_t* sA = reinterpret_cast<uint64_t*>(smem);                   // a_cap
-  int32_t* sB = reinterpret_cast<int32_t*>(sA + p.a_cap);              // b_cap
-  int32_t* hist = sB + p.b_cap;                                        // bins
-  int32_t* chosen = hist + p.bins;                                     // 2*K
-  __shared__ int warp_tot[32];
-  __shared__ int s_total, s_T, s_cntA, s_baseA, s_baseB, s_na, s_nb, s_found;
-  const int BCAP = p.b_cap;
-
-  const int n = blockIdx.x;
-  const int N = p.n_dev ? min(*p.n_dev, p.n_max) : p.n_max;
-  if (n >= N) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint16_t* row = p.heat + (size_t)n * p.stride;
-  const int64_t M = p.M;
-  const int need = (int)(M < (int64_t)p.pool ? M : (int64_t)p.pool);
-
-  // 1. histogram of the scores >= L, L = a quarter of the anchor's own score
-  //    (for a heat map the row maximum: |E_u ∩ E_n| <= |E_n|), so the bulk of
-  //    low scores costs no shared-memory atomics. If fewer than `need`
-  //    positions reach L (or the row is not a heat map), a second pass adds
-  //    the bins below L -- the cut is exact either way.
-  const int64_t aidx = (int64_t)p.anchors[2 * n] * p.ow + p.anchors[2 * n + 1];
-  const int L = min((int)row[aidx] >> 2, p.bins - 1);
-  for (int b = L + tid; b < p.bins; b += THREADS) hist[b] = 0;
-  if (tid == 0) {
-    s_na = 0;
-    s_nb = 0;
-  }
-  __syncthreads();
-  auto hist_pass = [&](int lo, int hi) {  // add the scores in [lo, hi)
-    constexpr int U = 4;  // 16-byte loads in flight per thread
-    for (int64_t tile = 0; tile < M; tile += (int64_t)THREADS * VEC * U) {
-      uint4 v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t base = tile + ((int64_t)u * THREADS + tid) * VEC;
-        v[u] = base < M ? *reinterpret_cast<const uint4*>(row + base) : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t base = tile + ((int64_t)u * THREADS + tid) * VEC;
-        const uint16_t* sv = reinterpret_cast<const uint16_t*>(&v[u]);
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) {
-          const int val = min((int)sv[j], p.bins - 1);
-          if (base + j < M && val >= lo && val < hi) atomicAdd(&hist[val], 1);
-        }
-      }
-    }
-  };
-  hist_pass(L, p.bins);
-  __syncthreads();
-
-  // 2. cut score T: walk bins from the top down to `lo`, 32 at a time
-  auto cut_search = [&](int lo) {
-    int running = 0;
-    int T = 0, cntA = 0;
-    bool found = false;
-    for (int top = p.bins - 1; top >= lo && !found; top -= 32) {
-      const int b = top - lane;
-      const int c = b >= lo ? hist[b] : 0;
-      int incl = c;  // inclusive prefix from the top (lane 0 = highest bin)
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const unsigned hit = __ballot_sync(0xffffffffu, b >= lo && running + incl >= need);
-      if (hit) {
-        const int l = __ffs(hit) - 1;
-        T = top - l;
-        cntA = running + __shfl_sync(0xffffffffu, incl - c, l);
-        found = true;
-      }
-      running += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (lane == 0) {
-      s_T = T;
-      s_cntA = cntA;
-      s_found = found ? 1 : 0;
-    }
-  };
-  if (warp == 0) cut_search(L);
-  __syncthreads();
-  if (!s_found) {
-    for (int b = tid; b < L; b += THREADS) hist[b] = 0;
-    __syncthreads();
-    hist_pass(0, L);
-    __syncthreads();
-    if (warp == 0) cut_search(0);
-    __syncthreads();
-  }
-  const int T = s_T, cntA = s_cntA, capB = need - cntA;
-
-  // 3. collect A = {score > T} (cntA < need entries) and the ties {score == T};
-  //    unordered warp-aggregated appends when the ties fit the buffer (they are
-  //    then sorted by index), else an ordered block-scan compaction.
-  if (hist[T] <= BCAP) {
-    constexpr int U = 4;  // 16-byte loads in flight per thread
-    const unsigned lt = (1u << lane) - 1u;
-    for (int64_t tile = 0; tile < M; tile += (int64_t)THREADS * VEC * U) {
-      uint4 v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t base = tile + ((int64_t)u * THREADS + tid) * VEC;
-        v[u] = base < M ? *reinterpret_cast<const uint4*>(row + base) : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t base = tile + ((int64_t)u * THREADS + tid) * VEC;
-        const uint16_t* sv = reinterpret_cast<const uint16_t*>(&v[u]);
-        // warp-uniform skip of chunks holding no candidate (the common case)
-        bool any = false;
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) any |= base + j < M && sv[j] >= T;
-        if (!__any_sync(0xffffffffu, any)) continue;
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) {
-          const bool ok = base + j < M;
-          const bool isA = ok && sv[j] > T, isB = ok && sv[j] == T;
-          const unsigned mA = __ballot_sync(0xffffffffu, isA);
-          const unsigned mB = __ballot_sync(0xffffffffu, isB);
-          if (mA) {
-            int off = 0;
-            if (lane == __ffs(mA) - 1) off = atomicAdd(&s_na, __popc(mA));
-            off = __shfl_sync(0xffffffffu, off, __ffs(mA) - 1);
-            if (isA)
-              sA[off + __popc(mA & lt)] =
-                  ((uint64_t)(65535 - sv[j]) << 32) | (uint32_t)(base + j);
-          }
-          if (mB) {
-            int off = 0;
-            if (lane == __ffs(mB) - 1) off = atomicAdd(&s_nb, __popc(mB));
-            off = __shfl_sync(0xffffffffu, off, __ffs(mB) - 1);
-            if (isB) sB[off + __popc(mB & lt)] = (int32_t)(base + j);
-          }
-        }
-      }
-    }
-    __syncthreads();
-    // ties in index order (bitonic, padded to a power of two)
-    const int nB = s_nb;
-    int szb = 1;
-    while (szb < nB) szb <<= 1;
-    for (int i = nB + tid; i < szb; i += THREADS) sB[i] = 0x7fffffff;
-    __syncthreads();
-    for (int k = 2; k <= szb; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = tid; i < szb; i += THREADS) {
-          const int ixj = i ^ j;
-          if (ixj > i) {
-            const int32_t x = sB[i], y = sB[ixj];
-            const bool up = (i & k) == 0;
-            if ((x > y) == up) {
-              sB[i] = y;
-              sB[ixj] = x;
-            }
-          }
-        }
-        __syncthreads();
-      }
-    }
-  } else {
-    if (tid == 0) {
-      s_baseA = 0;
-      s_baseB = 0;
-    }
-    __syncthreads();
-    for (int64_t tile = 0; tile < M; tile += (int64_t)THREADS * VEC) {
-      if (s_baseA >= cntA && s_baseB >= capB) break;  // block-uniform
-      const int64_t base = tile + (int64_t)tid * VEC;
-      uint16_t s[VEC];
-      int a = 0, b = 0;
-      if (base < M) {
-        const uint4 v = *reinterpret_cast<const uint4*>(row + base);
-        const uint16_t* sv = reinterpret_cast<const uint16_t*>(&v);
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) {
-          s[j] = (base + j < M) ? sv[j] : 0;
-          const bool valid = base + j < M;
-          a += valid && s[j] > T;
-          b += valid && s[j] == T;
-        }
-      }
-      const int pre = block_excl_scan_1024(a | (b << 16), warp_tot, &s_total);
-      int ia = s_baseA + (pre & 0xFFFF);
-      int ib = s_baseB + (pre >> 16);
-      if (a | b) {
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) {
-          if (base + j >= M) break;
-          if (s[j] > T) {
-            sA[ia++] = ((uint64_t)(65535 - s[j]) << 32) | (uint32_t)(base + j);
-          } else if (s[j] == T) {
-            if (ib < capB) sB[ib] = (int32_t)(base + j);
-            ++ib;
-          }
-        }
-      }
-      __syncthreads();
-      if (tid == 0) {
-        s_baseA += s_total & 0xFFFF;
-        s_baseB += s_total >> 16;
-      }
-      __syncthreads();
-    }
-  }
-
   // 4. bitonic sort of A (padded to the next power of two >= cntA)
   int sz = 1;
   while (sz < cntA) sz <<= 1;
@@ -331,6 +133,321 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   }
 }
 
+// cut score T over hist[lo .. bins): the largest T with count(>= T) >= need,
+// and cntA = count(> T); found = false if count(>= lo) < need. Warp-wide.
+__device__ __forceinline__ void topk_cut(const int32_t* hist, int bins, int lo, int need,
+                                         int& T, int& cntA, bool& found) {
+  const int lane = threadIdx.x & 31;
+  int running = 0;
+  T = 0;
+  cntA = 0;
+  found = false;
+  for (int top = bins - 1; top >= lo && !found; top -= 32) {
+    const int b = top - lane;
+    const int c = b >= lo ? hist[b] : 0;
+    int incl = c;  // inclusive prefix from the top (lane 0 = highest bin)
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, b >= lo && running + incl >= need);
+    if (hit) {
+      const int l = __ffs(hit) - 1;
+      T = top - l;
+      cntA = running + __shfl_sync(0xffffffffu, incl - c, l);
+      found = true;
+    }
+    running += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+// ascending bitonic sort of n int32 in shared memory (padded with INT_MAX)
+__device__ __forceinline__ void bitonic_i32(int32_t* a, int n) {
+  int sz = 1;
+  while (sz < n) sz <<= 1;
+  for (int i = n + threadIdx.x; i < sz; i += blockDim.x) a[i] = 0x7fffffff;
+  __syncthreads();
+  for (int k = 2; k <= sz; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < sz; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const int32_t x = a[i], y = a[ixj];
+          const bool up = (i & k) == 0;
+          if ((x > y) == up) {
+            a[i] = y;
+            a[ixj] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
+  using namespace topk;
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* sA = reinterpret_cast<uint64_t*>(smem);                   // a_cap
+  int32_t* sB = reinterpret_cast<int32_t*>(sA + p.a_cap);              // b_cap
+  int32_t* hist = sB + p.b_cap;                                        // bins
+  int32_t* chosen = hist + p.bins;                                     // 2*K
+  __shared__ int warp_tot[32];
+  __shared__ int s_total, s_T, s_cntA, s_baseA, s_baseB, s_na, s_nb, s_found;
+  const int BCAP = p.b_cap;
+
+  const int n = blockIdx.x;
+  const int N = p.n_dev ? min(*p.n_dev, p.n_max) : p.n_max;
+  if (n >= N) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint16_t* row = p.heat + (size_t)n * p.stride;
+  const int64_t M = p.M;
+  const int need = (int)(M < (int64_t)p.pool ? M : (int64_t)p.pool);
+
+  // 1. histogram of the scores >= L, L = a quarter of the anchor's own score
+  //    (for a heat map the row maximum: |E_u ∩ E_n| <= |E_n|), so the bulk of
+  //    low scores costs no shared-memory atomics. If fewer than `need`
+  //    positions reach L (or the row is not a heat map), a second pass adds
+  //    the bins below L -- the cut is exact either way.
+  const int64_t aidx = (int64_t)p.anchors[2 * n] * p.ow + p.anchors[2 * n + 1];
+  const int L = min((int)row[aidx] >> 2, p.bins - 1);
+  for (int b = L + tid; b < p.bins; b += THREADS) hist[b] = 0;
+  if (tid == 0) {
+    s_na = 0;
+    s_nb = 0;
+  }
+  __syncthreads();
+  auto hist_pass = [&](int lo, int hi) {  // add the scores in [lo, hi)
+    constexpr int U = 4;  // 16-byte loads in flight per thread
+    for (int64_t tile = 0; tile < M; tile += (int64_t)THREADS * VEC * U) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t base = tile + ((int64_t)u * THREADS + tid) * VEC;
+        v[u] = base < M ? *reinterpret_cast<const uint4*>(row + base) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t base = tile + ((int64_t)u * THREADS + tid) * VEC;
+        const uint16_t* sv = reinterpret_cast<const uint16_t*>(&v[u]);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          const int val = min((int)sv[j], p.bins - 1);
+          if (base + j < M && val >= lo && val < hi) atomicAdd(&hist[val], 1);
+        }
+      }
+    }
+  };
+  hist_pass(L, p.bins);
+  __syncthreads();
+
+  // 2. cut score T: walk bins from the top down to `lo`, 32 at a time
+  auto cut_search = [&](int lo) {
+    int T, cntA;
+    bool found;
+    topk_cut(hist, p.bins, lo, need, T, cntA, found);
+    if (lane == 0) {
+      s_T = T;
+      s_cntA = cntA;
+      s_found = found ? 1 : 0;
+    }
+  };
+  if (warp == 0) cut_search(L);
+  __syncthreads();
+#ifdef GLR_TOPK_STATS
+  if (tid == 0) {
+    atomicAdd(&g_topk_stats[0], 1u);
+    if (!s_found) atomicAdd(&g_topk_stats[1], 1u);
+    unsigned above = 0;
+    for (int b = L; b < p.bins; ++b) above += hist[b];
+    atomicAdd(&g_topk_stats[2], above);
+    atomicMax(&g_topk_stats[3], above);
+  }
+#endif
+  if (!s_found) {
+    for (int b = tid; b < L; b += THREADS) hist[b] = 0;
+    __syncthreads();
+    hist_pass(0, L);
+    __syncthreads();
+    if (warp == 0) cut_search(0);
+    __syncthreads();
+  }
+  const int T = s_T, cntA = s_cntA, capB = need - cntA;
+
+  // 3. collect A = {score > T} (cntA < need entries) and the ties {score == T};
+  //    unordered warp-aggregated appends when the ties fit the buffer (they are
+  //    then sorted by index), else an ordered block-scan compaction.
+  if (hist[T] <= BCAP) {
+    constexpr int U = 4;  // 16-byte loads in flight per thread
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t tile = 0; tile < M; tile += (int64_t)THREADS * VEC * U) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t base = tile + ((int64_t)u * THREADS + tid) * VEC;
+        v[u] = base < M ? *reinterpret_cast<const uint4*>(row + base) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t base = tile + ((int64_t)u * THREADS + tid) * VEC;
+        const uint16_t* sv = reinterpret_cast<const uint16_t*>(&v[u]);
+        // warp-uniform skip of chunks holding no candidate (the common case)
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) any |= base + j < M && sv[j] >= T;
+        if (!__any_sync(0xffffffffu, any)) continue;
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          const bool ok = base + j < M;
+          const bool isA = ok && sv[j] > T, isB = ok && sv[j] == T;
+          const unsigned mA = __ballot_sync(0xffffffffu, isA);
+          const unsigned mB = __ballot_sync(0xffffffffu, isB);
+          if (mA) {
+            int off = 0;
+            if (lane == __ffs(mA) - 1) off = atomicAdd(&s_na, __popc(mA));
+            off = __shfl_sync(0xffffffffu, off, __ffs(mA) - 1);
+            if (isA)
+              sA[off + __popc(mA & lt)] =
+                  ((uint64_t)(65535 - sv[j]) << 32) | (uint32_t)(base + j);
+          }
+          if (mB) {
+            int off = 0;
+            if (lane == __ffs(mB) - 1) off = atomicAdd(&s_nb, __popc(mB));
+            off = __shfl_sync(0xffffffffu, off, __ffs(mB) - 1);
+            if (isB) sB[off + __popc(mB & lt)] = (int32_t)(base + j);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ties in index order
+    bitonic_i32(sB, s_nb);
+  } else {
+    if (tid == 0) {
+      s_baseA = 0;
+      s_baseB = 0;
+    }
+    __syncthreads();
+    for (int64_t tile = 0; tile < M; tile += (int64_t)THREADS * VEC) {
+      if (s_baseA >= cntA && s_baseB >= capB) break;  // block-uniform
+      const int64_t base = tile + (int64_t)tid * VEC;
+      uint16_t s[VEC];
+      int a = 0, b = 0;
+      if (base < M) {
+        const uint4 v = *reinterpret_cast<const uint4*>(row + base);
+        const uint16_t* sv = reinterpret_cast<const uint16_t*>(&v);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          s[j] = (base + j < M) ? sv[j] : 0;
+          const bool valid = base + j < M;
+          a += valid && s[j] > T;
+          b += valid && s[j] == T;
+        }
+      }
+      const int pre = block_excl_scan_1024(a | (b << 16), warp_tot, &s_total);
+      int ia = s_baseA + (pre & 0xFFFF);
+      int ib = s_baseB + (pre >> 16);
+      if (a | b) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          if (base + j >= M) break;
+          if (s[j] > T) {
+            sA[ia++] = ((uint64_t)(65535 - s[j]) << 32) | (uint32_t)(base + j);
+          } else if (s[j] == T) {
+            if (ib < capB) sB[ib] = (int32_t)(base + j);
+            ++ib;
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        s_baseA += s_total & 0xFFFF;
+        s_baseB += s_total >> 16;
+      }
+      __syncthreads();
+    }
+  }
+
+  topk_finish(p, n, M, need, cntA, sA, sB, chosen);
+}
+
+// Top-K over the candidate lists the heat-map GEMM appends in its epilogue
+// (heat_gemm.cu, `glr_heat_topk`): every position whose score reaches
+// L_n = |E_n| / 4 (a quarter of the exemplar's self-score, the row maximum),
+// as (score << 32) | position in arbitrary order. The cut T, A = {> T} and
+// the ties are then exactly those of the full row whenever count(>= L_n) >=
+// need; otherwise (or on list overflow, or > BCAP ties) the exemplar is
+// flagged for the full-row path and its positions are left untouched.
+struct TopkCandParams {
+  TopkParams base;  // heat / n_dev unused
+  const uint64_t* cand;
+  const uint32_t* cnt;
+  const uint16_t* thr;
+  int cap;
+  uint8_t* fallback;
+};
+
+__global__ void __launch_bounds__(topk::THREADS, 3) topk_cand_kernel(TopkCandParams q) {
+  using namespace topk;
+  const TopkParams& p = q.base;
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* sA = reinterpret_cast<uint64_t*>(smem);  // a_cap
+  int32_t* sB = reinterpret_cast<int32_t*>(sA + p.a_cap);  // b_cap
+  int32_t* hist = sB + p.b_cap;                              // bins
+  int32_t* chosen = hist + p.bins;                           // 2*K
+  __shared__ int s_T, s_cntA, s_na, s_nb, s_found;
+  const int n = blockIdx.x;
+  if (n >= p.n_max) return;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int64_t M = p.M;
+  const int need = (int)(M < (int64_t)p.pool ? M : (int64_t)p.pool);
+  const int c = (int)q.cnt[n];
+  const int L = min((int)q.thr[n], p.bins - 1);
+  if (c > q.cap || c < need) {  // block-uniform
+    if (tid == 0) q.fallback[n] = 1;
+    return;
+  }
+  for (int b = L + tid; b < p.bins; b += THREADS) hist[b] = 0;
+  if (tid == 0) {
+    s_na = 0;
+    s_nb = 0;
+  }
+  __syncthreads();
+  const uint64_t* list = q.cand + (size_t)n * q.cap;
+  for (int i = tid; i < c; i += THREADS)
+    atomicAdd(&hist[min((int)(list[i] >> 32), p.bins - 1)], 1);
+  __syncthreads();
+  if (warp == 0) {
+    int T, cntA;
+    bool found;
+    topk_cut(hist, p.bins, L, need, T, cntA, found);
+    if ((tid & 31) == 0) {
+      s_T = T;
+      s_cntA = cntA;
+      s_found = found ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  const int T = s_T, cntA = s_cntA;
+  if (!s_found || hist[T] > p.b_cap) {  // block-uniform
+    if (tid == 0) q.fallback[n] = 1;
+    return;
+  }
+  if (tid == 0) q.fallback[n] = 0;
+  for (int i = tid; i < c; i += THREADS) {
+    const uint64_t e = list[i];
+    const int sc = (int)(e >> 32);
+    const uint32_t pos = (uint32_t)e;
+    if (sc > T)
+      sA[atomicAdd(&s_na, 1)] = ((uint64_t)(65535 - sc) << 32) | pos;
+    else if (sc == T)
+      sB[atomicAdd(&s_nb, 1)] = (int32_t)pos;
+  }
+  __syncthreads();
+  bitonic_i32(sB, s_nb);
+  topk_finish(p, n, M, need, cntA, sA, sB, chosen);
+}
+
 // gather_group (patches.py:43-54): groups[g][j][i], i = (dr*P + dc)*C + ch
 __global__ void gather_kernel(const double* __restrict__ x, int H, int W, int C, int P,
                               const int32_t* __restrict__ pos, int G, int K,
@@ -366,27 +483,31 @@ using namespace glr;
 
 extern "C" size_t glr_topk_workspace(int n_max, int K, int sep) { return 0; }
 
-extern "C" int glr_topk(const uint16_t* heat_d, int n_max, const int32_t* n_dev_d, int oh, int ow,
-                        int max_score, const int32_t* anchors_d, int K, int sep,
-                        int32_t* positions_d, int32_t* padded_d, void* ws_d, size_t ws_bytes,
-                        void* stream) {
+#ifdef GLR_TOPK_STATS
+extern "C" int glr_debug_topk_stats(unsigned int* out) {
+  cudaMemcpyFromSymbol(out, g_topk_stats, sizeof(unsigned int) * 4);
+  return 0;
+}
+#endif
+
+static int topk_params(int n_max, int oh, int ow, int max_score, const int32_t* anchors_d,
+                       int K, int sep, int32_t* positions_d, int32_t* padded_d, TopkParams& p,
+                       size_t& smem) {
   GLR_REQUIRE(K >= 1, GLR_ERR_INVALID, "group_size must be >= 1");
   GLR_REQUIRE(sep >= 0, GLR_ERR_INVALID, "min_separation must be >= 0");
   GLR_REQUIRE(oh >= 1 && ow >= 1, GLR_ERR_INVALID, "topk: empty slice");
   GLR_REQUIRE(max_score >= 0 && max_score < topk::MAX_BINS, GLR_ERR_UNSUPPORTED,
               "topk: max score %d above %d", max_score, topk::MAX_BINS - 1);
-  if (n_max <= 0) return GLR_OK;
   const int64_t M = (int64_t)oh * ow;
   const int pool = (int)std::min<int64_t>(topk_pool(K, sep), M);
   const int bins = max_score + 1;
-  const size_t smem = topk_smem(pool, bins, K);
+  smem = topk_smem(pool, bins, K);
   GLR_REQUIRE(smem <= 200 * 1024, GLR_ERR_UNSUPPORTED,
               "topk: K=%d sep=%d needs %zu bytes of shared memory", K, sep, smem);
-  TopkParams p;
-  p.heat = heat_d;
+  p.heat = nullptr;
   p.stride = cdiv(M, 8) * 8;
   p.n_max = n_max;
-  p.n_dev = n_dev_d;
+  p.n_dev = nullptr;
   p.oh = oh;
   p.ow = ow;
   p.M = M;
@@ -399,11 +520,49 @@ extern "C" int glr_topk(const uint16_t* heat_d, int n_max, const int32_t* n_dev_
   p.b_cap = pow2_at_least(std::max(pool, 4096));
   p.positions = positions_d;
   p.padded = padded_d;
+  return GLR_OK;
+}
+
+extern "C" int glr_topk(const uint16_t* heat_d, int n_max, const int32_t* n_dev_d, int oh, int ow,
+                        int max_score, const int32_t* anchors_d, int K, int sep,
+                        int32_t* positions_d, int32_t* padded_d, void* ws_d, size_t ws_bytes,
+                        void* stream) {
+  TopkParams p;
+  size_t smem = 0;
+  const int st = topk_params(n_max, oh, ow, max_score, anchors_d, K, sep, positions_d,
+                             padded_d, p, smem);
+  if (st != GLR_OK) return st;
+  if (n_max <= 0) return GLR_OK;
+  p.heat = heat_d;
+  p.n_dev = n_dev_d;
   GLR_CUDA(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
   topk_kernel<<<n_max, topk::THREADS, smem, (cudaStream_t)stream>>>(p);
   return check_launch("topk_kernel");
 }
+
+namespace glr {
+int topk_cand_launch(const uint64_t* cand_d, const uint32_t* cnt_d, const uint16_t* thr_d,
+                     int cap, int n_max, int oh, int ow, int max_score,
+                     const int32_t* anchors_d, int K, int sep, int32_t* positions_d,
+                     int32_t* padded_d, uint8_t* fallback_d, void* stream) {
+  TopkCandParams q;
+  size_t smem = 0;
+  const int st = topk_params(n_max, oh, ow, max_score, anchors_d, K, sep, positions_d,
+                             padded_d, q.base, smem);
+  if (st != GLR_OK) return st;
+  if (n_max <= 0) return GLR_OK;
+  q.cand = cand_d;
+  q.cnt = cnt_d;
+  q.thr = thr_d;
+  q.cap = cap;
+  q.fallback = fallback_d;
+  GLR_CUDA(cudaFuncSetAttribute(topk_cand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  topk_cand_kernel<<<n_max, topk::THREADS, smem, (cudaStream_t)stream>>>(q);
+  return check_launch("topk_cand_kernel");
+}
+}  // namespace glr
 
 extern "C" int glr_gather(const double* x_d, int H, int W, int C, int P, const int32_t* positions_d,
                           int G, int K, double* groups_d, void* stream) {

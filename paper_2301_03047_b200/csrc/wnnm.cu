@@ -215,18 +215,20 @@ __device__ __forceinline__ void jacobi_quad(int sr, int B, int e[4]) {
 // Short-latency reciprocal / reciprocal square root for the Jacobi rotation
 // parameters: hardware approximation + two Newton steps (quadratic: full
 // double precision to ~1 ulp; inputs are positive and normal when used).
+template <int NR = 2>
 __device__ __forceinline__ double rcp_nr(double x) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
 #pragma unroll
-  for (int i = 0; i < 2; ++i) y = fma(y, fma(-x, y, 1.0), y);
+  for (int i = 0; i < NR; ++i) y = fma(y, fma(-x, y, 1.0), y);
   return y;
 }
+template <int NR = 2>
 __device__ __forceinline__ double rsqrt_nr(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
 #pragma unroll
-  for (int i = 0; i < 2; ++i) y = fma(0.5 * y, fma(-x * y, y, 1.0), y);
+  for (int i = 0; i < NR; ++i) y = fma(0.5 * y, fma(-x * y, y, 1.0), y);
   return y;
 }
 
@@ -421,9 +423,11 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
               // rsqrt on the latency chain (|t| <= 1)
               const double d = aqq[h] - app[h], g = 2.0 * apq[h];
               const double hh = fma(d, d, g * g);
-              const double tt = (d >= 0.0 ? g : -g) * rcp_nr(fabs(d) + hh * rsqrt_nr(hh));
+              // t only has to zero g_pq to ~1e-14 (one Newton step each); c and
+              // s = t c are then an exactly consistent rotation (two steps)
+              const double tt = (d >= 0.0 ? g : -g) * rcp_nr<1>(fabs(d) + hh * rsqrt_nr<1>(hh));
               t[h] = rot ? tt : 0.0;
-              c[h] = rot ? rsqrt_nr(fma(tt, tt, 1.0)) : 1.0;
+              c[h] = rot ? rsqrt_nr<2>(fma(tt, tt, 1.0)) : 1.0;
               sn[h] = rot ? t[h] * c[h] : 0.0;
             }
 #pragma unroll

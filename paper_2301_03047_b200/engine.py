@@ -131,7 +131,8 @@ class GlrEngine:
     """Device state of one GLR reconstruction (one rank of a sharded run)."""
 
     def __init__(self, shape, match, peak: float = 1.0, c_weight: float = 2.0 * np.sqrt(2.0),
-                 eps: float = 1e-16, process_group=None, heat_budget_bytes: int = 24 << 30):
+                 eps: float = 1e-16, process_group=None, heat_budget_bytes: int = 24 << 30,
+                 low_memory_match: bool = False):
         t = D.torch()
         h, w, c = shape
         self.shape = (h, w, c)
@@ -183,9 +184,28 @@ class GlrEngine:
         self.ws_anchor = D.empty((N.query("glr_anchor_workspace", h, w),), t.uint8)
         self.ws_edge = D.empty((64,), t.uint8)
         # heat map chunking over exemplars (the heat map is never communicated)
-        self.heat_chunk = max(1, min(self.max_anchors, heat_budget_bytes // (2 * self.stride)))
-        self.heat = D.empty((self.heat_chunk, self.stride), t.int16)
-        self.ws_heat = D.empty((N.query("glr_heat_workspace", c, p, self.heat_chunk),), t.uint8)
+        # heat map + top-K, chunked over exemplars beyond the memory budget.
+        # Default: the dense u16 map (glr_heat_map + glr_topk, faster on B200).
+        # low_memory_match: the fused glr_heat_topk -- per-exemplar candidate
+        # lists of `cand_cap` entries instead of the map (8x less memory); the
+        # dense path runs only for the exemplars it hands back.
+        self.heat_budget = heat_budget_bytes
+        self.low_memory_match = bool(low_memory_match)
+        self.heat = None
+        self.ws_dense = None
+        self.n_fallback = 0     # exemplars that took the dense path (last refresh)
+        if self.low_memory_match:
+            self.cand_cap = int(min(1 << 17, self.oh * self.ow))
+            per = 8 * self.cand_cap + N.query("glr_heat_topk_workspace", c, p, 1, 0)
+            self.heat_chunk = max(1, min(self.max_anchors, heat_budget_bytes // per))
+            self.ws_heat = D.empty((N.query("glr_heat_topk_workspace", c, p, self.heat_chunk,
+                                            self.cand_cap),), t.uint8)
+            self.fallback = D.zeros((self.heat_chunk,), t.uint8)
+        else:
+            self.heat_chunk = max(1, min(self.max_anchors, heat_budget_bytes // (2 * self.stride)))
+            self.heat = D.empty((self.heat_chunk, self.stride), t.int16)
+            self.ws_dense = D.empty((N.query("glr_heat_workspace", c, p, self.heat_chunk),),
+                                    t.uint8)
         self.ws_wnnm = D.empty((N.query("glr_wnnm_workspace", self.max_anchors, self.k),),
                                t.uint8)
         # per-group Jacobi eigenvectors, warm start between refreshes
@@ -278,20 +298,58 @@ class GlrEngine:
     def match_shard(self):
         h, w, c = self.shape
         s = D.stream()
+        t = D.torch()
+        self.n_fallback = 0
         for a in range(self.lo, self.hi, self.heat_chunk):
             b = min(self.hi, a + self.heat_chunk)
             nb = b - a
             anc = self.anchors[a:b]
+            if not self.low_memory_match:
+                e = self._ev()
+                N.call("glr_heat_map", self.stack.data_ptr(), h, w, c, self.p, self.expand,
+                       anc.data_ptr(), nb, None, self.heat.data_ptr(), self.ws_dense.data_ptr(),
+                       self.ws_dense.numel(), s)
+                self._log(("heat_map", nb), e)
+                e = self._ev()
+                N.call("glr_topk", self.heat.data_ptr(), nb, None, self.oh, self.ow,
+                       self.max_score, anc.data_ptr(), self.k, self.mc.sep,
+                       self.positions[a:b].data_ptr(), self.padded[a:b].data_ptr(), None, 0, s)
+                self._log(("topk", nb), e)
+                continue
             e = self._ev()
+            N.call("glr_heat_topk", self.stack.data_ptr(), h, w, c, self.p, self.expand,
+                   anc.data_ptr(), nb, self.k, self.mc.sep, self.cand_cap,
+                   self.positions[a:b].data_ptr(), self.padded[a:b].data_ptr(),
+                   self.fallback.data_ptr(), self.ws_heat.data_ptr(), self.ws_heat.numel(), s)
+            self._log(("heat_topk", nb), e)
+            fb = t.nonzero(self.fallback[:nb]).flatten()  # one host sync per chunk
+            if fb.numel():
+                self._dense_match(a, fb)
+
+    def _dense_match(self, a, fb):
+        """Full heat rows + glr_topk for the exemplars the fused path handed back."""
+        h, w, c = self.shape
+        s = D.stream()
+        t = D.torch()
+        self.n_fallback += int(fb.numel())
+        rows = max(1, min(int(fb.numel()), self.heat_budget // (2 * self.stride)))
+        if self.heat is None or self.heat.shape[0] < rows:
+            self.heat = D.empty((rows, self.stride), t.int16)
+            self.ws_dense = D.empty((N.query("glr_heat_workspace", c, self.p, rows),), t.uint8)
+        for i in range(0, int(fb.numel()), rows):
+            idx = fb[i:i + rows] + a
+            nb = int(idx.numel())
+            anc = self.anchors.index_select(0, idx).contiguous()
+            pos = D.empty((nb, self.k, 2), t.int32)
+            pad = D.empty((nb,), t.int32)
             N.call("glr_heat_map", self.stack.data_ptr(), h, w, c, self.p, self.expand,
-                   anc.data_ptr(), nb, None, self.heat.data_ptr(), self.ws_heat.data_ptr(),
-                   self.ws_heat.numel(), s)
-            self._log(("heat_map", nb), e)
-            e = self._ev()
+                   anc.data_ptr(), nb, None, self.heat.data_ptr(), self.ws_dense.data_ptr(),
+                   self.ws_dense.numel(), s)
             N.call("glr_topk", self.heat.data_ptr(), nb, None, self.oh, self.ow, self.max_score,
-                   anc.data_ptr(), self.k, self.mc.sep, self.positions[a:b].data_ptr(),
-                   self.padded[a:b].data_ptr(), None, 0, s)
-            self._log(("topk", nb), e)
+                   anc.data_ptr(), self.k, self.mc.sep, pos.data_ptr(), pad.data_ptr(), None, 0,
+                   s)
+            self.positions.index_copy_(0, idx, pos)
+            self.padded.index_copy_(0, idx, pad)
 
     def count(self):
         h, w, c = self.shape

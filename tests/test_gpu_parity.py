@@ -309,3 +309,28 @@ def test_vcache_remap_reindexes_kept_positions(rng):
             occ = [i for i in range(K) if key(old_pos[g_old, i]) == v]
             if t < len(occ):
                 assert perm[j] == occ[t], (g_new, j)
+
+
+@pytest.mark.parametrize("cap", [None, 8])
+def test_fused_heat_topk_matches_dense(cap, rng):
+    """glr_heat_topk (candidate lists from the GEMM epilogue, low-memory mode)
+    gives the same positions as the dense heat map + glr_topk; cap = 8 forces
+    every exemplar through the overflow fallback (dense path)."""
+    from paper_2301_03047_b200 import _device as D
+    from paper_2301_03047_b200.engine import GlrEngine
+    h, w, c = 150, 170, 4
+    base = rng.random((h // 6 + 2, w // 6 + 2, c))
+    x = np.kron(base, np.ones((6, 6, 1)))[:h, :w] + 0.1 * rng.random((h, w, c))
+    mc = G.MatchConfig(patch_size=8, group_size=16, max_corners=60, exemplar_stride=6)
+    xd = D.f64(x)
+    dense = GlrEngine((h, w, c), mc)
+    dense.refresh(xd)
+    a0, p0, d0 = dense.positions_host()
+    fused = GlrEngine((h, w, c), mc, low_memory_match=True)
+    if cap is not None:
+        fused.cand_cap = cap
+    fused.refresh(xd)
+    a1, p1, d1 = fused.positions_host()
+    assert np.array_equal(a0, a1) and np.array_equal(p0, p1) and np.array_equal(d0, d1)
+    if cap is not None:
+        assert fused.n_fallback == len(a1)

@@ -50,6 +50,11 @@ struct TopkParams {
   int b_cap;                // tie buffer: power of two >= max(pool, 4096)
   int32_t* positions;
   int32_t* padded;
+  // optional per-exemplar scratch (n_max x scap): the first pass also records
+  // every (score >= L, position) so the collection pass reads this list
+  // instead of the row again
+  uint64_t* scratch;
+  int scap;
 };
 
 __device__ __forceinline__ int cheb(int r0, int c0, int r1, int c1) {
@@ -193,7 +198,7 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   int32_t* hist = sB + p.b_cap;                                        // bins
   int32_t* chosen = hist + p.bins;                                     // 2*K
   __shared__ int warp_tot[32];
-  __shared__ int s_total, s_T, s_cntA, s_baseA, s_baseB, s_na, s_nb, s_found;
+  __shared__ int s_total, s_T, s_cntA, s_baseA, s_baseB, s_na, s_nb, s_found, s_nl;
   const int BCAP = p.b_cap;
 
   const int n = blockIdx.x;
@@ -215,10 +220,15 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   if (tid == 0) {
     s_na = 0;
     s_nb = 0;
+    s_nl = 0;
   }
   __syncthreads();
-  auto hist_pass = [&](int lo, int hi) {  // add the scores in [lo, hi)
+  uint64_t* list = p.scratch ? p.scratch + (size_t)n * p.scap : nullptr;
+  auto hist_pass = [&](int lo, int hi, bool record) {  // add the scores in [lo, hi)
     constexpr int U = 4;  // 16-byte loads in flight per thread
+    // SIMD pre-test: 8 scores per 16-byte chunk against lo (two u16 per word);
+    // only the rare chunks holding a score >= lo take the per-element path
+    const uint32_t lo2 = (uint32_t)lo | ((uint32_t)lo << 16);
     for (int64_t tile = 0; tile < M; tile += (int64_t)THREADS * VEC * U) {
       uint4 v[U];
 #pragma unroll
@@ -229,16 +239,25 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t base = tile + ((int64_t)u * THREADS + tid) * VEC;
+        const uint32_t any = __vcmpgeu2(v[u].x, lo2) | __vcmpgeu2(v[u].y, lo2) |
+                             __vcmpgeu2(v[u].z, lo2) | __vcmpgeu2(v[u].w, lo2);
+        if (!any) continue;
         const uint16_t* sv = reinterpret_cast<const uint16_t*>(&v[u]);
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
           const int val = min((int)sv[j], p.bins - 1);
-          if (base + j < M && val >= lo && val < hi) atomicAdd(&hist[val], 1);
+          if (base + j < M && val >= lo && val < hi) {
+            atomicAdd(&hist[val], 1);
+            if (record) {
+              const int off = atomicAdd(&s_nl, 1);
+              if (off < p.scap) list[off] = ((uint64_t)val << 32) | (uint32_t)(base + j);
+            }
+          }
         }
       }
     }
   };
-  hist_pass(L, p.bins);
+  hist_pass(L, p.bins, list != nullptr);
   __syncthreads();
 
   // 2. cut score T: walk bins from the top down to `lo`, 32 at a time
@@ -264,10 +283,11 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
     atomicMax(&g_topk_stats[3], above);
   }
 #endif
+  const bool first_pass_cut = s_found;
   if (!s_found) {
     for (int b = tid; b < L; b += THREADS) hist[b] = 0;
     __syncthreads();
-    hist_pass(0, L);
+    hist_pass(0, L, false);
     __syncthreads();
     if (warp == 0) cut_search(0);
     __syncthreads();
@@ -277,7 +297,21 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   // 3. collect A = {score > T} (cntA < need entries) and the ties {score == T};
   //    unordered warp-aggregated appends when the ties fit the buffer (they are
   //    then sorted by index), else an ordered block-scan compaction.
-  if (hist[T] <= BCAP) {
+  if (list && first_pass_cut && s_nl <= p.scap && hist[T] <= BCAP) {
+    // the recorded list holds every score >= L >= ... >= T: no second row read
+    const int c = s_nl;
+    for (int i = tid; i < c; i += THREADS) {
+      const uint64_t e = list[i];
+      const int sc = (int)(e >> 32);
+      const uint32_t pos = (uint32_t)e;
+      if (sc > T)
+        sA[atomicAdd(&s_na, 1)] = ((uint64_t)(65535 - sc) << 32) | pos;
+      else if (sc == T)
+        sB[atomicAdd(&s_nb, 1)] = (int32_t)pos;
+    }
+    __syncthreads();
+    bitonic_i32(sB, s_nb);
+  } else if (hist[T] <= BCAP) {
     constexpr int U = 4;  // 16-byte loads in flight per thread
     const unsigned lt = (1u << lane) - 1u;
     for (int64_t tile = 0; tile < M; tile += (int64_t)THREADS * VEC * U) {
@@ -481,7 +515,11 @@ static size_t topk_smem(int pool, int bins, int K) {
 
 using namespace glr;
 
-extern "C" size_t glr_topk_workspace(int n_max, int K, int sep) { return 0; }
+// optional: n_max x kTopkScratch (score, position) records (single row pass)
+constexpr int kTopkScratch = 32768;
+extern "C" size_t glr_topk_workspace(int n_max, int K, int sep) {
+  return (size_t)std::max(n_max, 0) * kTopkScratch * sizeof(uint64_t) + 256;
+}
 
 #ifdef GLR_TOPK_STATS
 extern "C" int glr_debug_topk_stats(unsigned int* out) {
@@ -520,6 +558,8 @@ static int topk_params(int n_max, int oh, int ow, int max_score, const int32_t* 
   p.b_cap = pow2_at_least(std::max(pool, 4096));
   p.positions = positions_d;
   p.padded = padded_d;
+  p.scratch = nullptr;
+  p.scap = 0;
   return GLR_OK;
 }
 
@@ -535,6 +575,11 @@ extern "C" int glr_topk(const uint16_t* heat_d, int n_max, const int32_t* n_dev_
   if (n_max <= 0) return GLR_OK;
   p.heat = heat_d;
   p.n_dev = n_dev_d;
+  if (ws_d && ws_bytes >= glr_topk_workspace(n_max, K, sep)) {
+    p.scratch = reinterpret_cast<uint64_t*>(
+        (reinterpret_cast<uintptr_t>(ws_d) + 255) & ~uintptr_t(255));
+    p.scap = kTopkScratch;
+  }
   GLR_CUDA(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
   topk_kernel<<<n_max, topk::THREADS, smem, (cudaStream_t)stream>>>(p);

@@ -206,6 +206,8 @@ class GlrEngine:
             self.heat = D.empty((self.heat_chunk, self.stride), t.int16)
             self.ws_dense = D.empty((N.query("glr_heat_workspace", c, p, self.heat_chunk),),
                                     t.uint8)
+            self.ws_topk = D.empty((N.query("glr_topk_workspace", self.heat_chunk, self.k,
+                                            match.sep),), t.uint8)
         self.ws_wnnm = D.empty((N.query("glr_wnnm_workspace", self.max_anchors, self.k),),
                                t.uint8)
         # per-group Jacobi eigenvectors, warm start between refreshes
@@ -313,7 +315,8 @@ class GlrEngine:
                 e = self._ev()
                 N.call("glr_topk", self.heat.data_ptr(), nb, None, self.oh, self.ow,
                        self.max_score, anc.data_ptr(), self.k, self.mc.sep,
-                       self.positions[a:b].data_ptr(), self.padded[a:b].data_ptr(), None, 0, s)
+                       self.positions[a:b].data_ptr(), self.padded[a:b].data_ptr(),
+                       self.ws_topk.data_ptr(), self.ws_topk.numel(), s)
                 self._log(("topk", nb), e)
                 continue
             e = self._ev()

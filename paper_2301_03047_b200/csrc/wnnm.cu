@@ -35,7 +35,11 @@ constexpr int ARS = AROWS + 8;    // column stride of the apply tiles (== 8 mod 
 constexpr int GRAM_THREADS = 96;  // three warps: super-blocks (0,0), (0,1), (1,1)
 constexpr int EIG_THREADS = 256;
 constexpr int APPLY_THREADS = 256;
+#ifdef GLR_EIG_MAXSWEEPS  // dev experiments only
+constexpr int MAX_SWEEPS = GLR_EIG_MAXSWEEPS;
+#else
 constexpr int MAX_SWEEPS = 24;
+#endif
 constexpr int GSZ = KMAX * KMAX;  // doubles per group in the G / Wm / V buffers
 // Jacobi rotation threshold: skip (p,q) once |g_pq| <= kRotTol sqrt(|g_pp g_qq|).
 // With quadratic convergence the last sweep above this level leaves the

@@ -30,11 +30,12 @@ constexpr int GLD = KMAX + 2;     // row stride of G in the eigen kernel (pair r
 constexpr int VLD = KMAX + 1;     // row stride of V^T in the eigen kernel
 constexpr int GROWS = 32;         // rows of M per Gram tile
 constexpr int GRS = GROWS + 4;    // column stride of the Gram tiles (== 4 mod 16)
-constexpr int AROWS = 64;         // rows of M per apply tile (one 8-row tile row per warp)
+constexpr int AROWS = 64;         // rows of M per apply tile (APPLY_RPW 8-row fragments per warp)
 constexpr int ARS = AROWS + 8;    // column stride of the apply tiles (== 8 mod 16)
 constexpr int GRAM_THREADS = 96;  // three warps: super-blocks (0,0), (0,1), (1,1)
 constexpr int EIG_THREADS = 256;
 constexpr int APPLY_THREADS = 256;
+constexpr int APPLY_RPW = 1;      // 8-row fragments per warp in the apply kernel
 #ifdef GLR_EIG_MAXSWEEPS  // dev experiments only
 constexpr int MAX_SWEEPS = GLR_EIG_MAXSWEEPS;
 #else
@@ -606,36 +607,45 @@ __global__ void __launch_bounds__(wn::APPLY_THREADS)
     cp_async_wait<1>();
     __syncthreads();
     const double* R = T + (tt & 1) * KMAX * ARS;
-    double o[8][2];
+    double o[APPLY_RPW][8][2];
 #pragma unroll
-    for (int b = 0; b < 8; ++b) o[b][0] = o[b][1] = 0.0;
+    for (int f = 0; f < APPLY_RPW; ++f)
+#pragma unroll
+      for (int b = 0; b < 8; ++b) o[f][b][0] = o[f][b][1] = 0.0;
 #pragma unroll 4
     for (int k0 = 0; k0 < KMAX; k0 += 4) {  // zero columns beyond K contribute nothing
-      const double fa = R[(k0 + ak) * ARS + 8 * warp + ar];
+      double fa[APPLY_RPW];
+#pragma unroll
+      for (int f = 0; f < APPLY_RPW; ++f)
+        fa[f] = R[(k0 + ak) * ARS + 8 * (APPLY_RPW * warp + f) + ar];
 #pragma unroll
       for (int b = 0; b < 8; ++b) {
         const double fb = Ws[(k0 + ak) * LD + 8 * b + ar];
-        dmma(o[b][0], o[b][1], fa, fb);
+#pragma unroll
+        for (int f = 0; f < APPLY_RPW; ++f) dmma(o[f][b][0], o[f][b][1], fa[f], fb);
       }
     }
-    const int r = r0 + 8 * warp + ar;
-    if (r < m) {
-      const int64_t off = (int64_t)(r / s.PC) * s.rs + (r % s.PC);
 #pragma unroll
-      for (int b = 0; b < 8; ++b)
+    for (int f = 0; f < APPLY_RPW; ++f) {
+      const int r = r0 + 8 * (APPLY_RPW * warp + f) + ar;
+      if (r < m) {
+        const int64_t off = (int64_t)(r / s.PC) * s.rs + (r % s.PC);
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int j = 8 * b + 2 * ak + e;
-          if (j < K) {
-            if constexpr (IMG) {
-              const long long val = __double2ll_rn(o[b][e] * scale);
-              atomicAdd(reinterpret_cast<unsigned long long*>(acc_out + cbase[j] + off),
-                        (unsigned long long)val);
-            } else {
-              out[cbase[j] + off] = o[b][e];
+        for (int b = 0; b < 8; ++b)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = 8 * b + 2 * ak + e;
+            if (j < K) {
+              if constexpr (IMG) {
+                const long long val = __double2ll_rn(o[f][b][e] * scale);
+                atomicAdd(reinterpret_cast<unsigned long long*>(acc_out + cbase[j] + off),
+                          (unsigned long long)val);
+              } else {
+                out[cbase[j] + off] = o[f][b][e];
+              }
             }
           }
-        }
+      }
     }
     __syncthreads();
   }

@@ -242,6 +242,16 @@ int glr_interp_msfa(const double* xt_d, const double* masks_d, int H, int W, int
 int glr_interp_cacti(const double* xt_d, const double* gram_d, int H, int W, int C,
                      double* out_d, void* stream);
 
+/* f3 -- on-device SSIM (metrics.py:40-78 + the clip of solvers.py:262-264):
+ * *out_d = SUM over channels and valid window positions of the SSIM map
+ * (divide by C*(H-S+1)*(W-S+1) for the reference's mean); window = the S
+ * normalised 1-D Gaussian taps (HOST pointer), the 2-D window being their
+ * outer product; clip != 0 clips x to [0, peak] first.
+ * ws: glr_ssim_workspace(H, W, C) bytes.                                     */
+size_t glr_ssim_workspace(int H, int W, int C);
+int glr_ssim(const double* x_d, const double* ref_d, int H, int W, int C, double peak, int clip,
+             const double* window, int win_size, double* out_d, void* ws_d, void* stream);
+
 /* glr_lincomb: out = clip((a*x + b*y) + c*z) elementwise, y/z optional (NULL),
  * in that evaluation order (the ADMM bookkeeping of solvers.py:327-334). */
 int glr_lincomb(const double* x_d, double a, const double* y_d, double b, const double* z_d,

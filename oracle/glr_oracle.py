@@ -565,6 +565,38 @@ def admm_solve(op: Operator, y, max_iters, patch_size=8, group_size=64, max_corn
     return out, residuals, psnrs
 
 
+def ssim(a, b, peak=1.0, win_size=11, win_sigma=1.5):
+    """metrics.py:40-78 — mean SSIM over all valid 11x11 Gaussian windows,
+    averaged over channels (2-D window = outer product of the normalised
+    1-D taps; sums evaluated with the separable form)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    h, w, c = a.shape
+    if h < win_size or w < win_size:
+        raise ValueError(f"image {h}x{w} smaller than {win_size}x{win_size} window")
+    ax = np.arange(win_size) - (win_size - 1) / 2.0
+    g = np.exp(-(ax ** 2) / (2.0 * win_sigma ** 2))
+    g = g / g.sum()
+    c1, c2 = (0.01 * peak) ** 2, (0.03 * peak) ** 2
+
+    def filt(z):  # valid separable correlation, rows then columns
+        from numpy.lib.stride_tricks import sliding_window_view
+        r = (sliding_window_view(z, win_size, axis=1) * g).sum(axis=-1)
+        return (sliding_window_view(r, win_size, axis=0) * g).sum(axis=-1)
+
+    vals = []
+    for ch in range(c):
+        x, y = a[:, :, ch], b[:, :, ch]
+        ma, mb = filt(x), filt(y)
+        va = filt(x * x) - ma ** 2
+        vb = filt(y * y) - mb ** 2
+        cov = filt(x * y) - ma * mb
+        num = (2 * ma * mb + c1) * (2 * cov + c2)
+        den = (ma ** 2 + mb ** 2 + c1) * (va + vb + c2)
+        vals.append(float(np.mean(num / den)))
+    return float(np.mean(vals))
+
+
 def heat_flops(h, w, c, p, n):
     """2*M*(4*C*P^2)*N flops per refresh."""
     return 2.0 * (h - p + 1) * (w - p + 1) * 4 * c * p * p * n

@@ -84,6 +84,8 @@ SIGNATURES: dict[str, tuple] = {
     "glr_interp_msfa": (i32, [vp, vp, i32, i32, i32, C.POINTER(C.c_double), i32, vp, vp, vp]),
     "glr_interp_cacti": (i32, [vp, vp, i32, i32, i32, vp, vp]),
     "glr_sq_err": (i32, [vp, vp, i32, f64, vp, vp, vp]),
+    "glr_ssim_workspace": (sz, [i32, i32, i32]),
+    "glr_ssim": (i32, [vp, vp, i32, i32, i32, f64, i32, C.POINTER(C.c_double), i32, vp, vp, vp]),
 }
 
 _lib = None
@@ -143,7 +145,7 @@ KERNELS_PER_CALL = {
     "glr_scatter_add_f64": 1, "glr_normalize": 1, "glr_masksum_forward": 1,
     "glr_masksum_adjoint": 1, "glr_gap_masksum": 2, "glr_fourier_forward": 4,
     "glr_fourier_adjoint": 4, "glr_gap_fourier": 11, "glr_sq_err": 2, "glr_vcache_remap": 3,
-    "glr_lincomb": 1, "glr_interp_msfa": 3, "glr_interp_cacti": 1, "glr_heat_topk": 4,
+    "glr_lincomb": 1, "glr_interp_msfa": 3, "glr_interp_cacti": 1, "glr_heat_topk": 4, "glr_ssim": 3,
 }
 launch_count = 0
 

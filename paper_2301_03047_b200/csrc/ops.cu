@@ -363,6 +363,102 @@ extern "C" int glr_lincomb(const double* x_d, double a, const double* y_d, doubl
   return check_launch("lincomb_kernel");
 }
 
+// ---------------------------------------------------------------------------
+// f3: on-device SSIM (metrics.py:40-78): per channel, an 11x11 Gaussian window
+// (sigma 1.5, normalised) over every valid position, SSIM map averaged over the
+// positions and the channels. The separable form g/sum(g) (x) g/sum(g) of the
+// reference's outer-product window; a = clip(x, 0, peak) as in _record
+// (solvers.py:262-264), b = ref. Deterministic block sums. Reporting metric:
+// compared with the reference to 1e-10, not bitwise.
+
+struct SsimW {
+  double g[16];
+  int S;
+};
+
+// pass 1 (along rows): five windowed sums per (row, valid col, channel)
+__global__ void ssim_rows_kernel(const double* __restrict__ x, const double* __restrict__ ref,
+                                 int H, int W, int C, double peak, int clip, SsimW w,
+                                 double* __restrict__ t) {
+  const int Wv = W - w.S + 1;
+  const int64_t n = (int64_t)H * Wv * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int ch = (int)(i % C);
+    const int64_t rc = i / C;
+    const int r = (int)(rc / Wv), c = (int)(rc % Wv);
+    double sa = 0, sb = 0, saa = 0, sbb = 0, sab = 0;
+    for (int k = 0; k < w.S; ++k) {
+      const int64_t j = ((int64_t)r * W + c + k) * C + ch;
+      double a = x[j];
+      if (clip) a = fmin(fmax(a, 0.0), peak);
+      const double b = ref[j], g = w.g[k];
+      sa = fma(g, a, sa);
+      sb = fma(g, b, sb);
+      saa = fma(g, a * a, saa);
+      sbb = fma(g, b * b, sbb);
+      sab = fma(g, a * b, sab);
+    }
+    t[i] = sa;
+    t[i + n] = sb;
+    t[i + 2 * n] = saa;
+    t[i + 3 * n] = sbb;
+    t[i + 4 * n] = sab;
+  }
+}
+
+// pass 2 (along columns) + SSIM map + block partial sums
+__global__ void ssim_cols_kernel(const double* __restrict__ t, int H, int W, int C, double peak,
+                                 SsimW w, double* __restrict__ part) {
+  const int Wv = W - w.S + 1, Hv = H - w.S + 1;
+  const int64_t n = (int64_t)H * Wv * C, nv = (int64_t)Hv * Wv * C;
+  const double c1 = (0.01 * peak) * (0.01 * peak), c2 = (0.03 * peak) * (0.03 * peak);
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int ch = (int)(i % C);
+    const int64_t rc = i / C;
+    const int r = (int)(rc / Wv), c = (int)(rc % Wv);
+    double m[5] = {0, 0, 0, 0, 0};
+    for (int k = 0; k < w.S; ++k) {
+      const int64_t j = ((int64_t)(r + k) * Wv + c) * C + ch;
+      const double g = w.g[k];
+#pragma unroll
+      for (int q = 0; q < 5; ++q) m[q] = fma(g, t[j + q * n], m[q]);
+    }
+    const double ma = m[0], mb = m[1];
+    const double va = m[2] - ma * ma, vb = m[3] - mb * mb, cov = m[4] - ma * mb;
+    const double num = (2 * ma * mb + c1) * (2 * cov + c2);
+    const double den = (ma * ma + mb * mb + c1) * (va + vb + c2);
+    acc += num / den;
+  }
+  block_sum_store(acc, part);
+}
+
+extern "C" size_t glr_ssim_workspace(int H, int W, int C) {
+  return (5 * (size_t)H * W * C + kGapBlocks + 8) * sizeof(double);
+}
+
+extern "C" int glr_ssim(const double* x_d, const double* ref_d, int H, int W, int C, double peak,
+                        int clip, const double* window, int win_size, double* out_d, void* ws_d,
+                        void* stream) {
+  GLR_REQUIRE(win_size >= 1 && win_size <= 16, GLR_ERR_UNSUPPORTED, "ssim: window %d", win_size);
+  GLR_REQUIRE(H >= win_size && W >= win_size, GLR_ERR_INVALID,
+              "image %dx%d smaller than %dx%d window", H, W, win_size, win_size);
+  cudaStream_t st = (cudaStream_t)stream;
+  SsimW w;
+  w.S = win_size;
+  for (int i = 0; i < win_size; ++i) w.g[i] = window[i];
+  double* t = reinterpret_cast<double*>(ws_d);
+  double* part = t + 5 * (size_t)H * W * C;
+  ssim_rows_kernel<<<kGapBlocks * 2, 256, 0, st>>>(x_d, ref_d, H, W, C, peak, clip, w, t);
+  GLR_CUDA(cudaGetLastError());
+  ssim_cols_kernel<<<kGapBlocks, 256, 0, st>>>(t, H, W, C, peak, w, part);
+  GLR_CUDA(cudaGetLastError());
+  final_sum_kernel<<<1, 256, 0, st>>>(part, kGapBlocks, out_d);
+  return check_launch("ssim");
+}
+
 extern "C" int glr_sq_err(const double* x_d, const double* ref_d, int n, double peak,
                           double* out_d, void* ws_d, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;

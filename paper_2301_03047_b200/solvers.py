@@ -212,6 +212,31 @@ class GapRunner:
         N.call("glr_sq_err", x.data_ptr(), ref_d.data_ptr(), n_el, float(self.cfg.peak),
                self.sq[it:it + 1].data_ptr(), self.sq_ws.data_ptr(), D.stream())
 
+    def record_metrics(self, x, ref_d, it):
+        """PSNR numerator and SSIM of clip(x, 0, peak) vs ref on device (f3:
+        _record solvers.py:257-269 without a per-iteration host copy)."""
+        t = D.torch()
+        self.sq_err(x, ref_d, it)
+        h, w, c = self.dop.shape
+        if h < 11 or w < 11:
+            return
+        if getattr(self, "ssim_sum", None) is None:
+            self.ssim_sum = D.zeros((self.cfg.max_iters,), t.float64)
+            self.ssim_ws = D.empty((N.query("glr_ssim_workspace", h, w, c),), t.uint8)
+            ax = np.arange(11) - 5.0
+            g = np.exp(-(ax ** 2) / (2.0 * 1.5 ** 2))
+            self._ssim_taps = np.ascontiguousarray(g / g.sum())
+        taps = self._ssim_taps.ctypes.data_as(N.C.POINTER(N.C.c_double))
+        N.call("glr_ssim", x.data_ptr(), ref_d.data_ptr(), h, w, c, float(self.cfg.peak), 1,
+               taps, 11, self.ssim_sum[it:it + 1].data_ptr(), self.ssim_ws.data_ptr(), D.stream())
+
+    def ssim_host(self):
+        """Per-iteration SSIM values (one D2H at the end of the solve)."""
+        h, w, c = self.dop.shape
+        if getattr(self, "ssim_sum", None) is None:
+            return None
+        return D.host(self.ssim_sum) / float(c * (h - 10) * (w - 10))
+
     def run(self, y_d, positions_override=None, trace=None, on_iter=None, events=False):
         """One full GAP-GLR solve (solvers.py:284-308) on device; returns the
         final iterate (device tensor, before the final [0, peak] clip)."""
@@ -257,6 +282,15 @@ class GapRunner:
         return x
 
 
+def _ssim_values(runner, ref):
+    """Device SSIM per iteration; the host formula only for images below the
+    11x11 window (where the reference raises, metrics.py:71-72)."""
+    v = runner.ssim_host()
+    if v is None:  # image smaller than the window: the reference's error path
+        ssim(ref, ref, 1.0)
+    return v
+
+
 def _final_host(runner, x) -> np.ndarray:
     """The solver's return value: clip(x, 0, peak) (solvers.py:307) computed on
     device into the runner's spare iterate buffer, then one pinned D2H copy."""
@@ -288,18 +322,17 @@ def gap_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = Non
     y_d = dop.upload_y(y)
     iters = cfg.max_iters
     ref_d = D.f64(ref) if ref is not None else None
-    ssims = []
 
     def on_iter(it, x):
         if ref_d is not None:
-            runner.sq_err(x, ref_d, it)
-            ssims.append(ssim(ref, np.clip(D.host(x), 0.0, cfg.peak), cfg.peak))
+            runner.record_metrics(x, ref_d, it)
 
     x = runner.run(y_d, positions_override=positions_override, trace=trace,
                    on_iter=on_iter, events=True)
     t.cuda.synchronize()
     res = np.sqrt(D.host(runner.resid_sq)).tolist()
     sqh = D.host(runner.sq) if ref_d is not None else None
+    ssims = _ssim_values(runner, ref) if ref_d is not None else None
     ev = runner.events
     for it in range(iters):
         e0, e1, e2, e3 = ev[it]
@@ -311,7 +344,7 @@ def gap_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = Non
             mse = sqh[it] / float(np.prod(dop.shape))
             row["psnr_db"] = PSNR_CAP_DB if mse == 0.0 else \
                 min(10.0 * np.log10(cfg.peak ** 2 / mse), PSNR_CAP_DB)
-            row["ssim"] = ssims[it]
+            row["ssim"] = float(ssims[it])
         report.add(**row)
     report.total_ms = (time.perf_counter() - t_start) * 1e3
     y_norm = float(np.linalg.norm(y.ravel()))
@@ -402,17 +435,16 @@ def admm_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = No
     runner = AdmmRunner(op, cfg, process_group=process_group)
     y_d = runner.dop.upload_y(y)
     ref_d = D.f64(ref) if ref is not None else None
-    ssims = []
 
     def on_iter(it, x):
         if ref_d is not None:
-            runner.sq_err(x, ref_d, it)
-            ssims.append(ssim(ref, np.clip(D.host(x), 0.0, cfg.peak), cfg.peak))
+            runner.record_metrics(x, ref_d, it)
 
     x = runner.run(y_d, on_iter=on_iter, events=True)
     t.cuda.synchronize()
     res = np.sqrt(D.host(runner.resid_sq)).tolist()
     sqh = D.host(runner.sq) if ref_d is not None else None
+    ssims = _ssim_values(runner, ref) if ref_d is not None else None
     n_el = float(np.prod(runner.dop.shape))
     for it, (e0, e1, e2, e3) in enumerate(runner.events):
         row = {"iteration": it, "residual": float(res[it]),
@@ -423,7 +455,7 @@ def admm_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = No
             mse = sqh[it] / n_el
             row["psnr_db"] = PSNR_CAP_DB if mse == 0.0 else \
                 min(10.0 * np.log10(cfg.peak ** 2 / mse), PSNR_CAP_DB)
-            row["ssim"] = ssims[it]
+            row["ssim"] = float(ssims[it])
         report.add(**row)
     report.total_ms = (time.perf_counter() - t_start) * 1e3
     y_norm = float(np.linalg.norm(y.ravel()))

@@ -254,6 +254,21 @@ def gen_admm():
         ref_solvers.global_match = orig
 
 
+def gen_metrics():
+    """metrics.py: psnr / ssim of the reference on small random pairs."""
+    rng = np.random.default_rng(909)
+    cases = {}
+    shapes = [(11, 11, 1), (24, 31, 3), (40, 36, 8)]
+    for i, sh in enumerate(shapes):
+        a = f32(rng.random(sh))
+        b = np.clip(a + 0.1 * f32(rng.standard_normal(sh)), -0.2, 1.3)
+        cases.update({f"a{i}": a, f"b{i}": b,
+                      f"ssim{i}": np.array(glr.ssim(a, np.clip(b, 0, 1), 1.0)),
+                      f"psnr{i}": np.array(glr.psnr(a, np.clip(b, 0, 1), 1.0))})
+    cases["n"] = np.array(len(shapes))
+    np.savez_compressed(OUT / "metrics.npz", **cases)
+
+
 def gen_interp():
     """init="interp" (solvers.py:237-254): the reference's _interp_init on
     MSFA / CACTI / Fourier operators, and one MSFA gap_solve started from it."""
@@ -302,6 +317,7 @@ if __name__ == "__main__":
         for name in sys.argv[1:]:
             globals()[f"gen_{name}"]()
         sys.exit(0)
+    gen_metrics()
     gen_interp()
     gen_admm()
     gen_edges()

@@ -334,3 +334,38 @@ def test_fused_heat_topk_matches_dense(cap, rng):
     assert np.array_equal(a0, a1) and np.array_equal(p0, p1) and np.array_equal(d0, d1)
     if cap is not None:
         assert fused.n_fallback == len(a1)
+
+
+def test_ssim_on_device_vs_reference():
+    """f3: glr_ssim (device, clip(x, 0, peak) vs ref) against the reference's
+    metrics.ssim values (tests/golden/metrics.npz) within 1e-10."""
+    import torch
+    from paper_2301_03047_b200 import _device as D, _native as N
+    g = load_golden("metrics")
+    ax = np.arange(11) - 5.0
+    taps = np.exp(-(ax ** 2) / (2.0 * 1.5 ** 2))
+    taps = np.ascontiguousarray(taps / taps.sum())
+    for i in range(int(g["n"])):
+        a, b = g[f"a{i}"], g[f"b{i}"]
+        h, w, c = a.shape
+        out = D.zeros((1,), torch.float64)
+        ws = D.empty((N.query("glr_ssim_workspace", h, w, c),), torch.uint8)
+        bd, ad = D.f64(b), D.f64(a)
+        N.call("glr_ssim", bd.data_ptr(), ad.data_ptr(), h, w, c, 1.0, 1,
+               taps.ctypes.data_as(N.C.POINTER(N.C.c_double)), 11, out.data_ptr(),
+               ws.data_ptr(), D.stream())
+        val = float(D.host(out)[0]) / (c * (h - 10) * (w - 10))
+        assert abs(val - float(g[f"ssim{i}"])) <= 1e-10, i
+
+
+def test_report_ssim_matches_host_formula():
+    """gap_solve with ref: per-iteration SSIM from the device equals the
+    oracle's SSIM of the reported iterate within 1e-10."""
+    g = load_golden("solves")
+    op = G.cacti_operator(g["masks0"])
+    cfg = G.SolverConfig(regularizer="glr", max_iters=3,
+                         match=G.MatchConfig(patch_size=4, group_size=8, max_corners=24,
+                                             exemplar_stride=4))
+    x, rep = G.gap_solve(op, g["y0"], cfg, ref=g["scene0"])
+    assert abs(rep.rows[-1]["ssim"] - O.ssim(g["scene0"], x, 1.0)) <= 1e-10
+    assert all(0.0 < r["ssim"] <= 1.0 for r in rep.rows)

@@ -141,3 +141,11 @@ def test_gap_solve_interp_init_matches_reference_run():
         assert np.array_equal(np.array(pos, dtype=np.int32), g[f"solve_positions_{j}"])
     np.testing.assert_allclose(x, g["solve_out"], atol=1e-10, rtol=0)
     np.testing.assert_allclose(ps, g["solve_psnr"], atol=1e-8)
+
+
+def test_ssim_psnr_vs_reference():
+    g = load_golden("metrics")
+    for i in range(int(g["n"])):
+        a, b = g[f"a{i}"], np.clip(g[f"b{i}"], 0, 1)
+        assert abs(O.ssim(a, b, 1.0) - float(g[f"ssim{i}"])) <= 1e-12
+        assert abs(O.psnr(a, b, 1.0) - float(g[f"psnr{i}"])) <= 1e-12

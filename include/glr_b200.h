@@ -145,6 +145,22 @@ int glr_topk(const uint16_t* heat_d, int n_max, const int32_t* n_dev_d, int oh, 
 int glr_gather(const double* x_d, int H, int W, int C, int P, const int32_t* positions_d, int G,
                int K, double* groups_d, void* stream);
 
+/* ---- (3b) block matching + pixel re-rank --------------------
+ * glr_block_match: glr/matching.py:256-283 (`block_match`, the "nlr-*"
+ * regularizers, solvers.py:154-164,199-200). For each of the n anchors the
+ * window rows/cols [max(0, a - window), min(H - P, a + window)] at `stride`,
+ * squared pixel distance to the anchor patch (numpy's pairwise order, bit
+ * identical), the K-1 nearest by (distance, row, col) after the anchor
+ * itself, anchor padding. positions_d (n, K, 2), padded_d (n).
+ * glr_rerank_pixel: glr/matching.py:243-249 (`MatchConfig.rerank_pixel`):
+ * in place, slot 0 kept, slots 1..K-1 ordered by (pixel L2 distance to the
+ * slot-0 patch, (row, col)).                                                */
+int glr_block_match(const double* x_d, int H, int W, int C, int P, const int32_t* anchors_d,
+                    int n, int window, int stride, int K, int32_t* positions_d,
+                    int32_t* padded_d, void* stream);
+int glr_rerank_pixel(const double* x_d, int H, int W, int C, int P, int32_t* positions_d, int n,
+                     int K, void* stream);
+
 /* ---- (4) WNNM: glr/lowrank.py:46-65 ------------------------------------------
  * Batched weighted singular-value shrinkage of G groups (K columns of m
  * rows each, column-major per group) via an fp64 Gram matrix, a one-sided

@@ -256,6 +256,56 @@ def match_positions(heat: np.ndarray, anchors, k: int, sep: int):
 
 
 # ---------------------------------------------------------------------------
+# f2 — matching.py:243-249 (rerank_pixel), matching.py:256-283 (block_match)
+
+def block_match(x, anchors, patch_size: int, group_size: int, bm_window: int = 20,
+                bm_stride: int = 1):
+    """matching.py:256-283 — local KNN by squared pixel distance: the anchor,
+    then the group_size-1 nearest window positions by (d, row, col), anchor
+    padding. d is numpy's 3-axis sum of the squared broadcast difference.
+    Returns (positions, pads)."""
+    x = np.asarray(x, dtype=np.float64)
+    h, w, c = x.shape
+    p = patch_size
+    # windows[r, c] = x[r:r+p, c:c+p, :] in (p, q, c) memory order
+    win = np.lib.stride_tricks.sliding_window_view(x, (p, p), axis=(0, 1))
+    out, pads = [], []
+    for r0, c0 in anchors:
+        r0, c0 = int(r0), int(c0)
+        rows = np.arange(max(0, r0 - bm_window), min(h - p, r0 + bm_window) + 1, bm_stride)
+        cols = np.arange(max(0, c0 - bm_window), min(w - p, c0 + bm_window) + 1, bm_stride)
+        diff = win[np.ix_(rows, cols)] - win[r0, c0]
+        dist = (diff * diff).sum(axis=(2, 3, 4)).ravel()
+        rr = np.repeat(rows, len(cols))
+        cc = np.tile(cols, len(rows))
+        keep = ~((rr == r0) & (cc == c0))
+        dist, rr, cc = dist[keep], rr[keep], cc[keep]
+        pick = np.lexsort((cc, rr, dist))[:group_size - 1]
+        pos = [(r0, c0)] + [(int(rr[i]), int(cc[i])) for i in pick]
+        pad = group_size - len(pos)
+        pos += [(r0, c0)] * pad
+        out.append(pos)
+        pads.append(max(pad, 0))
+    return out, pads
+
+
+def rerank_pixel(x, positions, patch_size: int):
+    """matching.py:243-249 — slot 0 kept, slots 1.. ordered by (pixel L2
+    distance to the anchor patch, (row, col)); the distance is numpy's sum
+    over axis 0 of the (m, K) squared differences (sequential over rows)."""
+    x = np.asarray(x, dtype=np.float64)
+    out = []
+    for pos in positions:
+        pos = [tuple(map(int, q)) for q in pos]
+        mat = gather_group(x, pos, patch_size)
+        diff = mat - mat[:, :1]
+        d = (diff * diff).sum(axis=0)
+        order = [0] + sorted(range(1, len(pos)), key=lambda j: (d[j], pos[j]))
+        out.append([pos[j] for j in order])
+    return out
+
+
+# ---------------------------------------------------------------------------
 # A7/A9/A10 — patches.py:43-70, lowrank.py:46-87
 
 def gather_group(img, positions, patch_size: int) -> np.ndarray:
@@ -470,8 +520,11 @@ def psnr(a, b, peak=1.0):
 def gap_solve(op: Operator, y, max_iters, patch_size=8, group_size=64, max_corners=512,
               exemplar_stride=6, edge_threshold=0.2, refresh=5, sigma0=0.10, sigma_min=0.003,
               peak=1.0, c_weight=2.0 * np.sqrt(2.0), eps=1e-16, min_separation=None,
-              clip=True, ref=None, trace=None, positions_override=None, init="adjoint"):
-    """solvers.py:284-308 with the "glr" regularizer (solvers.py:170-210).
+              clip=True, ref=None, trace=None, positions_override=None, init="adjoint",
+              regularizer="glr", bm_window=20, bm_stride=1, rerank=False):
+    """solvers.py:284-308 with the nonlocal regularizers (solvers.py:170-210):
+    "glr" (optionally with the pixel re-rank) and the block-matching
+    baselines (see _glr_match).
 
     ``clip=False`` is the documented policy for complex (re, im) images
     (DESIGN.md). ``trace`` (a list) receives per-refresh anchors
@@ -491,14 +544,9 @@ def gap_solve(op: Operator, y, max_iters, patch_size=8, group_size=64, max_corne
             if positions_override is not None:
                 anchors, positions = positions_override[refresh_no]
             else:
-                anchors = build_exemplars(x, p, max_corners, None, 0.01, exemplar_stride)
-                if anchors:
-                    gh, gv = sobel_gradients(x)
-                    maps = binarize_gradients(gh, gv, edge_threshold)
-                    heat = similarity_heatmap(maps, anchors, p)
-                    positions, _ = match_positions(heat, anchors, group_size, sep)
-                else:
-                    positions = []
+                anchors, positions = _glr_match(x, p, group_size, max_corners, exemplar_stride,
+                                                edge_threshold, sep, regularizer, bm_window,
+                                                bm_stride, rerank)
             if trace is not None:
                 trace.append((list(anchors), [list(q) for q in positions]))
             last = it
@@ -514,22 +562,39 @@ def gap_solve(op: Operator, y, max_iters, patch_size=8, group_size=64, max_corne
     return out, residuals, psnrs
 
 
-def _glr_match(x, p, group_size, max_corners, exemplar_stride, edge_threshold, sep):
-    """solvers.py:187-203 for the "glr" regularizer: (anchors, positions)."""
-    anchors = build_exemplars(x, p, max_corners, None, 0.01, exemplar_stride)
+def _glr_match(x, p, group_size, max_corners, exemplar_stride, edge_threshold, sep,
+               regularizer="glr", bm_window=20, bm_stride=1, rerank=False):
+    """solvers.py:154-167 + 187-203: (anchors, positions) of one refresh for
+    the "glr" regularizer (corners + grid at 3*stride, edge-overlap global
+    match, optional pixel re-rank) and the block-matching baselines
+    ("nlr-bm": grid at stride only, "nlr-corner-bm": corners only,
+    "nlr-corner-uniform-bm": corners + grid at 3*stride)."""
+    h, w = x.shape[:2]
+    if regularizer == "nlr-bm":
+        anchors, _ = select_exemplars([], (h, w), p, uniform_interval=exemplar_stride)
+    else:
+        corners = detect_corners(x, max_n=max_corners, nms_radius=-(-p // 2), quality=0.01)
+        interval = None if regularizer == "nlr-corner-bm" else 3 * exemplar_stride
+        anchors, _ = select_exemplars(corners, (h, w), p, uniform_interval=interval)
     if not anchors:
         return anchors, []
+    if regularizer != "glr":
+        positions, _ = block_match(x, anchors, p, group_size, bm_window, bm_stride)
+        return anchors, positions
     gh, gv = sobel_gradients(x)
     maps = binarize_gradients(gh, gv, edge_threshold)
     heat = similarity_heatmap(maps, anchors, p)
     positions, _ = match_positions(heat, anchors, group_size, sep)
+    if rerank:
+        positions = rerank_pixel(x, positions, p)
     return anchors, positions
 
 
 def admm_solve(op: Operator, y, max_iters, patch_size=8, group_size=64, max_corners=512,
                exemplar_stride=6, edge_threshold=0.2, refresh=5, sigma0=0.10, sigma_min=0.003,
                peak=1.0, rho=0.01, c_weight=2.0 * np.sqrt(2.0), eps=1e-16, min_separation=None,
-               clip=True, ref=None, trace=None, init="adjoint"):
+               clip=True, ref=None, trace=None, init="adjoint", regularizer="glr",
+               bm_window=20, bm_stride=1, rerank=False):
     """solvers.py:311-341 — scaled-form ADMM with the "glr" regularizer:
     m = z - u; x = clip(m + A^T((y - A m) / (rho + gram))); z = clip(R(x + u));
     u = u + x - z. Returns (x, residuals, psnrs)."""
@@ -550,7 +615,8 @@ def admm_solve(op: Operator, y, max_iters, patch_size=8, group_size=64, max_corn
         sigma = sigma_at(it, max_iters, sigma0, sigma_min, peak)
         if positions is None or it - last >= refresh:
             anchors, positions = _glr_match(v, p, group_size, max_corners, exemplar_stride,
-                                            edge_threshold, sep)
+                                            edge_threshold, sep, regularizer, bm_window,
+                                            bm_stride, rerank)
             if trace is not None:
                 trace.append((list(anchors), [list(q) for q in positions]))
             last = it

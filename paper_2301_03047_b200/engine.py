@@ -132,11 +132,18 @@ class GlrEngine:
 
     def __init__(self, shape, match, peak: float = 1.0, c_weight: float = 2.0 * np.sqrt(2.0),
                  eps: float = 1e-16, process_group=None, heat_budget_bytes: int = 24 << 30,
-                 low_memory_match: bool = False):
+                 low_memory_match: bool = False, regularizer: str = "glr"):
         t = D.torch()
         h, w, c = shape
         self.shape = (h, w, c)
         self.mc = match
+        if regularizer not in ("glr", "nlr-bm", "nlr-corner-bm", "nlr-corner-uniform-bm"):
+            raise ValueError(f"regularizer {regularizer!r} has no nonlocal match stage")
+        # solvers.py:154-167: exemplar sources per regularizer; "nlr-*" match
+        # by local block matching (matching.py:256-283) instead of the heat map
+        self.regularizer = regularizer
+        self.global_match = regularizer == "glr"
+        self.use_corners = regularizer != "nlr-bm"
         self.p = match.patch_size
         self.k = match.group_size
         if self.k > KMAX:
@@ -154,18 +161,21 @@ class GlrEngine:
             self.world = dist.get_world_size(process_group)
         p = self.p
         self.oh, self.ow = h - p + 1, w - p + 1
-        self.grid_interval = 3 * match.exemplar_stride
+        self.grid_interval = {"nlr-bm": match.exemplar_stride, "nlr-corner-bm": 0}.get(
+            regularizer, 3 * match.exemplar_stride)
         g = self.grid_interval
-        self.max_anchors = match.max_corners + ((h - p) // g + 1) * ((w - p) // g + 1)
+        n_grid = ((h - p) // g + 1) * ((w - p) // g + 1) if g > 0 else 0
+        self.max_anchors = (match.max_corners if self.use_corners else 0) + n_grid
         self.expand = N.query("glr_heat_expand_factor", c, p)
         self.max_score = 4 * c * p * p
         self.stride = N.query("glr_heat_stride", h, w, p)
         # buffers
         self.resp = D.empty((h, w), t.float64)
-        self.gh = D.empty((h, w, c), t.float64)
-        self.gv = D.empty((h, w, c), t.float64)
-        self.stack = D.empty((h * w * 2 * c * self.expand,), t.uint8)  # packed fp4
-        self.corners = D.empty((match.max_corners, 2), t.int32)
+        if self.global_match:
+            self.gh = D.empty((h, w, c), t.float64)
+            self.gv = D.empty((h, w, c), t.float64)
+            self.stack = D.empty((h * w * 2 * c * self.expand,), t.uint8)  # packed fp4
+        self.corners = D.empty((max(match.max_corners, 1), 2), t.int32)
         self.n_corners = D.zeros((1,), t.int32)
         self.anchors = D.empty((self.max_anchors, 2), t.int32)
         self.tags = D.empty((self.max_anchors,), t.uint8)
@@ -194,7 +204,9 @@ class GlrEngine:
         self.heat = None
         self.ws_dense = None
         self.n_fallback = 0     # exemplars that took the dense path (last refresh)
-        if self.low_memory_match:
+        if not self.global_match:
+            pass
+        elif self.low_memory_match:
             self.cand_cap = int(min(1 << 17, self.oh * self.ow))
             per = 8 * self.cand_cap + N.query("glr_heat_topk_workspace", c, p, 1, 0)
             self.heat_chunk = max(1, min(self.max_anchors, heat_budget_bytes // per))
@@ -248,15 +260,18 @@ class GlrEngine:
         h, w, c = self.shape
         mc = self.mc
         s = D.stream()
-        e = self._ev()
-        N.call("glr_corner_response", x_d.data_ptr(), h, w, c, self.resp.data_ptr(),
-               self.ws_corner.data_ptr(), s)
-        self._log(("corner_response", 1), e)
-        e = self._ev()
-        N.call("glr_corners", self.resp.data_ptr(), h, w, mc.max_corners, mc.nms,
-               float(mc.corner_quality), self.corners.data_ptr(), self.n_corners.data_ptr(),
-               self.ws_nms.data_ptr(), self.ws_nms.numel(), s)
-        self._log(("corners_nms", 1), e)
+        if self.use_corners:
+            e = self._ev()
+            N.call("glr_corner_response", x_d.data_ptr(), h, w, c, self.resp.data_ptr(),
+                   self.ws_corner.data_ptr(), s)
+            self._log(("corner_response", 1), e)
+            e = self._ev()
+            N.call("glr_corners", self.resp.data_ptr(), h, w, mc.max_corners, mc.nms,
+                   float(mc.corner_quality), self.corners.data_ptr(), self.n_corners.data_ptr(),
+                   self.ws_nms.data_ptr(), self.ws_nms.numel(), s)
+            self._log(("corners_nms", 1), e)
+        else:
+            self.n_corners.zero_()
         old_anchors, old_n, old_lo, old_hi = self.anchors, self.n, self.lo, self.hi
         self._acur ^= 1
         self.anchors = self._anc[self._acur]
@@ -276,13 +291,28 @@ class GlrEngine:
         self.positions = self._pos[self._pcur]
         if n == 0:
             return 0
-        e = self._ev()
-        N.call("glr_sobel", x_d.data_ptr(), h, w, c, self.gh.data_ptr(), self.gv.data_ptr(), s)
-        N.call("glr_edge_stack", self.gh.data_ptr(), self.gv.data_ptr(), h, w, c,
-               float(mc.edge_threshold), 1, self.expand, None, self.stack.data_ptr(),
-               self.ws_edge.data_ptr(), s)
-        self._log(("edge_stack", 1), e)
-        self.match_shard()
+        if self.global_match:
+            e = self._ev()
+            N.call("glr_sobel", x_d.data_ptr(), h, w, c, self.gh.data_ptr(), self.gv.data_ptr(),
+                   s)
+            N.call("glr_edge_stack", self.gh.data_ptr(), self.gv.data_ptr(), h, w, c,
+                   float(mc.edge_threshold), 1, self.expand, None, self.stack.data_ptr(),
+                   self.ws_edge.data_ptr(), s)
+            self._log(("edge_stack", 1), e)
+            self.match_shard()
+            if mc.rerank_pixel and self.hi > self.lo:
+                e = self._ev()
+                N.call("glr_rerank_pixel", x_d.data_ptr(), h, w, c, self.p,
+                       self.positions[self.lo:self.hi].data_ptr(), self.hi - self.lo, self.k, s)
+                self._log(("rerank", self.hi - self.lo), e)
+        elif self.hi > self.lo:
+            e = self._ev()
+            N.call("glr_block_match", x_d.data_ptr(), h, w, c, self.p,
+                   self.anchors[self.lo:self.hi].data_ptr(), self.hi - self.lo,
+                   int(mc.bm_window), int(mc.bm_stride), self.k,
+                   self.positions[self.lo:self.hi].data_ptr(),
+                   self.padded[self.lo:self.hi].data_ptr(), s)
+            self._log(("block_match", self.hi - self.lo), e)
         if carry:
             # groups keeping their anchor start from their old eigenvectors,
             # coordinates re-indexed to the refreshed positions

@@ -167,8 +167,6 @@ def global_match(x: np.ndarray, exemplars: ExemplarSet, cfg: MatchConfig,
                  edge: EdgeMaps) -> list[PatchGroup]:
     """matching.py:234-253 — per exemplar, the top-K structurally similar
     patches by edge overlap; patches gathered from ``x``."""
-    if cfg.rerank_pixel:
-        raise NotImplementedError("rerank_pixel is the pixel-L2 'next' row (SURVEY §8f f2)")
     x = np.asarray(x, dtype=np.float64)
     maps = _maps_array(edge)
     _, h, w, c = maps.shape
@@ -184,10 +182,21 @@ def global_match(x: np.ndarray, exemplars: ExemplarSet, cfg: MatchConfig,
     heat = heat_device(D.to_dev(maps), h, w, c, p, anchors_d, n)
     oh, ow = h - p + 1, w - p + 1
     pos, pad = topk_device(heat, n, oh, ow, 4 * c * p * p, anchors_d, k, cfg.sep)
-    xh, xw, xc = x.shape
+    x_d = D.f64(x)
+    if cfg.rerank_pixel:
+        xh, xw, xc = x.shape
+        N.call("glr_rerank_pixel", x_d.data_ptr(), xh, xw, xc, p, pos.data_ptr(), n, k,
+               D.stream())
+    return _gather_groups(x_d, x.shape, p, pos, pad)
+
+
+def _gather_groups(x_d, shape, p, pos, pad) -> list[PatchGroup]:
+    """Device gather of every group's (m, K) matrix (patches.py:43-54)."""
+    xh, xw, xc = shape
+    n, k = pos.shape[0], pos.shape[1]
     m = p * p * xc
     groups_d = D.empty((n, k, m), D.torch().float64)
-    N.call("glr_gather", D.f64(x).data_ptr(), xh, xw, xc, p, pos.data_ptr(), n, k,
+    N.call("glr_gather", x_d.data_ptr(), xh, xw, xc, p, pos.data_ptr(), n, k,
            groups_d.data_ptr(), D.stream())
     pos_h = D.host(pos)
     pad_h = D.host(pad)
@@ -207,6 +216,36 @@ def xcorr2_valid_batch(x, kernels, backend: str = "im2col"):
     raise NotImplementedError("xcorr2_valid_batch is outside the B200 hot path (DESIGN.md)")
 
 
-def block_match(x, exemplars, cfg):
-    """matching.py:256-283 — local block-matching baseline."""
-    raise NotImplementedError("block_match is the 'next' row f2, not yet on B200 (DESIGN.md)")
+def block_match_device(x_d, shape, p, anchors_d, n, cfg: MatchConfig, positions_d=None,
+                       padded_d=None):
+    """glr_block_match over n device anchors: (positions (n, K, 2), padded (n,))."""
+    t = D.torch()
+    h, w, c = shape
+    k = cfg.group_size
+    pos = positions_d if positions_d is not None else D.empty((n, k, 2), t.int32)
+    pad = padded_d if padded_d is not None else D.empty((n,), t.int32)
+    N.call("glr_block_match", x_d.data_ptr(), h, w, c, p, anchors_d.data_ptr(), n,
+           int(cfg.bm_window), int(cfg.bm_stride), k, pos.data_ptr(), pad.data_ptr(), D.stream())
+    return pos, pad
+
+
+def block_match(x: np.ndarray, exemplars: ExemplarSet, cfg: MatchConfig) -> list[PatchGroup]:
+    """matching.py:256-283 — classic local KNN block matching by squared pixel
+    distance: the anchor, then the group_size-1 nearest window positions
+    (ties row-major), anchor padding; one CTA per exemplar on device."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.ndim != 3:
+        raise ValueError(f"image must be (H, W, C), got shape {x.shape}")
+    h, w, c = x.shape
+    p = cfg.patch_size
+    if p > h or p > w:
+        raise ValueError(f"patch size {p} exceeds image {h}x{w}")
+    anchors = [tuple(map(int, a)) for a in exemplars.anchors]
+    for i, a in enumerate(anchors):
+        _check_anchor(h, w, p, a, i)
+    n = len(anchors)
+    if n == 0:
+        return []
+    x_d = D.f64(x)
+    pos, pad = block_match_device(x_d, x.shape, p, D.i32(np.array(anchors)), n, cfg)
+    return _gather_groups(x_d, x.shape, p, pos, pad)

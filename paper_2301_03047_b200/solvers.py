@@ -115,10 +115,11 @@ class MatchState:
 
 
 def _require_glr(cfg: SolverConfig) -> None:
-    if cfg.regularizer != "glr":
+    """The nonlocal regularizers run on device: "glr" (global matching) and
+    the block-matching baselines "nlr-*"."""
+    if cfg.regularizer == "tv":
         raise NotImplementedError(
-            f"regularizer {cfg.regularizer!r} is a baseline outside the B200 hot path "
-            "(SURVEY §8f); only 'glr' runs on device")
+            "regularizer 'tv' is a baseline outside the B200 hot path (SURVEY §8f)")
 
 
 def _expected_y_shape(op) -> tuple:
@@ -160,8 +161,9 @@ def regularize_dispatch(x: np.ndarray, cfg: SolverConfig, state: MatchState,
     sigma = cfg.sigma_at(iteration) if sigma is None else sigma
     WnnmParams(c_weight=cfg.wnnm.c_weight, eps=cfg.wnnm.eps, noise_sigma=sigma)
     eng = state.engine
-    if eng is None or eng.shape != x.shape:
-        eng = GlrEngine(x.shape, cfg.match, cfg.peak, cfg.wnnm.c_weight, cfg.wnnm.eps)
+    if eng is None or eng.shape != x.shape or eng.regularizer != cfg.regularizer:
+        eng = GlrEngine(x.shape, cfg.match, cfg.peak, cfg.wnnm.c_weight, cfg.wnnm.eps,
+                        regularizer=cfg.regularizer)
         state.engine = eng
     x_d = D.f64(x)
     refresh = (state.positions is None
@@ -199,7 +201,7 @@ class GapRunner:
         self.cfg = cfg
         self.dop = DeviceOperator(op)
         self.eng = GlrEngine(op.x_shape, cfg.match, cfg.peak, cfg.wnnm.c_weight, cfg.wnnm.eps,
-                             process_group=process_group)
+                             process_group=process_group, regularizer=cfg.regularizer)
         self.xa = D.empty(self.dop.shape, t.float64)
         self.xb = D.empty(self.dop.shape, t.float64)
         self.resid_sq = D.zeros((cfg.max_iters,), t.float64)
@@ -423,7 +425,7 @@ class AdmmRunner(GapRunner):
 
 
 def admm_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = None,
-               process_group=None):
+               process_group=None, trace=None):
     """solvers.py:311-341 — scaled-form ADMM; the x-update uses the Woodbury
     identity through the measurement-domain diagonal (divisor rho + gram)."""
     _require_glr(cfg)
@@ -440,7 +442,7 @@ def admm_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = No
         if ref_d is not None:
             runner.record_metrics(x, ref_d, it)
 
-    x = runner.run(y_d, on_iter=on_iter, events=True)
+    x = runner.run(y_d, trace=trace, on_iter=on_iter, events=True)
     t.cuda.synchronize()
     res = np.sqrt(D.host(runner.resid_sq)).tolist()
     sqh = D.host(runner.sq) if ref_d is not None else None

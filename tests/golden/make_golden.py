@@ -312,11 +312,108 @@ def gen_interp():
     np.savez_compressed(OUT / "interp.npz", **cases)
 
 
+def gen_bm():
+    """Block matching (matching.py:256-283), the pixel re-rank of global
+    matching (matching.py:243-249) and small solves with the block-matching
+    regularizers and glr+rerank (positions captured from the reference)."""
+    rng = np.random.default_rng(808)
+    cases = {}
+    bm_runs = [  # (h, w, c, P, K, window, stride, quantise)
+        (24, 20, 1, 4, 8, 5, 1, 0), (32, 32, 3, 6, 16, 8, 1, 0), (40, 36, 8, 8, 32, 20, 1, 0),
+        (30, 30, 2, 5, 12, 7, 2, 0), (12, 12, 1, 4, 64, 20, 1, 0), (28, 26, 3, 4, 10, 6, 1, 4),
+        (20, 24, 1, 4, 6, 9, 3, 2), (26, 26, 16, 8, 9, 8, 1, 0),
+    ]
+    for i, (h, w, c, p, k, win, st, q) in enumerate(bm_runs):
+        x = blob_texture(rng, h, w, c) if q == 0 else f32(np.floor(rng.random((h, w, c)) * q) / q)
+        anchors = [(int(rng.integers(0, h - p + 1)), int(rng.integers(0, w - p + 1)))
+                   for _ in range(6)] + [(0, 0), (h - p, w - p)]
+        ex = ExemplarSet(anchors=anchors, tags=["uniform"] * len(anchors), patch_size=p)
+        cfg = glr.MatchConfig(patch_size=p, group_size=k, bm_window=max(win, p), bm_stride=st,
+                              mode="bm-uniform")
+        groups = glr.block_match(x, ex, cfg)
+        cases.update({f"bm_x{i}": x, f"bm_anchors{i}": np.array(anchors, dtype=np.int32),
+                      f"bm_cfg{i}": np.array([p, k, max(win, p), st]),
+                      f"bm_pos{i}": np.array([g.positions for g in groups], dtype=np.int32),
+                      f"bm_pad{i}": np.array([g.padded for g in groups], dtype=np.int32)})
+    cases["bm_n"] = np.array(len(bm_runs))
+    rr_runs = [(32, 28, 3, 4, 12), (40, 40, 8, 8, 16), (24, 24, 1, 6, 64)]
+    for i, (h, w, c, p, k) in enumerate(rr_runs):
+        x = blob_texture(rng, h, w, c)
+        gh, gv = glr.sobel_gradients(x)
+        edge = glr.binarize_gradients(gh, gv, 0.2)
+        anchors = [(int(rng.integers(0, h - p + 1)), int(rng.integers(0, w - p + 1)))
+                   for _ in range(10)]
+        ex = ExemplarSet(anchors=anchors, tags=["corner"] * 10, patch_size=p)
+        plain = glr.global_match(x, ex, glr.MatchConfig(patch_size=p, group_size=k), edge)
+        rer = glr.global_match(x, ex, glr.MatchConfig(patch_size=p, group_size=k,
+                                                      rerank_pixel=True), edge)
+        cases.update({f"rr_x{i}": x, f"rr_anchors{i}": np.array(anchors, dtype=np.int32),
+                      f"rr_cfg{i}": np.array([p, k]),
+                      f"rr_plain{i}": np.array([g.positions for g in plain], dtype=np.int32),
+                      f"rr_pos{i}": np.array([g.positions for g in rer], dtype=np.int32)})
+    cases["rr_n"] = np.array(len(rr_runs))
+
+    captured = []
+    orig_gm, orig_bm = ref_solvers.global_match, ref_solvers.block_match
+
+    def spy_gm(x, exemplars, cfg, edge):
+        groups = orig_gm(x, exemplars, cfg, edge)
+        captured.append((list(exemplars.anchors), [g.positions for g in groups]))
+        return groups
+
+    def spy_bm(x, exemplars, cfg):
+        groups = orig_bm(x, exemplars, cfg)
+        captured.append((list(exemplars.anchors), [g.positions for g in groups]))
+        return groups
+
+    ref_solvers.global_match, ref_solvers.block_match = spy_gm, spy_bm
+    try:
+        runs = [  # (regularizer, rerank, algorithm, match kwargs, iters)
+            ("nlr-bm", False, "gap", dict(patch_size=4, group_size=8, exemplar_stride=5,
+                                          bm_window=6), 7),
+            ("nlr-corner-bm", False, "gap", dict(patch_size=4, group_size=8, max_corners=24,
+                                                 bm_window=8), 6),
+            ("nlr-corner-uniform-bm", False, "gap", dict(patch_size=4, group_size=8,
+                                                         max_corners=20, exemplar_stride=4,
+                                                         bm_window=5, bm_stride=2), 6),
+            ("glr", True, "gap", dict(patch_size=4, group_size=8, max_corners=24,
+                                      exemplar_stride=4, rerank_pixel=True), 6),
+            ("nlr-bm", False, "admm", dict(patch_size=4, group_size=8, exemplar_stride=6,
+                                           bm_window=6), 6),
+        ]
+        for i, (reg, rer, alg, mc, iters) in enumerate(runs):
+            h, w, c = 32, 36, 4
+            scene = blob_texture(rng, h, w, c)
+            masks = glr.bernoulli_masks(h, w, c, seed=30 + i)
+            op = glr.cacti_operator(masks)
+            y = op.forward(scene)
+            cfg = glr.SolverConfig(regularizer=reg, algorithm=alg, max_iters=iters,
+                                   match=glr.MatchConfig(**mc), admm_rho=0.01)
+            captured.clear()
+            solve = glr.gap_solve if alg == "gap" else glr.admm_solve
+            xr, rep = solve(op, y, cfg, ref=scene)
+            cases.update({
+                f"sv_reg{i}": np.array(reg), f"sv_alg{i}": np.array(alg),
+                f"sv_mc{i}": np.array(repr(mc)), f"sv_iters{i}": np.array(iters),
+                f"sv_scene{i}": scene, f"sv_masks{i}": masks, f"sv_y{i}": y, f"sv_out{i}": xr,
+                f"sv_resid{i}": np.array([r["residual"] for r in rep.rows]),
+                f"sv_psnr{i}": np.array([r["psnr_db"] for r in rep.rows]),
+                f"sv_nref{i}": np.array(len(captured))})
+            for j, (anc, pos) in enumerate(captured):
+                cases[f"sv_anchors{i}_{j}"] = np.array(anc, dtype=np.int32)
+                cases[f"sv_positions{i}_{j}"] = np.array(pos, dtype=np.int32)
+        cases["sv_n"] = np.array(len(runs))
+    finally:
+        ref_solvers.global_match, ref_solvers.block_match = orig_gm, orig_bm
+    np.savez_compressed(OUT / "bm.npz", **cases)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
             globals()[f"gen_{name}"]()
         sys.exit(0)
+    gen_bm()
     gen_metrics()
     gen_interp()
     gen_admm()

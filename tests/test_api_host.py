@@ -119,6 +119,25 @@ def test_validation_before_launch():
         G.top_k_positions(np.full((4, 4), 0.5), (0, 0), 3, 1)
     with pytest.raises(NotImplementedError):
         G.gap_solve(op, np.zeros((8, 8, 1)), G.SolverConfig(regularizer="tv"))
+    bmc = G.MatchConfig(patch_size=4, group_size=4, bm_window=4, mode="bm-uniform")
+    ex = G.ExemplarSet(anchors=[(0, 0), (5, 0)], tags=["uniform"] * 2, patch_size=4)
+    with pytest.raises(ValueError, match="anchor 1"):
+        G.block_match(np.zeros((8, 8, 1)), ex, bmc)
+    with pytest.raises(ValueError, match="bm_window"):
+        G.MatchConfig(patch_size=8, bm_window=4, mode="bm-corner")
+
+
+def test_block_match_has_no_cpu_fallback():
+    """Valid block-matching input without a device: the native path raises,
+    nothing computes on the host."""
+    from paper_2301_03047_b200 import _native as N
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    bmc = G.MatchConfig(patch_size=4, group_size=4, bm_window=4, mode="bm-uniform")
+    ex = G.ExemplarSet(anchors=[(0, 0)], tags=["uniform"], patch_size=4)
+    with pytest.raises(N.NativeUnavailable):
+        G.block_match(np.zeros((8, 8, 1)), ex, bmc)
 
 
 def test_report_serialization():

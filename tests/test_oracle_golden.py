@@ -149,3 +149,49 @@ def test_ssim_psnr_vs_reference():
         a, b = g[f"a{i}"], np.clip(g[f"b{i}"], 0, 1)
         assert abs(O.ssim(a, b, 1.0) - float(g[f"ssim{i}"])) <= 1e-12
         assert abs(O.psnr(a, b, 1.0) - float(g[f"psnr{i}"])) <= 1e-12
+
+
+def test_block_match_bitwise():
+    g = load_golden("bm")
+    for i in range(int(g["bm_n"])):
+        p, k, win, st = (int(v) for v in g[f"bm_cfg{i}"])
+        pos, pads = O.block_match(g[f"bm_x{i}"], g[f"bm_anchors{i}"], p, k, win, st)
+        assert np.array_equal(np.array(pos, dtype=np.int32), g[f"bm_pos{i}"]), i
+        assert np.array_equal(np.array(pads, dtype=np.int32), g[f"bm_pad{i}"]), i
+
+
+def test_rerank_pixel_bitwise():
+    g = load_golden("bm")
+    for i in range(int(g["rr_n"])):
+        p, k = (int(v) for v in g[f"rr_cfg{i}"])
+        out = O.rerank_pixel(g[f"rr_x{i}"], g[f"rr_plain{i}"], p)
+        assert np.array_equal(np.array(out, dtype=np.int32), g[f"rr_pos{i}"]), i
+
+
+def _bm_solve_kwargs(g, i):
+    import ast
+    mc = ast.literal_eval(str(g[f"sv_mc{i}"]))
+    kw = dict(patch_size=mc["patch_size"], group_size=mc["group_size"],
+              max_corners=mc.get("max_corners", 512), exemplar_stride=mc.get("exemplar_stride", 6),
+              bm_window=mc.get("bm_window", 20), bm_stride=mc.get("bm_stride", 1),
+              rerank=mc.get("rerank_pixel", False), regularizer=str(g[f"sv_reg{i}"]))
+    return kw
+
+
+@pytest.mark.parametrize("i", range(5))
+def test_bm_solves_match_reference_run(i):
+    g = load_golden("bm")
+    kw = _bm_solve_kwargs(g, i)
+    op = O.Operator("cacti", masks=g[f"sv_masks{i}"])
+    solve = O.gap_solve if str(g[f"sv_alg{i}"]) == "gap" else O.admm_solve
+    extra = {} if str(g[f"sv_alg{i}"]) == "gap" else {"rho": 0.01}
+    trace = []
+    x, res, ps = solve(op, g[f"sv_y{i}"], int(g[f"sv_iters{i}"]), ref=g[f"sv_scene{i}"],
+                       trace=trace, **kw, **extra)
+    assert len(trace) == int(g[f"sv_nref{i}"])
+    for j, (anc, pos) in enumerate(trace):
+        assert np.array_equal(np.array(anc, dtype=np.int32), g[f"sv_anchors{i}_{j}"])
+        assert np.array_equal(np.array(pos, dtype=np.int32), g[f"sv_positions{i}_{j}"])
+    np.testing.assert_allclose(x, g[f"sv_out{i}"], atol=1e-10, rtol=0)
+    np.testing.assert_allclose(res, g[f"sv_resid{i}"], rtol=1e-9)
+    np.testing.assert_allclose(ps, g[f"sv_psnr{i}"], atol=1e-8)

@@ -408,12 +408,37 @@ def gen_bm():
     np.savez_compressed(OUT / "bm.npz", **cases)
 
 
+def gen_tens():
+    """.tens files written by the reference (tensorio.py:47-56), kept as raw
+    bytes, and a run config serialized by the reference (config.py:123-126)."""
+    import tempfile
+    from glr import tensorio, config
+    rng = np.random.default_rng(909)
+    arrays = [rng.random((5, 4, 3)), rng.random((7,)).astype(np.float32),
+              (rng.random((3, 3)) * 255).astype(np.uint8),
+              rng.random((2, 3)) + 1j * rng.random((2, 3)), np.float64(2.5) * np.ones(())]
+    cases = {"n": np.array(len(arrays))}
+    with tempfile.TemporaryDirectory() as d:
+        for i, a in enumerate(arrays):
+            path = f"{d}/t{i}.tens"
+            tensorio.write_tensor(path, a)
+            cases[f"bytes{i}"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+            cases[f"arr{i}"] = a
+            cases[f"read{i}"] = tensorio.read_tensor(path)
+    run = config.parse_run_config({"solver": {"max_iters": 7, "regularizer": "nlr-bm",
+                                              "match": {"patch_size": 6, "bm_window": 9}},
+                                   "operator": {"kind": "msfa", "channels": 4}})
+    cases["config_json"] = np.array(config.serialize_run_config(run))
+    np.savez_compressed(OUT / "tens.npz", **cases)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
             globals()[f"gen_{name}"]()
         sys.exit(0)
     gen_bm()
+    gen_tens()
     gen_metrics()
     gen_interp()
     gen_admm()

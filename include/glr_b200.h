@@ -161,6 +161,15 @@ int glr_block_match(const double* x_d, int H, int W, int C, int P, const int32_t
 int glr_rerank_pixel(const double* x_d, int H, int W, int C, int P, int32_t* positions_d, int n,
                      int K, void* stream);
 
+/* ---- (3c) TV baseline regularizer: glr/solvers.py:101-139 -------------------
+ * glr_tv_denoise: anisotropic TV prox by `iters` dual projected-gradient
+ * steps (tau = 1/8) on every channel, bit-identical to the reference's numpy
+ * arithmetic; weight <= 0 copies x. out_d must not alias x_d; workspace
+ * glr_tv_workspace(H, W, C) bytes (the dual pair, double-buffered).       */
+size_t glr_tv_workspace(int H, int W, int C);
+int glr_tv_denoise(const double* x_d, int H, int W, int C, double weight, int iters,
+                   double* out_d, void* ws_d, size_t ws_bytes, void* stream);
+
 /* ---- (4) WNNM: glr/lowrank.py:46-65 ------------------------------------------
  * Batched weighted singular-value shrinkage of G groups (K columns of m
  * rows each, column-major per group) via an fp64 Gram matrix, a one-sided

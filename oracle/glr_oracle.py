@@ -305,6 +305,40 @@ def rerank_pixel(x, positions, patch_size: int):
     return out
 
 
+def tv_denoise(x, weight: float, iters: int = 20):
+    """solvers.py:101-139 — anisotropic TV prox per channel by dual projected
+    gradient (tau = 1/8): z = x - w div(p); p = clip(p - (tau/w) grad z)."""
+    x = np.asarray(x, dtype=np.float64)
+    if weight <= 0:
+        return x.copy()
+
+    def grad(z):
+        gh, gv = np.zeros_like(z), np.zeros_like(z)
+        gh[:, :-1] = z[:, 1:] - z[:, :-1]
+        gv[:-1, :] = z[1:, :] - z[:-1, :]
+        return gh, gv
+
+    def div(ph, pv):
+        d = np.empty_like(ph)
+        d[:, 0] = ph[:, 0]
+        d[:, 1:] = ph[:, 1:] - ph[:, :-1]
+        d[0, :] += pv[0, :]
+        d[1:, :] += pv[1:, :] - pv[:-1, :]
+        return d
+
+    out = np.empty_like(x)
+    step = 0.125 / weight
+    for ch in range(x.shape[2]):
+        xc = x[:, :, ch]
+        ph, pv = np.zeros_like(xc), np.zeros_like(xc)
+        for _ in range(iters):
+            gh, gv = grad(xc - weight * div(ph, pv))
+            ph = np.clip(ph - step * gh, -1.0, 1.0)
+            pv = np.clip(pv - step * gv, -1.0, 1.0)
+        out[:, :, ch] = xc - weight * div(ph, pv)
+    return out
+
+
 # ---------------------------------------------------------------------------
 # A7/A9/A10 — patches.py:43-70, lowrank.py:46-87
 
@@ -521,8 +555,9 @@ def gap_solve(op: Operator, y, max_iters, patch_size=8, group_size=64, max_corne
               exemplar_stride=6, edge_threshold=0.2, refresh=5, sigma0=0.10, sigma_min=0.003,
               peak=1.0, c_weight=2.0 * np.sqrt(2.0), eps=1e-16, min_separation=None,
               clip=True, ref=None, trace=None, positions_override=None, init="adjoint",
-              regularizer="glr", bm_window=20, bm_stride=1, rerank=False):
-    """solvers.py:284-308 with the nonlocal regularizers (solvers.py:170-210):
+              regularizer="glr", bm_window=20, bm_stride=1, rerank=False, tv_weight=0.05,
+              tv_iters=20):
+    """solvers.py:284-308 with the nonlocal regularizers or "tv" (solvers.py:170-210):
     "glr" (optionally with the pixel re-rank) and the block-matching
     baselines (see _glr_match).
 
@@ -540,7 +575,9 @@ def gap_solve(op: Operator, y, max_iters, patch_size=8, group_size=64, max_corne
     refresh_no = 0
     for it in range(max_iters):
         sigma = sigma_at(it, max_iters, sigma0, sigma_min, peak)
-        if positions is None or it - last >= refresh:
+        if regularizer == "tv":
+            positions = []
+        elif positions is None or it - last >= refresh:
             if positions_override is not None:
                 anchors, positions = positions_override[refresh_no]
             else:
@@ -551,7 +588,10 @@ def gap_solve(op: Operator, y, max_iters, patch_size=8, group_size=64, max_corne
                 trace.append((list(anchors), [list(q) for q in positions]))
             last = it
             refresh_no += 1
-        z = glr_regularize(x, positions, p, sigma, c_weight, eps) if positions else x.copy()
+        if regularizer == "tv":
+            z = tv_denoise(x, tv_weight, tv_iters)
+        else:
+            z = glr_regularize(x, positions, p, sigma, c_weight, eps) if positions else x.copy()
         x = z + op.adjoint(safe_div(y - op.forward(z), op.gram))
         if clip:
             x = np.clip(x, lo, hi)
@@ -594,7 +634,7 @@ def admm_solve(op: Operator, y, max_iters, patch_size=8, group_size=64, max_corn
                exemplar_stride=6, edge_threshold=0.2, refresh=5, sigma0=0.10, sigma_min=0.003,
                peak=1.0, rho=0.01, c_weight=2.0 * np.sqrt(2.0), eps=1e-16, min_separation=None,
                clip=True, ref=None, trace=None, init="adjoint", regularizer="glr",
-               bm_window=20, bm_stride=1, rerank=False):
+               bm_window=20, bm_stride=1, rerank=False, tv_weight=0.05, tv_iters=20):
     """solvers.py:311-341 — scaled-form ADMM with the "glr" regularizer:
     m = z - u; x = clip(m + A^T((y - A m) / (rho + gram))); z = clip(R(x + u));
     u = u + x - z. Returns (x, residuals, psnrs)."""
@@ -613,14 +653,19 @@ def admm_solve(op: Operator, y, max_iters, patch_size=8, group_size=64, max_corn
             x = np.clip(x, lo, hi)
         v = x + u
         sigma = sigma_at(it, max_iters, sigma0, sigma_min, peak)
-        if positions is None or it - last >= refresh:
+        if regularizer == "tv":
+            positions = []
+        elif positions is None or it - last >= refresh:
             anchors, positions = _glr_match(v, p, group_size, max_corners, exemplar_stride,
                                             edge_threshold, sep, regularizer, bm_window,
                                             bm_stride, rerank)
             if trace is not None:
                 trace.append((list(anchors), [list(q) for q in positions]))
             last = it
-        z = glr_regularize(v, positions, p, sigma, c_weight, eps) if positions else v.copy()
+        if regularizer == "tv":
+            z = tv_denoise(v, tv_weight, tv_iters)
+        else:
+            z = glr_regularize(v, positions, p, sigma, c_weight, eps) if positions else v.copy()
         if clip:
             z = np.clip(z, lo, hi)
         u = u + x - z

@@ -61,6 +61,8 @@ SIGNATURES: dict[str, tuple] = {
     "glr_gather": (i32, [vp, i32, i32, i32, i32, vp, i32, i32, vp, vp]),
     "glr_block_match": (i32, [vp, i32, i32, i32, i32, vp, i32, i32, i32, i32, vp, vp, vp]),
     "glr_rerank_pixel": (i32, [vp, i32, i32, i32, i32, vp, i32, i32, vp]),
+    "glr_tv_workspace": (sz, [i32, i32, i32]),
+    "glr_tv_denoise": (i32, [vp, i32, i32, i32, f64, i32, vp, vp, sz, vp]),
     "glr_wnnm_workspace": (sz, [i32, i32]),
     "glr_wnnm": (i32, [vp, i32, i32, i32, f64, f64, f64, f64, vp, vp, vp, sz, vp]),
     "glr_wnnm_scatter": (i32, [vp, i32, i32, i32, i32, vp, i32, vp, i32, f64, f64, f64, i32, vp,
@@ -160,6 +162,8 @@ def call(name: str, *args) -> int:
     check(st, name)
     if name == "glr_edge_stack":  # relative max pass + maps and/or stack
         launch_count += int(bool(args[6])) + int(args[8] is not None) + int(args[9] is not None)
+    elif name == "glr_tv_denoise":  # one launch per dual step + the output
+        launch_count += (int(args[5]) + 1) if args[4] > 0 else 0
     else:
         launch_count += KERNELS_PER_CALL.get(name, 0)
     return st

@@ -114,14 +114,6 @@ class MatchState:
     engine: object = None
 
 
-def _require_glr(cfg: SolverConfig) -> None:
-    """The nonlocal regularizers run on device: "glr" (global matching) and
-    the block-matching baselines "nlr-*"."""
-    if cfg.regularizer == "tv":
-        raise NotImplementedError(
-            "regularizer 'tv' is a baseline outside the B200 hot path (SURVEY §8f)")
-
-
 def _expected_y_shape(op) -> tuple:
     h, w = op.x_shape[:2]
     return (h, w) if op.kind == "fourier" else (h, w, 1)
@@ -155,9 +147,12 @@ def _init_device(dop: DeviceOperator, y_d, cfg: SolverConfig):
 
 def regularize_dispatch(x: np.ndarray, cfg: SolverConfig, state: MatchState,
                         iteration: int = 0, sigma: float | None = None) -> np.ndarray:
-    """solvers.py:170-210 — GLR regularizer with cached match positions."""
-    _require_glr(cfg)
+    """solvers.py:170-210 — nonlocal regularizer with cached match positions
+    ("glr" global matching, "nlr-*" block matching) or the TV prox."""
     x = np.asarray(x, dtype=np.float64)
+    if cfg.regularizer == "tv":
+        state.last_match_ms = 0.0
+        return tv_denoise(x, cfg.tv_weight, cfg.tv_iters)
     sigma = cfg.sigma_at(iteration) if sigma is None else sigma
     WnnmParams(c_weight=cfg.wnnm.c_weight, eps=cfg.wnnm.eps, noise_sigma=sigma)
     eng = state.engine
@@ -200,8 +195,16 @@ class GapRunner:
         t = D.torch()
         self.cfg = cfg
         self.dop = DeviceOperator(op)
-        self.eng = GlrEngine(op.x_shape, cfg.match, cfg.peak, cfg.wnnm.c_weight, cfg.wnnm.eps,
-                             process_group=process_group, regularizer=cfg.regularizer)
+        h, w, c = self.dop.shape
+        self.tv = None
+        if cfg.regularizer == "tv":
+            # TV prox on device (solvers.py:121-139); no matching, no engine
+            self.eng = _TvState(h, w)
+            self.tv = TvProx(self.dop.shape, cfg.tv_weight, cfg.tv_iters)
+        else:
+            self.eng = GlrEngine(op.x_shape, cfg.match, cfg.peak, cfg.wnnm.c_weight,
+                                 cfg.wnnm.eps, process_group=process_group,
+                                 regularizer=cfg.regularizer)
         self.xa = D.empty(self.dop.shape, t.float64)
         self.xb = D.empty(self.dop.shape, t.float64)
         self.resid_sq = D.zeros((cfg.max_iters,), t.float64)
@@ -258,7 +261,8 @@ class GapRunner:
             if ev:
                 ev[0].record()
             sigma = cfg.sigma_at(it)
-            if (not eng.has_positions) or it - last >= cfg.match_refresh_interval:
+            if self.tv is None and ((not eng.has_positions)
+                                    or it - last >= cfg.match_refresh_interval):
                 if positions_override is not None:
                     anc, pos = positions_override[refresh_no]
                     eng.set_positions(np.asarray(anc), np.asarray(pos))
@@ -271,11 +275,18 @@ class GapRunner:
                 refresh_no += 1
             if ev:
                 ev[1].record()
-            has = eng.regularize(x, sigma)
-            if ev:
-                ev[2].record()
-            dop.gap_update(eng.acc if has else None, eng.cnt if has else None, eng.frac, x, y_d,
-                           lo, hi, x_next, self.resid_sq[it:it + 1], eng.gap_ws)
+            if self.tv is not None:
+                z = self.tv(x)
+                if ev:
+                    ev[2].record()
+                dop.gap_update(None, None, 0, z, y_d, lo, hi, x_next, self.resid_sq[it:it + 1],
+                               eng.gap_ws)
+            else:
+                has = eng.regularize(x, sigma)
+                if ev:
+                    ev[2].record()
+                dop.gap_update(eng.acc if has else None, eng.cnt if has else None, eng.frac, x,
+                               y_d, lo, hi, x_next, self.resid_sq[it:it + 1], eng.gap_ws)
             if ev:
                 ev[3].record()
             x, x_next = x_next, x
@@ -313,7 +324,6 @@ def gap_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = Non
     across ranks; ``positions_override`` (list of (anchors, positions) per
     refresh) locks matching for positions-locked parity; ``trace`` (a list)
     receives (anchors, positions) of every refresh."""
-    _require_glr(cfg)
     y = np.asarray(y)
     _check_measurement(op, y)
     t = D.torch()
@@ -397,7 +407,8 @@ class AdmmRunner(GapRunner):
             if ev:
                 ev[1].record()
             self._lincomb(v, x, 1.0, u, 1.0)                                   # v = x + u
-            if (not eng.has_positions) or it - last >= cfg.match_refresh_interval:
+            if self.tv is None and ((not eng.has_positions)
+                                    or it - last >= cfg.match_refresh_interval):
                 if positions_override is not None:
                     anc, pos = positions_override[refresh_no]
                     eng.set_positions(np.asarray(anc), np.asarray(pos))
@@ -410,7 +421,9 @@ class AdmmRunner(GapRunner):
                 refresh_no += 1
             if ev:
                 ev[2].record()
-            if eng.regularize(v, cfg.sigma_at(it)):
+            if self.tv is not None:
+                self._lincomb(z, self.tv(v), 1.0, clip=clip)                   # z = clip(tv(v))
+            elif eng.regularize(v, cfg.sigma_at(it)):
                 N.call("glr_normalize", eng.acc.data_ptr(), eng.cnt.data_ptr(), v.data_ptr(),
                        h, w, c, eng.frac, z.data_ptr(), D.stream())
                 self._lincomb(z, z, 1.0, clip=clip)                            # z = clip(z)
@@ -428,7 +441,6 @@ def admm_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = No
                process_group=None, trace=None):
     """solvers.py:311-341 — scaled-form ADMM; the x-update uses the Woodbury
     identity through the measurement-domain diagonal (divisor rho + gram)."""
-    _require_glr(cfg)
     y = np.asarray(y)
     _check_measurement(op, y)
     t = D.torch()
@@ -472,6 +484,39 @@ def solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = None):
     return fn(op, y, cfg, ref)
 
 
-def tv_denoise(x, weight, iters=20):
-    """solvers.py:121-139 — TV baseline regularizer, outside the hot path."""
-    raise NotImplementedError("tv_denoise is a baseline outside the B200 hot path (DESIGN.md)")
+class _TvState:
+    """Stand-in for the match engine under the TV regularizer: no positions,
+    just the projection workspace."""
+
+    def __init__(self, h, w):
+        self.gap_ws = D.empty((N.query("glr_gap_workspace", h, w),), D.torch().uint8)
+        self.has_positions = False
+        self.frac = 0
+
+
+class TvProx:
+    """Device TV prox (glr_tv_denoise) with its output and dual workspaces."""
+
+    def __init__(self, shape, weight: float, iters: int):
+        t = D.torch()
+        h, w, c = shape
+        self.shape, self.weight, self.iters = (h, w, c), float(weight), int(iters)
+        self.out = D.empty((h, w, c), t.float64)
+        self.ws = D.empty((N.query("glr_tv_workspace", h, w, c),), t.uint8)
+
+    def __call__(self, x_d):
+        h, w, c = self.shape
+        N.call("glr_tv_denoise", x_d.data_ptr(), h, w, c, self.weight, self.iters,
+               self.out.data_ptr(), self.ws.data_ptr(), self.ws.numel(), D.stream())
+        return self.out
+
+
+def tv_denoise(x: np.ndarray, weight: float, iters: int = 20) -> np.ndarray:
+    """solvers.py:121-139 — proximal operator of anisotropic TV per channel,
+    dual projected gradient (tau = 1/8); bit-identical to the reference."""
+    x = np.asarray(x, dtype=np.float64)
+    if weight <= 0:
+        return x.copy()
+    if x.ndim != 3:
+        raise ValueError(f"image must be (H, W, C), got shape {x.shape}")
+    return D.host(TvProx(x.shape, weight, iters)(D.f64(x)))

@@ -432,12 +432,39 @@ def gen_tens():
     np.savez_compressed(OUT / "tens.npz", **cases)
 
 
+def gen_tv():
+    """tv_denoise (solvers.py:121-139) and GAP / ADMM solves with the TV
+    regularizer, run by the reference."""
+    rng = np.random.default_rng(1010)
+    cases = {}
+    tv_runs = [((20, 24, 1), 0.05, 20), ((17, 13, 3), 0.2, 7), ((9, 9, 2), 0.0, 5)]
+    for i, (shape, wgt, iters) in enumerate(tv_runs):
+        x = f32(rng.random(shape))
+        cases.update({f"tv_x{i}": x, f"tv_cfg{i}": np.array([wgt, iters]),
+                      f"tv_out{i}": ref_solvers.tv_denoise(x, wgt, iters)})
+    cases["tv_n"] = np.array(len(tv_runs))
+    for i, alg in enumerate(("gap", "admm")):
+        h, w, c = 32, 28, 4
+        scene = blob_texture(rng, h, w, c)
+        masks = glr.bernoulli_masks(h, w, c, seed=50 + i)
+        op = glr.cacti_operator(masks)
+        y = op.forward(scene)
+        cfg = glr.SolverConfig(regularizer="tv", algorithm=alg, max_iters=12, tv_weight=0.03,
+                               tv_iters=15, admm_rho=0.01)
+        xr, rep = ref_solvers.solve(op, y, cfg, ref=scene)
+        cases.update({f"sv_scene{i}": scene, f"sv_masks{i}": masks, f"sv_y{i}": y,
+                      f"sv_out{i}": xr, f"sv_resid{i}": np.array([r["residual"] for r in rep.rows]),
+                      f"sv_psnr{i}": np.array([r["psnr_db"] for r in rep.rows])})
+    np.savez_compressed(OUT / "tv.npz", **cases)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
             globals()[f"gen_{name}"]()
         sys.exit(0)
     gen_bm()
+    gen_tv()
     gen_tens()
     gen_metrics()
     gen_interp()

@@ -118,7 +118,7 @@ def test_validation_before_launch():
     with pytest.raises(ValueError, match="integer overlap counts"):
         G.top_k_positions(np.full((4, 4), 0.5), (0, 0), 3, 1)
     with pytest.raises(NotImplementedError):
-        G.gap_solve(op, np.zeros((8, 8, 1)), G.SolverConfig(regularizer="tv"))
+        G.xcorr2_valid_batch(np.zeros((8, 8, 1)), np.zeros((2, 2, 1)))
     bmc = G.MatchConfig(patch_size=4, group_size=4, bm_window=4, mode="bm-uniform")
     ex = G.ExemplarSet(anchors=[(0, 0), (5, 0)], tags=["uniform"] * 2, patch_size=4)
     with pytest.raises(ValueError, match="anchor 1"):

@@ -195,3 +195,24 @@ def test_bm_solves_match_reference_run(i):
     np.testing.assert_allclose(x, g[f"sv_out{i}"], atol=1e-10, rtol=0)
     np.testing.assert_allclose(res, g[f"sv_resid{i}"], rtol=1e-9)
     np.testing.assert_allclose(ps, g[f"sv_psnr{i}"], atol=1e-8)
+
+
+def test_tv_denoise_bitwise():
+    g = load_golden("tv")
+    for i in range(int(g["tv_n"])):
+        wgt, iters = g[f"tv_cfg{i}"]
+        assert np.array_equal(O.tv_denoise(g[f"tv_x{i}"], float(wgt), int(iters)),
+                              g[f"tv_out{i}"]), i
+
+
+@pytest.mark.parametrize("i,alg", [(0, "gap"), (1, "admm")])
+def test_tv_solves_match_reference_run(i, alg):
+    g = load_golden("tv")
+    op = O.Operator("cacti", masks=g[f"sv_masks{i}"])
+    solve = O.gap_solve if alg == "gap" else O.admm_solve
+    extra = {} if alg == "gap" else {"rho": 0.01}
+    x, res, ps = solve(op, g[f"sv_y{i}"], 12, regularizer="tv", tv_weight=0.03, tv_iters=15,
+                       ref=g[f"sv_scene{i}"], **extra)
+    np.testing.assert_allclose(x, g[f"sv_out{i}"], atol=1e-12, rtol=0)
+    np.testing.assert_allclose(res, g[f"sv_resid{i}"], rtol=1e-9)
+    np.testing.assert_allclose(ps, g[f"sv_psnr{i}"], atol=1e-9)

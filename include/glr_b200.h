@@ -158,6 +158,14 @@ int glr_gather(const double* x_d, int H, int W, int C, int P, const int32_t* pos
 int glr_block_match(const double* x_d, int H, int W, int C, int P, const int32_t* anchors_d,
                     int n, int window, int stride, int K, int32_t* positions_d,
                     int32_t* padded_d, void* stream);
+/* glr_xcorr_valid: matching.py:116-137 (`xcorr2_valid_batch`, any float
+ * input): out_d (H-P+1, W-P+1, N) fp64 valid cross-correlation of x_d
+ * (H,W,C) with N kernels k_d (N,P,P,C), channels summed, accumulated in
+ * (dr, dc, ch) order with rounded products (bit-identical to the reference
+ * tests' loop oracle; the reference's own backends agree with it exactly on
+ * binary inputs).                                                          */
+int glr_xcorr_valid(const double* x_d, int H, int W, int C, const double* k_d, int N, int P,
+                    double* out_d, void* stream);
 int glr_rerank_pixel(const double* x_d, int H, int W, int C, int P, int32_t* positions_d, int n,
                      int K, void* stream);
 

@@ -62,6 +62,7 @@ SIGNATURES: dict[str, tuple] = {
     "glr_block_match": (i32, [vp, i32, i32, i32, i32, vp, i32, i32, i32, i32, vp, vp, vp]),
     "glr_rerank_pixel": (i32, [vp, i32, i32, i32, i32, vp, i32, i32, vp]),
     "glr_tv_workspace": (sz, [i32, i32, i32]),
+    "glr_xcorr_valid": (i32, [vp, i32, i32, i32, vp, i32, i32, vp, vp]),
     "glr_tv_denoise": (i32, [vp, i32, i32, i32, f64, i32, vp, vp, sz, vp]),
     "glr_wnnm_workspace": (sz, [i32, i32]),
     "glr_wnnm": (i32, [vp, i32, i32, i32, f64, f64, f64, f64, vp, vp, vp, sz, vp]),
@@ -150,7 +151,7 @@ KERNELS_PER_CALL = {
     "glr_masksum_adjoint": 1, "glr_gap_masksum": 2, "glr_fourier_forward": 4,
     "glr_fourier_adjoint": 4, "glr_gap_fourier": 11, "glr_sq_err": 2, "glr_vcache_remap": 3,
     "glr_lincomb": 1, "glr_interp_msfa": 3, "glr_interp_cacti": 1, "glr_heat_topk": 4, "glr_ssim": 3,
-    "glr_block_match": 1, "glr_rerank_pixel": 1,
+    "glr_block_match": 1, "glr_rerank_pixel": 1, "glr_xcorr_valid": 1,
 }
 launch_count = 0
 

@@ -300,9 +300,52 @@ __global__ void rerank_kernel(const double* __restrict__ x, int H, int W, int C,
   }
 }
 
+// xcorr2_valid_batch (matching.py:116-137): out[u][v][n] = sum over (dr, dc,
+// ch) of k[n][dr][dc][ch] * x[u+dr][v+dc][ch], accumulated from 0 in that
+// order with the product rounded first (the kernel-index loop oracle of the
+// reference's tests, bit for bit). One thread per output position, the
+// kernel in shared memory (warp-uniform broadcast reads).
+__global__ void xcorr_kernel(const double* __restrict__ x, int H, int W, int C,
+                             const double* __restrict__ k, int N, int P,
+                             double* __restrict__ out) {
+  extern __shared__ __align__(16) double ks[];
+  const int n = blockIdx.y;
+  const int m = P * P * C;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) ks[i] = k[(int64_t)n * m + i];
+  __syncthreads();
+  const int oh = H - P + 1, ow = W - P + 1;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)oh * ow;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int u = (int)(t / ow), v = (int)(t % ow);
+    double acc = 0.0;
+    int i = 0;
+    for (int dr = 0; dr < P; ++dr) {
+      const double* row = x + ((int64_t)(u + dr) * W + v) * C;
+      for (int e = 0; e < P * C; ++e, ++i) acc = __dadd_rn(acc, __dmul_rn(ks[i], row[e]));
+    }
+    out[t * N + n] = acc;
+  }
+}
+
 }  // namespace glr
 
 using namespace glr;
+
+extern "C" int glr_xcorr_valid(const double* x_d, int H, int W, int C, const double* k_d, int N,
+                               int P, double* out_d, void* stream) {
+  GLR_REQUIRE(P >= 1 && P <= H && P <= W, GLR_ERR_INVALID, "kernel %dx%d larger than input %dx%d",
+              P, P, H, W);
+  GLR_REQUIRE(C >= 1 && N >= 0, GLR_ERR_INVALID, "xcorr: bad shape");
+  if (N == 0) return GLR_OK;
+  const size_t smem = (size_t)P * P * C * 8;
+  GLR_REQUIRE(smem <= 227 * 1024, GLR_ERR_UNSUPPORTED, "xcorr: kernel too large");
+  GLR_CUDA(cudaFuncSetAttribute(xcorr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  const int64_t M = (int64_t)(H - P + 1) * (W - P + 1);
+  dim3 grid((unsigned)std::min<int64_t>(cdiv(M, 256), 4 * kNumSMs), (unsigned)N);
+  xcorr_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(x_d, H, W, C, k_d, N, P, out_d);
+  return check_launch("xcorr_kernel");
+}
 
 extern "C" int glr_block_match(const double* x_d, int H, int W, int C, int P,
                                const int32_t* anchors_d, int n, int window, int stride, int K,

@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(wn::GRAM_THREADS) gram_kernel(GroupSrc s, int 
   if (tid < KMAX) cbase[tid] = tid < s.K ? col_base<IMG>(s, g, tid) : 0;
   __syncthreads();
   const int SI = warp == 2 ? 1 : 0, SJ = warp == 0 ? 0 : 1;
+  const bool diag = SI == SJ;
   const int ar = lane >> 2, ak = lane & 3;
   double acc[4][4][2];
 #pragma unroll
@@ -148,10 +149,13 @@ __global__ void __launch_bounds__(wn::GRAM_THREADS) gram_kernel(GroupSrc s, int 
       for (int a = 0; a < 4; ++a) fa[a] = Tc[(32 * SI + 8 * a + ar) * GRS + k0 + ak];
 #pragma unroll
       for (int b = 0; b < 4; ++b) fb[b] = Tc[(32 * SJ + 8 * b + ar) * GRS + k0 + ak];
+      // diagonal super-blocks: the upper 10 of 16 tiles (the lower 6 are
+      // their mirrors), 36 DMMAs per k-step instead of 48 for the CTA
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+        for (int b = 0; b < 4; ++b)
+          if (!diag || b >= a) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
     }
     __syncthreads();
   }
@@ -162,9 +166,10 @@ __global__ void __launch_bounds__(wn::GRAM_THREADS) gram_kernel(GroupSrc s, int 
     for (int b = 0; b < 4; ++b)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
+        if (diag && b < a) continue;
         const int i = 32 * SI + 8 * a + ar, j = 32 * SJ + 8 * b + 2 * ak + e;
         Gg[i * KMAX + j] = acc[a][b][e];
-        if (SI != SJ) Gg[j * KMAX + i] = acc[a][b][e];
+        if (!diag || b > a) Gg[j * KMAX + i] = acc[a][b][e];
       }
 }
 // ---------------------------------------------------------------------------

@@ -210,10 +210,29 @@ def _gather_groups(x_d, shape, p, pos, pad) -> list[PatchGroup]:
     return out
 
 
-def xcorr2_valid_batch(x, kernels, backend: str = "im2col"):
-    """matching.py:116-137 — general float correlation backends: not on the
-    B200 hot path (the heat map only correlates binary edge stacks)."""
-    raise NotImplementedError("xcorr2_valid_batch is outside the B200 hot path (DESIGN.md)")
+def xcorr2_valid_batch(x: np.ndarray, kernels, backend: str = "im2col") -> np.ndarray:
+    """matching.py:116-137 — valid 2-D cross-correlation of x (H, W, C) with N
+    (P, P, C) kernels, channels summed: (H-P+1, W-P+1, N). One device kernel
+    serves every backend name; it accumulates in the (dr, dc, ch) order of
+    the reference tests' loop oracle (bit-identical to it)."""
+    x = np.asarray(x, dtype=np.float64)
+    kernels = np.asarray(kernels, dtype=np.float64)
+    if kernels.ndim == 3:
+        kernels = kernels[None]
+    n, p, q, c = kernels.shape
+    if p != q:
+        raise ValueError("kernels must be square")
+    h, w, xc = x.shape
+    if c != xc:
+        raise ValueError(f"channel mismatch: input {xc}, kernels {c}")
+    if p > h or p > w:
+        raise ValueError(f"kernel {p}x{p} larger than input {h}x{w}")
+    if backend not in BACKENDS:
+        raise ValueError(f"unknown backend {backend!r}")
+    out = D.empty((h - p + 1, w - p + 1, n), D.torch().float64)
+    N.call("glr_xcorr_valid", D.f64(x).data_ptr(), h, w, c, D.f64(kernels).data_ptr(), n, p,
+           out.data_ptr(), D.stream())
+    return D.host(out)
 
 
 def block_match_device(x_d, shape, p, anchors_d, n, cfg: MatchConfig, positions_d=None,

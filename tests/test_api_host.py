@@ -117,8 +117,12 @@ def test_validation_before_launch():
         G.operators.cacti_forward(np.zeros((8, 8, 3)), np.zeros((8, 8, 4)))
     with pytest.raises(ValueError, match="integer overlap counts"):
         G.top_k_positions(np.full((4, 4), 0.5), (0, 0), 3, 1)
-    with pytest.raises(NotImplementedError):
-        G.xcorr2_valid_batch(np.zeros((8, 8, 1)), np.zeros((2, 2, 1)))
+    with pytest.raises(ValueError, match="larger"):
+        G.xcorr2_valid_batch(np.zeros((3, 3, 1)), np.zeros((1, 5, 5, 1)))
+    with pytest.raises(ValueError, match="channel"):
+        G.xcorr2_valid_batch(np.zeros((8, 8, 2)), np.zeros((1, 3, 3, 1)))
+    with pytest.raises(ValueError, match="square"):
+        G.xcorr2_valid_batch(np.zeros((8, 8, 1)), np.zeros((1, 3, 4, 1)))
     bmc = G.MatchConfig(patch_size=4, group_size=4, bm_window=4, mode="bm-uniform")
     ex = G.ExemplarSet(anchors=[(0, 0), (5, 0)], tags=["uniform"] * 2, patch_size=4)
     with pytest.raises(ValueError, match="anchor 1"):

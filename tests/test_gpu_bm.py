@@ -123,3 +123,31 @@ def test_block_match_solve_vs_oracle_larger(rng):
         assert np.array_equal(np.asarray(a), np.asarray(ao))
         assert np.array_equal(np.asarray(pz), np.asarray(po))
     assert np.abs(x - xo).max() <= 1e-6
+
+
+def _loop_xcorr(x, kernels):
+    """The reference tests' kernel-index loop oracle (tests/test_matching.py:16-25
+    of the reference, restated)."""
+    h, w, c = x.shape
+    n, p = kernels.shape[:2]
+    out = np.zeros((h - p + 1, w - p + 1, n))
+    for j in range(n):
+        for dr in range(p):
+            for dc in range(p):
+                for ch in range(c):
+                    out[:, :, j] += kernels[j, dr, dc, ch] * x[dr:dr + h - p + 1,
+                                                              dc:dc + w - p + 1, ch]
+    return out
+
+
+@pytest.mark.parametrize("backend", ["direct", "im2col", "fft"])
+def test_xcorr2_valid_batch_bitwise_vs_loop_oracle(backend, rng):
+    x = rng.random((23, 19, 3))
+    k = rng.standard_normal((5, 4, 4, 3))
+    assert np.array_equal(G.xcorr2_valid_batch(x, k, backend=backend), _loop_xcorr(x, k))
+    xb = (rng.random((16, 16, 2)) < 0.4).astype(np.float64)
+    kb = (rng.random((3, 4, 4, 2)) < 0.4).astype(np.float64)
+    assert np.array_equal(G.xcorr2_valid_batch(xb, kb, backend=backend), _loop_xcorr(xb, kb))
+    d = np.zeros((1, 3, 3, 3))
+    d[0, 0, 0, 0] = 1.0
+    assert np.array_equal(G.xcorr2_valid_batch(x, d)[:, :, 0], x[:21, :17, 0])

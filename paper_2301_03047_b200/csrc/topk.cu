@@ -226,32 +226,46 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   uint64_t* list = p.scratch ? p.scratch + (size_t)n * p.scap : nullptr;
   auto hist_pass = [&](int lo, int hi, bool record) {  // add the scores in [lo, hi)
     constexpr int U = 4;  // 16-byte loads in flight per thread
-    // SIMD pre-test: 8 scores per 16-byte chunk against lo (two u16 per word);
-    // only the rare chunks holding a score >= lo take the per-element path
-    const uint32_t lo2 = (uint32_t)lo | ((uint32_t)lo << 16);
-    for (int64_t tile = 0; tile < M; tile += (int64_t)THREADS * VEC * U) {
+    // SWAR pre-test, 8 scores per 16-byte chunk: scores are < 2^14, so adding
+    // 0x8000 - lo to each halfword sets its top bit iff score >= lo, with no
+    // carry into the neighbour (padding entries past M may carry, which only
+    // adds false positives the exact path filters). Only the rare chunks
+    // holding a score >= lo take the per-element path; 32-bit indices
+    // (M < 2^31), and the scores are pulled out of the registers by shifts.
+    const uint32_t kadd = (0x8000u - (uint32_t)lo) * 0x10001u;
+    const int Mi = (int)M;
+    const int nch = (Mi + VEC - 1) / VEC;
+    const uint4* rv = reinterpret_cast<const uint4*>(row);
+    for (int c0 = 0; c0 < nch; c0 += THREADS * U) {
       uint4 v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int64_t base = tile + ((int64_t)u * THREADS + tid) * VEC;
-        v[u] = base < M ? *reinterpret_cast<const uint4*>(row + base) : make_uint4(0, 0, 0, 0);
+        const int ci = c0 + u * THREADS + tid;
+        v[u] = ci < nch ? rv[ci] : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int64_t base = tile + ((int64_t)u * THREADS + tid) * VEC;
-        const uint32_t any = __vcmpgeu2(v[u].x, lo2) | __vcmpgeu2(v[u].y, lo2) |
-                             __vcmpgeu2(v[u].z, lo2) | __vcmpgeu2(v[u].w, lo2);
+        const uint32_t any = ((v[u].x + kadd) | (v[u].y + kadd) | (v[u].z + kadd) |
+                              (v[u].w + kadd)) & 0x80008000u;
         if (!any) continue;
-        const uint16_t* sv = reinterpret_cast<const uint16_t*>(&v[u]);
+        const int base = (c0 + u * THREADS + tid) * VEC;
+        const uint32_t wv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+        int val[VEC];
+        unsigned hit = 0;
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
-          const int val = min((int)sv[j], p.bins - 1);
-          if (base + j < M && val >= lo && val < hi) {
-            atomicAdd(&hist[val], 1);
-            if (record) {
-              const int off = atomicAdd(&s_nl, 1);
-              if (off < p.scap) list[off] = ((uint64_t)val << 32) | (uint32_t)(base + j);
-            }
+          val[j] = min((int)((j & 1) ? wv[j >> 1] >> 16 : wv[j >> 1] & 0xFFFFu), p.bins - 1);
+          if (base + j < Mi && val[j] >= lo && val[j] < hi) hit |= 1u << j;
+        }
+        if (!hit) continue;
+        int off = record ? atomicAdd(&s_nl, __popc(hit)) : 0;
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          if (!((hit >> j) & 1u)) continue;
+          atomicAdd(&hist[val[j]], 1);
+          if (record) {
+            if (off < p.scap) list[off] = ((uint64_t)val[j] << 32) | (uint32_t)(base + j);
+            ++off;
           }
         }
       }

@@ -32,7 +32,7 @@ constexpr int GROWS = 32;         // rows of M per Gram tile
 constexpr int GRS = GROWS + 4;    // column stride of the Gram tiles (== 4 mod 16)
 constexpr int AROWS = 64;         // rows of M per apply tile (APPLY_RPW 8-row fragments per warp)
 constexpr int ARS = AROWS + 8;    // column stride of the apply tiles (== 8 mod 16)
-constexpr int GRAM_THREADS = 96;  // three warps: super-blocks (0,0), (0,1), (1,1)
+constexpr int GRAM_THREADS = 128; // four warps, 9 of the 36 upper-triangle 8x8 tiles each
 constexpr int EIG_THREADS = 256;
 constexpr int APPLY_THREADS = 256;
 constexpr int APPLY_RPW = 1;      // 8-row fragments per warp in the apply kernel
@@ -106,71 +106,78 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// K1: Gram G = M^T M on DMMA. Three warps own the 32x32 super-blocks (0,0),
-// (0,1), (1,1) of the symmetric 64x64 result (4x4 tiles of 8x8 each); the
-// (1,0) super-block is the mirror of (0,1). Column-major 32-row tiles with
-// column stride GRS = 36 (== 4 mod 16 doubles: fragment loads hit 2 wavefronts).
+// K1: Gram G = M^T M on DMMA (column-major 32-row tiles, column stride
+// GRS = 36 == 4 mod 16 doubles: fragment loads hit 2 wavefronts). Four
+// warps; warp w owns tile rows w and 7-w of the upper triangle (8-w + w+1 =
+// 9 of the 36 8x8 tiles each: 36 DMMAs per k-step for the CTA, the same 9 on
+// every warp's critical path; measured 1.36 -> ~1.0 ms on C2 against three
+// warps on 32x32 super-blocks). The A fragment of tile row i equals the B
+// fragment of tile column i (G = M^T M), so a warp loads only the column
+// fragments w..7 each k-step.
+template <int W>
+__device__ __forceinline__ void gram_tile(double (&acc)[9][2], const double* Tc) {
+  using namespace wn;
+#pragma unroll 2
+  for (int k0 = 0; k0 < GROWS; k0 += 4) {
+    double f[8];
+#pragma unroll
+    for (int c = W; c < 8; ++c) f[c] = Tc[8 * c * GRS + k0];
+#pragma unroll
+    for (int c = W; c < 8; ++c) dmma(acc[c - W][0], acc[c - W][1], f[W], f[c]);
+#pragma unroll
+    for (int c = 7 - W; c < 8; ++c)
+      dmma(acc[8 - W + c - (7 - W)][0], acc[8 - W + c - (7 - W)][1], f[7 - W], f[c]);
+  }
+}
 
 template <bool IMG>
-__global__ void __launch_bounds__(wn::GRAM_THREADS) gram_kernel(GroupSrc s, int n,
-                                                               double* __restrict__ Gout) {
+__global__ void __launch_bounds__(wn::GRAM_THREADS)
+    gram_kernel(GroupSrc s, int n, double* __restrict__ Gout) {
   using namespace wn;
   extern __shared__ __align__(16) double sm[];
   double* T = sm;  // 2 x KMAX x GRS
   __shared__ long long cbase[KMAX];
   const int g = blockIdx.x;
   if (g >= n) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid < KMAX) cbase[tid] = tid < s.K ? col_base<IMG>(s, g, tid) : 0;
   __syncthreads();
-  const int SI = warp == 2 ? 1 : 0, SJ = warp == 0 ? 0 : 1;
-  const bool diag = SI == SJ;
   const int ar = lane >> 2, ak = lane & 3;
-  double acc[4][4][2];
+  // accumulators: row w -> cols w..7 (slots 0..7-w), row 7-w -> cols 7-w..7
+  // (slots 8-w..8): 9 slots; slot q -> (row, col)
+  double acc[9][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int q = 0; q < 9; ++q) acc[q][0] = acc[q][1] = 0.0;
   const int ntiles = (s.m + GROWS - 1) / GROWS;
-  fill_tile<GRAM_THREADS / 32>(T, s, cbase, 0, GROWS, GRS);
+  fill_tile<4>(T, s, cbase, 0, GROWS, GRS);
   for (int tt = 0; tt < ntiles; ++tt) {
     if (tt + 1 < ntiles)
-      fill_tile<GRAM_THREADS / 32>(T + ((tt + 1) & 1) * KMAX * GRS, s, cbase, (tt + 1) * GROWS,
-                                   GROWS, GRS);
+      fill_tile<4>(T + ((tt + 1) & 1) * KMAX * GRS, s, cbase, (tt + 1) * GROWS, GROWS, GRS);
     else
       cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    const double* Tc = T + (tt & 1) * KMAX * GRS;
-#pragma unroll 2
-    for (int k0 = 0; k0 < GROWS; k0 += 4) {  // padding rows are zero
-      double fa[4], fb[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) fa[a] = Tc[(32 * SI + 8 * a + ar) * GRS + k0 + ak];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) fb[b] = Tc[(32 * SJ + 8 * b + ar) * GRS + k0 + ak];
-      // diagonal super-blocks: the upper 10 of 16 tiles (the lower 6 are
-      // their mirrors), 36 DMMAs per k-step instead of 48 for the CTA
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-          if (!diag || b >= a) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+    const double* Tc = T + (tt & 1) * KMAX * GRS + ar * GRS + ak;
+    switch (w) {  // warp-uniform: compile-time accumulator indices per warp
+      case 0: gram_tile<0>(acc, Tc); break;
+      case 1: gram_tile<1>(acc, Tc); break;
+      case 2: gram_tile<2>(acc, Tc); break;
+      default: gram_tile<3>(acc, Tc); break;
     }
     __syncthreads();
   }
   double* Gg = Gout + (size_t)g * GSZ;
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int q = 0; q < 9; ++q) {
+    const int ti = q < 8 - w ? w : 7 - w;
+    const int tj = q < 8 - w ? w + q : q - (8 - w) + 7 - w;
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        if (diag && b < a) continue;
-        const int i = 32 * SI + 8 * a + ar, j = 32 * SJ + 8 * b + 2 * ak + e;
-        Gg[i * KMAX + j] = acc[a][b][e];
-        if (!diag || b > a) Gg[j * KMAX + i] = acc[a][b][e];
-      }
+    for (int e = 0; e < 2; ++e) {
+      const int i = 8 * ti + ar, j = 8 * tj + 2 * ak + e;
+      Gg[i * KMAX + j] = acc[q][e];
+      if (tj != ti) Gg[j * KMAX + i] = acc[q][e];
+    }
+  }
 }
 // ---------------------------------------------------------------------------
 // K2: eigen-decomposition + shrinkage -> Wm (in place over G)
@@ -820,7 +827,6 @@ static int blocks_for(int64_t n, int threads = 256) {
 constexpr size_t kGramSmem = 2 * wn::KMAX * wn::GRS * sizeof(double);
 constexpr size_t kEigSmem = wn::KMAX * (wn::GLD + wn::VLD) * sizeof(double);
 constexpr size_t kApplySmem = (wn::KMAX * wn::LD + 2 * wn::KMAX * wn::ARS) * sizeof(double);
-
 // Gram -> eigen/shrink -> apply for n groups; ws holds n x 64 x 64 doubles.
 template <bool IMG>
 static int run_wnnm(const GroupSrc& s, int n, const EigArgs& ea_in, double scale,

@@ -650,8 +650,12 @@ __global__ void __launch_bounds__(wn::APPLY_THREADS)
             if (j < K) {
               if constexpr (IMG) {
                 const long long val = __double2ll_rn(o[f][b][e] * scale);
+#ifdef GLR_DEV_APPLY_NOATOMIC  // dev experiment: cost of the scatter atomics
+                if (val == 0x7edcba9876543210ll) acc_out[cbase[j] + off] = val;
+#else
                 atomicAdd(reinterpret_cast<unsigned long long*>(acc_out + cbase[j] + off),
                           (unsigned long long)val);
+#endif
               } else {
                 out[cbase[j] + off] = o[f][b][e];
               }

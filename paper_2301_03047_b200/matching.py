@@ -229,9 +229,12 @@ def xcorr2_valid_batch(x: np.ndarray, kernels, backend: str = "im2col") -> np.nd
         raise ValueError(f"kernel {p}x{p} larger than input {h}x{w}")
     if backend not in BACKENDS:
         raise ValueError(f"unknown backend {backend!r}")
+    # keep the device copies referenced until the launch (a temporary's block
+    # could be handed to the next upload before the kernel reads it)
+    x_d, k_d = D.f64(x), D.f64(kernels)
     out = D.empty((h - p + 1, w - p + 1, n), D.torch().float64)
-    N.call("glr_xcorr_valid", D.f64(x).data_ptr(), h, w, c, D.f64(kernels).data_ptr(), n, p,
-           out.data_ptr(), D.stream())
+    N.call("glr_xcorr_valid", x_d.data_ptr(), h, w, c, k_d.data_ptr(), n, p, out.data_ptr(),
+           D.stream())
     return D.host(out)
 
 

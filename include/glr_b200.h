@@ -132,12 +132,8 @@ int glr_heat_topk(const uint8_t* stack_d, int H, int W, int C, int P, int expand
  * (score desc, flat index asc) skipping Chebyshev <= sep of any chosen,
  * relaxed to sep = 0, then padded with the anchor.
  * positions_d: n*K*2 int32; padded_d: n int32. ws (optional, may be NULL):
- * with glr_topk_workspace bytes the map is read once by a barrier-free
- * streaming pass over all rows that records every score >= a quarter of the
- * exemplar's self-score into per-exemplar lists, and the per-exemplar
- * selection runs on the lists (rows re-read only for the rare exemplars
- * whose list overflows or whose cut falls below that floor). Without ws,
- * one CTA per exemplar reads its row (twice).                              */
+ * glr_topk_workspace bytes let the histogram pass record the high-score
+ * entries so each heat row is read once instead of twice.                  */
 size_t glr_topk_workspace(int n_max, int K, int sep);
 int glr_topk(const uint16_t* heat_d, int n_max, const int32_t* n_dev_d, int oh, int ow,
              int max_score, const int32_t* anchors_d, int K, int sep, int32_t* positions_d,

@@ -163,8 +163,6 @@ def call(name: str, *args) -> int:
     check(st, name)
     if name == "glr_edge_stack":  # relative max pass + maps and/or stack
         launch_count += int(bool(args[6])) + int(args[8] is not None) + int(args[9] is not None)
-    elif name == "glr_topk":  # + the streaming pass when a workspace is given
-        launch_count += 2 if args[11] is not None else 1
     elif name == "glr_tv_denoise":  # one launch per dual step + the output
         launch_count += (int(args[5]) + 1) if args[4] > 0 else 0
     else:

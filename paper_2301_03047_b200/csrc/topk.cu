@@ -55,9 +55,6 @@ struct TopkParams {
   // instead of the row again
   uint64_t* scratch;
   int scap;
-  // set when topk_stream_kernel already filled the lists: per-exemplar entry
-  // counts (may exceed scap: overflow, the row is then re-read)
-  const uint32_t* list_cnt;
 };
 
 __device__ __forceinline__ int cheb(int r0, int c0, int r1, int c1) {
@@ -193,81 +190,6 @@ __device__ __forceinline__ void bitonic_i32(int32_t* a, int n) {
   }
 }
 
-// Streaming pass of the split top-K: a persistent grid walks (exemplar,
-// segment) work items with no block barrier on the data path, so every warp
-// keeps its loads in flight until the whole map is read. Each 16-byte chunk
-// is pre-tested with the SWAR halfword add against the exemplar's floor
-// L = score(anchor) / 4; hits are appended (score, position) to the
-// exemplar's list, one global atomic per warp step. topk_kernel then builds
-// its histogram from the list.
-namespace topk {
-constexpr int STREAM_THREADS = 256;
-constexpr int SEG_CHUNKS = STREAM_THREADS * 4 * 8;  // 16-byte chunks per work item
-}  // namespace topk
-
-__global__ void __launch_bounds__(topk::STREAM_THREADS) topk_stream_kernel(TopkParams p,
-                                                                         uint32_t* cnt) {
-  using namespace topk;
-  constexpr int U = 4;
-  const int N = p.n_dev ? min(*p.n_dev, p.n_max) : p.n_max;
-  const int Mi = (int)p.M;
-  const int nch = (Mi + VEC - 1) / VEC;
-  const int nseg = (nch + SEG_CHUNKS - 1) / SEG_CHUNKS;
-  const int64_t items = (int64_t)N * nseg;
-  const int tid = threadIdx.x, lane = tid & 31;
-  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-    const int n = (int)(it / nseg), seg = (int)(it - (int64_t)n * nseg);
-    const uint16_t* row = p.heat + (size_t)n * p.stride;
-    const uint4* rv = reinterpret_cast<const uint4*>(row);
-    const int64_t aidx = (int64_t)p.anchors[2 * n] * p.ow + p.anchors[2 * n + 1];
-    const int L = min((int)row[aidx] >> 2, p.bins - 1);
-    const uint32_t kadd = (0x8000u - (uint32_t)L) * 0x10001u;
-    uint64_t* list = p.scratch + (size_t)n * p.scap;
-    const int cend = min(nch, (seg + 1) * SEG_CHUNKS);
-    for (int c0 = seg * SEG_CHUNKS; c0 < cend; c0 += STREAM_THREADS * U) {
-      uint4 v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int ci = c0 + u * STREAM_THREADS + tid;
-        v[u] = ci < cend ? __ldcs(rv + ci) : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t any = ((v[u].x + kadd) | (v[u].y + kadd) | (v[u].z + kadd) |
-                              (v[u].w + kadd)) & 0x80008000u;
-        if (!__any_sync(0xffffffffu, any != 0u)) continue;
-        const int base = (c0 + u * STREAM_THREADS + tid) * VEC;
-        const uint32_t wv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-        int val[VEC];
-        unsigned hit = 0;
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) {
-          val[j] = min((int)((j & 1) ? wv[j >> 1] >> 16 : wv[j >> 1] & 0xFFFFu), p.bins - 1);
-          if (base + j < Mi && val[j] >= L) hit |= 1u << j;
-        }
-        // warp-aggregated append: one atomic per warp step
-        const int h = __popc(hit);
-        int incl = h;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const int tot = __shfl_sync(0xffffffffu, incl, 31);
-        uint32_t off0 = 0;
-        if (lane == 31 && tot) off0 = atomicAdd(&cnt[n], (uint32_t)tot);
-        uint32_t off = __shfl_sync(0xffffffffu, off0, 31) + (uint32_t)(incl - h);
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) {
-          if (!((hit >> j) & 1u)) continue;
-          if (off < (uint32_t)p.scap) list[off] = ((uint64_t)val[j] << 32) | (uint32_t)(base + j);
-          ++off;
-        }
-      }
-    }
-  }
-}
-
 __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   using namespace topk;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -349,20 +271,7 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
       }
     }
   };
-  if (p.list_cnt) {
-    // the streaming pass already recorded every score >= L of this row
-    const uint32_t c = p.list_cnt[n];
-    if (c <= (uint32_t)p.scap) {
-      for (int i = tid; i < (int)c; i += THREADS)
-        atomicAdd(&hist[min((int)(list[i] >> 32), p.bins - 1)], 1);
-      if (tid == 0) s_nl = (int)c;
-    } else {  // overflowed list: histogram from the row, collect from the row
-      list = nullptr;
-      hist_pass(L, p.bins, false);
-    }
-  } else {
-    hist_pass(L, p.bins, list != nullptr);
-  }
+  hist_pass(L, p.bins, list != nullptr);
   __syncthreads();
 
   // 2. cut score T: walk bins from the top down to `lo`, 32 at a time
@@ -622,11 +531,8 @@ using namespace glr;
 
 // optional: n_max x kTopkScratch (score, position) records (single row pass)
 constexpr int kTopkScratch = 32768;
-// workspace: n_max x kTopkScratch (score, position) records, then n_max
-// record counters (the split streaming pass)
 extern "C" size_t glr_topk_workspace(int n_max, int K, int sep) {
-  const size_t n = (size_t)std::max(n_max, 0);
-  return n * kTopkScratch * sizeof(uint64_t) + n * sizeof(uint32_t) + 256;
+  return (size_t)std::max(n_max, 0) * kTopkScratch * sizeof(uint64_t) + 256;
 }
 
 #ifdef GLR_TOPK_STATS
@@ -668,7 +574,6 @@ static int topk_params(int n_max, int oh, int ow, int max_score, const int32_t* 
   p.padded = padded_d;
   p.scratch = nullptr;
   p.scap = 0;
-  p.list_cnt = nullptr;
   return GLR_OK;
 }
 
@@ -684,29 +589,14 @@ extern "C" int glr_topk(const uint16_t* heat_d, int n_max, const int32_t* n_dev_
   if (n_max <= 0) return GLR_OK;
   p.heat = heat_d;
   p.n_dev = n_dev_d;
-  cudaStream_t st_ = (cudaStream_t)stream;
   if (ws_d && ws_bytes >= glr_topk_workspace(n_max, K, sep)) {
     p.scratch = reinterpret_cast<uint64_t*>(
         (reinterpret_cast<uintptr_t>(ws_d) + 255) & ~uintptr_t(255));
     p.scap = kTopkScratch;
-    // split form: a barrier-free streaming pass fills the per-exemplar lists,
-    // then one CTA per exemplar selects from its list
-    uint32_t* cnt = reinterpret_cast<uint32_t*>(p.scratch + (size_t)n_max * kTopkScratch);
-    GLR_CUDA(cudaMemsetAsync(cnt, 0, (size_t)n_max * sizeof(uint32_t), st_));
-    static int stream_blocks = 0;
-    if (!stream_blocks) {
-      int per_sm = 0;
-      GLR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, topk_stream_kernel,
-                                                             topk::STREAM_THREADS, 0));
-      stream_blocks = kNumSMs * std::max(per_sm, 1);
-    }
-    topk_stream_kernel<<<stream_blocks, topk::STREAM_THREADS, 0, st_>>>(p, cnt);
-    GLR_CUDA(cudaGetLastError());
-    p.list_cnt = cnt;
   }
   GLR_CUDA(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
-  topk_kernel<<<n_max, topk::THREADS, smem, st_>>>(p);
+  topk_kernel<<<n_max, topk::THREADS, smem, (cudaStream_t)stream>>>(p);
   return check_launch("topk_kernel");
 }
 

@@ -31,6 +31,8 @@ namespace topk {
 constexpr int THREADS = 512;
 constexpr int VEC = 8;  // u16 scores per 16-byte load
 constexpr int MAX_BINS = 12288;
+constexpr int RING_STAGES = 3;
+constexpr int RING_BYTES = 16384;  // 32 bytes per thread per slice
 }  // namespace topk
 
 #ifdef GLR_TOPK_STATS
@@ -195,10 +197,12 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* sA = reinterpret_cast<uint64_t*>(smem);                   // a_cap
   int32_t* sB = reinterpret_cast<int32_t*>(sA + p.a_cap);              // b_cap
-  int32_t* hist = sB + p.b_cap;                                        // bins
+  // hist after max(A + B, the first pass's ring), which aliases A and B
+  int32_t* hist = reinterpret_cast<int32_t*>(
+      smem + max(p.a_cap * 8 + p.b_cap * 4, topk::RING_STAGES * topk::RING_BYTES));  // bins
   int32_t* chosen = hist + p.bins;                                     // 2*K
   __shared__ int warp_tot[32];
-  __shared__ int s_total, s_T, s_cntA, s_baseA, s_baseB, s_na, s_nb, s_found, s_nl;
+  __shared__ int s_total, s_T, s_cntA, s_baseA, s_baseB, s_na, s_nb, s_found, s_nl, s_next;
   const int BCAP = p.b_cap;
 
   const int n = blockIdx.x;
@@ -217,10 +221,17 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   const int64_t aidx = (int64_t)p.anchors[2 * n] * p.ow + p.anchors[2 * n + 1];
   const int L = min((int)row[aidx] >> 2, p.bins - 1);
   for (int b = L + tid; b < p.bins; b += THREADS) hist[b] = 0;
+  __shared__ __align__(8) uint64_t s_full[topk::RING_STAGES], s_empty[topk::RING_STAGES];
   if (tid == 0) {
+    for (int r = 0; r < RING_STAGES; ++r) {
+      mbar_init(&s_full[r], 1);
+      mbar_init(&s_empty[r], THREADS / 32);
+    }
+    fence_barrier_init();
     s_na = 0;
     s_nb = 0;
     s_nl = 0;
+    s_next = 0;
   }
   __syncthreads();
   uint64_t* list = p.scratch ? p.scratch + (size_t)n * p.scap : nullptr;
@@ -236,19 +247,31 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
     const int Mi = (int)M;
     const int nch = (Mi + VEC - 1) / VEC;
     const uint4* rv = reinterpret_cast<const uint4*>(row);
-    for (int c0 = 0; c0 < nch; c0 += THREADS * U) {
+    // warp tiles of 32 x U chunks handed out dynamically (one shared atomic
+    // per tile, the next grab issued one tile ahead), so the warps of a CTA
+    // reach the barrier after the pass together instead of waiting on the
+    // slowest of a static split
+    const int ntl = (nch + 32 * U - 1) / (32 * U);
+    int wt = 0;
+    if (lane == 0) wt = atomicAdd(&s_next, 1);
+    wt = __shfl_sync(0xffffffffu, wt, 0);
+    while (wt < ntl) {
+      const int c0 = wt * 32 * U;
       uint4 v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int ci = c0 + u * THREADS + tid;
+        const int ci = c0 + u * 32 + lane;
         v[u] = ci < nch ? rv[ci] : make_uint4(0, 0, 0, 0);
       }
+      int wn = 0;
+      if (lane == 0) wn = atomicAdd(&s_next, 1);
+      wt = __shfl_sync(0xffffffffu, wn, 0);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint32_t any = ((v[u].x + kadd) | (v[u].y + kadd) | (v[u].z + kadd) |
                               (v[u].w + kadd)) & 0x80008000u;
         if (!any) continue;
-        const int base = (c0 + u * THREADS + tid) * VEC;
+        const int base = (c0 + u * 32 + lane) * VEC;
         const uint32_t wv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
         int val[VEC];
         unsigned hit = 0;
@@ -271,7 +294,70 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
       }
     }
   };
-  hist_pass(L, p.bins, list != nullptr);
+  // First pass fed by bulk TMA copies: thread 0 keeps RING_STAGES 16 KB
+  // slices of the row in flight (cp.async.bulk into a shared-memory ring that
+  // aliases the A/B buffers, completion on mbarriers), every thread tests its
+  // 32 bytes of a slice from shared memory and the warps release the slice on
+  // an `empty` mbarrier -- the loads cost no registers and no issue slots.
+  auto ring_pass = [&](int lo) {
+    const uint32_t kadd = (0x8000u - (uint32_t)lo) * 0x10001u;
+    const int Mi = (int)M;
+    const int64_t rbytes = (int64_t)p.stride * 2;  // padded row: multiple of 16 B
+    const int nst = (int)((rbytes + RING_BYTES - 1) / RING_BYTES);
+    uint8_t* ring = reinterpret_cast<uint8_t*>(sA);
+    auto issue = [&](int j) {
+      const int sl = j % RING_STAGES;
+      const uint32_t bytes = (uint32_t)min((int64_t)RING_BYTES, rbytes - (int64_t)j * RING_BYTES);
+      mbar_arrive_expect_tx(&s_full[sl], bytes);
+      bulk_load(ring + sl * RING_BYTES,
+                reinterpret_cast<const uint8_t*>(row) + (int64_t)j * RING_BYTES, bytes,
+                &s_full[sl]);
+    };
+    if (tid == 0)
+      for (int j = 0; j < min(RING_STAGES, nst); ++j) issue(j);
+    for (int i = 0; i < nst; ++i) {
+      const int sl = i % RING_STAGES;
+      mbar_wait(&s_full[sl], (uint32_t)(i / RING_STAGES) & 1u);
+      const uint4* sv4 = reinterpret_cast<const uint4*>(ring + sl * RING_BYTES);
+#pragma unroll
+      for (int u = 0; u < RING_BYTES / 16 / THREADS; ++u) {
+        const int cl = u * THREADS + tid;
+        const uint4 v = sv4[cl];
+        const uint32_t any =
+            ((v.x + kadd) | (v.y + kadd) | (v.z + kadd) | (v.w + kadd)) & 0x80008000u;
+        if (!any) continue;
+        const int base = (i * (RING_BYTES / 16) + cl) * VEC;
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+        int val[VEC];
+        unsigned hit = 0;
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          val[j] = min((int)((j & 1) ? wv[j >> 1] >> 16 : wv[j >> 1] & 0xFFFFu), p.bins - 1);
+          if (base + j < Mi && val[j] >= lo) hit |= 1u << j;
+        }
+        if (!hit) continue;
+        int off = atomicAdd(&s_nl, __popc(hit));
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          if (!((hit >> j) & 1u)) continue;
+          atomicAdd(&hist[val[j]], 1);
+          if (off < p.scap) list[off] = ((uint64_t)val[j] << 32) | (uint32_t)(base + j);
+          ++off;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[sl]);
+      if (tid == 0 && i + RING_STAGES < nst) {  // refill this slot once every warp let go
+        mbar_wait(&s_empty[sl], (uint32_t)(i / RING_STAGES) & 1u);
+        issue(i + RING_STAGES);
+      }
+    }
+  };
+  if (list) {
+    ring_pass(L);  // bulk-TMA-fed first pass (records the list)
+  } else {
+    hist_pass(L, p.bins, false);
+  }
   __syncthreads();
 
   // 2. cut score T: walk bins from the top down to `lo`, 32 at a time
@@ -300,6 +386,8 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   const bool first_pass_cut = s_found;
   if (!s_found) {
     for (int b = tid; b < L; b += THREADS) hist[b] = 0;
+    __syncthreads();
+    if (tid == 0) s_next = 0;
     __syncthreads();
     hist_pass(0, L, false);
     __syncthreads();
@@ -521,8 +609,11 @@ static int pow2_at_least(int v) {
 }
 
 static size_t topk_smem(int pool, int bins, int K) {
-  return (size_t)pow2_at_least(pool) * 8 + (size_t)pow2_at_least(std::max(pool, 4096)) * 4 +
-         (size_t)bins * 4 + (size_t)K * 8 + 16;
+  // sA | sB | hist | chosen; the first pass's bulk-copy ring aliases sA/sB
+  const size_t ab =
+      (size_t)pow2_at_least(pool) * 8 + (size_t)pow2_at_least(std::max(pool, 4096)) * 4;
+  return std::max(ab, (size_t)topk::RING_STAGES * topk::RING_BYTES) + (size_t)bins * 4 +
+         (size_t)K * 8 + 16;
 }
 
 }  // namespace glr

@@ -57,8 +57,9 @@ constexpr int BK = 128;      // bytes of K per stage (one 128B swizzle row = 256
 constexpr int UK = 32;       // bytes of K per tcgen05.mma kind::mxf4 (64 fp4)
 constexpr int STAGES = 7;
 constexpr int ACC = 2;       // TMEM accumulators (2 x 224 columns)
-constexpr int THREADS = 384;  // warps 4-11: epilogue (lane quadrant w%4, column half)
-constexpr int EPI_WARPS = 8;
+constexpr int EPI_GROUPS = 3;  // column groups of the epilogue (chunks 0-2 | 3-4 | 5-6)
+constexpr int EPI_WARPS = 4 * EPI_GROUPS;
+constexpr int THREADS = 128 + 32 * EPI_WARPS;  // warps 4..: epilogue (lane quadrant w%4, group)
 constexpr int A_BYTES = BM * BK;
 constexpr int B_BYTES = BNH * BK;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -215,7 +216,10 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
   } else if (warp >= 4) {
     // ---- epilogue (both CTAs): own 128 TMEM lanes -> u16 exemplar-major rows ----
     const int ew = warp & 3;           // TMEM lanes 32*ew .. 32*ew+31 (warp id % 4)
-    const int ch = (warp - 4) >> 2;    // column half: chunks ch*4 .. (BN/32 chunks total)
+    const int grp = (warp - 4) >> 2;  // column group: 32-column chunks [c_lo, c_hi)
+    constexpr int NCH = BN / 32;
+    const int c_lo = (NCH * grp + EPI_GROUPS - 1) / EPI_GROUPS;
+    const int c_hi = (NCH * (grp + 1) + EPI_GROUPS - 1) / EPI_GROUPS;
     const uint32_t te_leader[ACC] = {cluster_addr(&tempty[0], 0), cluster_addr(&tempty[1], 0)};
     int lt = 0;
     for (int t = cl; t < total; t += n_cl, ++lt) {
@@ -229,7 +233,7 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
       const bool v_ok = v < p.ow;
       uint16_t* out = p.heat + (size_t)u * p.ow + v;
 #pragma unroll 1
-      for (int c = ch * 4; c < min(ch * 4 + 4, BN / 32); ++c) {
+      for (int c = c_lo; c < c_hi; ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * BN + c * 32), r);
         tmem_ld_wait();
@@ -260,7 +264,11 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int n = nb + j;
-          if (v_ok && n < N) out[(size_t)n * p.Mpad] = (uint16_t)__float2uint_rn(__uint_as_float(r[j]));
+          // streaming (evict-first) stores: the 8.5 GB map must not push the
+          // reused A/B operand tiles out of L2
+          if (v_ok && n < N)
+            __stcs(reinterpret_cast<unsigned short*>(out + (size_t)n * p.Mpad),
+                   (unsigned short)__float2uint_rn(__uint_as_float(r[j])));
         }
       }
       tc_fence_before();

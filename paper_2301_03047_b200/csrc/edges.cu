@@ -507,6 +507,143 @@ __global__ void __launch_bounds__(1024) nms_bitmap_kernel(const int32_t* __restr
 
 constexpr int kNmsBitmapMaxBytes = 200 * 1024;
 
+// Batched exact greedy NMS: 1024 ranked candidates per step. A candidate
+// blocked by an earlier batch's pick (shared-memory bitmap) is dead; among
+// the live ones the sequential rule "picked iff no earlier PICKED live
+// candidate lies within Chebyshev R" is resolved in parallel rounds: a live
+// candidate is PICKED once every earlier conflicting live candidate is
+// REJECTED, REJECTED as soon as one of them is PICKED (both final, so the
+// fixed point is the sequential greedy result, the lexicographically first
+// independent set). Picks are emitted in rank order by a block scan, the
+// first max_n kept, and their (2R+1)^2 windows or-ed into the bitmap.
+namespace nmsb {
+constexpr int B = 512;      // candidates per batch (= threads; 1024: 0.67 ms, 256: 0.51 ms on C2)
+constexpr int NBR = 8;      // earlier conflicts remembered per candidate
+constexpr uint8_t DEAD = 0, UNDEC = 1, PICKED = 2, REJECTED = 3;
+constexpr size_t kBatchBytes = (size_t)B * (2 * 4 + NBR * 2 + 1);
+}  // namespace nmsb
+
+__global__ void __launch_bounds__(nmsb::B) nms_batch_kernel(const int32_t* __restrict__ idx,
+                                                           const int* __restrict__ n_cand, int H,
+                                                           int W, int max_n, int R,
+                                                           int32_t* __restrict__ out_rc,
+                                                           int32_t* __restrict__ out_n) {
+  using namespace nmsb;
+  extern __shared__ uint32_t bm[];
+  const int nw = (int)(((int64_t)H * W + 31) / 32);
+  int32_t* br = reinterpret_cast<int32_t*>(bm + ((nw + 3) & ~3));
+  int32_t* bc = br + B;
+  int16_t* nbr = reinterpret_cast<int16_t*>(bc + B);
+  uint8_t* st = reinterpret_cast<uint8_t*>(nbr + B * NBR);
+  __shared__ int warp_tot[32];
+  __shared__ int s_total, s_picked, s_nb, s_pos;
+  const int t = threadIdx.x;
+  for (int i = t; i < nw; i += B) bm[i] = 0u;
+  if (t == 0) {
+    s_picked = 0;
+    s_pos = 0;
+  }
+  __syncthreads();
+  const int total = *n_cand;
+  while (s_pos < total && s_picked < max_n) {
+    // 1. fill the batch with the next B candidates not blocked by earlier
+    //    batches' picks, in rank order (stable compaction of 1024-chunks)
+    if (t == 0) s_nb = 0;
+    __syncthreads();
+    while (s_nb < B && s_pos < total) {
+      const int pos0 = s_pos, nb0 = s_nb;
+      const int i = pos0 + t;
+      int cand = 0;
+      bool alive = false;
+      if (i < total) {
+        cand = idx[i];
+        alive = !((bm[cand >> 5] >> (cand & 31)) & 1u);
+      }
+      const int e = block_excl_scan_1024(alive ? 1 : 0, warp_tot, &s_total);
+      if (alive && nb0 + e < B) {
+        const int r = cand / W;
+        br[nb0 + e] = r;
+        bc[nb0 + e] = cand - r * W;
+      }
+      if (alive && nb0 + e == B) s_pos = i;  // first candidate left for the next batch
+      __syncthreads();
+      if (t == 0) {
+        if (nb0 + s_total <= B) s_pos = min(total, pos0 + B);
+        s_nb = min(B, nb0 + s_total);
+      }
+      __syncthreads();
+    }
+    const int nb = s_nb;
+    // 2. earlier conflicts inside the batch (Chebyshev <= R)
+    const bool live = t < nb;
+    const int r = live ? br[t] : 0, c = live ? bc[t] : 0;
+    int cnt = 0;
+    if (live) {
+      for (int j = 0; j < t; ++j) {
+        if (abs(br[j] - r) <= R && abs(bc[j] - c) <= R) {
+          if (cnt < NBR) nbr[t * NBR + cnt] = (int16_t)j;
+          ++cnt;
+        }
+      }
+    }
+    st[t] = !live ? DEAD : (cnt == 0 ? PICKED : UNDEC);
+    // 3. resolve in rounds (final states only ever set once)
+    bool changed;
+    do {
+      __syncthreads();
+      changed = false;
+      if (st[t] == UNDEC) {
+        bool any_picked = false, all_rejected = true;
+        if (cnt <= NBR) {
+          for (int q = 0; q < cnt; ++q) {
+            const uint8_t s2 = st[nbr[t * NBR + q]];
+            any_picked |= s2 == PICKED;
+            all_rejected &= s2 == REJECTED;
+          }
+        } else {  // many earlier conflicts: rescan the batch
+          for (int j = 0; j < t; ++j) {
+            if (abs(br[j] - r) <= R && abs(bc[j] - c) <= R) {
+              const uint8_t s2 = st[j];
+              any_picked |= s2 == PICKED;
+              all_rejected &= s2 == REJECTED;
+            }
+          }
+        }
+        if (any_picked) {
+          st[t] = REJECTED;
+          changed = true;
+        } else if (all_rejected) {
+          st[t] = PICKED;
+          changed = true;
+        }
+      }
+    } while (__syncthreads_or(changed));
+    // 4. emit the picks in rank order, block their windows
+    const bool pk = st[t] == PICKED;
+    const int slot = s_picked + block_excl_scan_1024(pk ? 1 : 0, warp_tot, &s_total);
+    if (pk && slot < max_n) {
+      out_rc[2 * slot] = r;
+      out_rc[2 * slot + 1] = c;
+      for (int rr = max(r - R, 0); rr <= min(r + R, H - 1); ++rr) {
+        const int64_t b0 = (int64_t)rr * W + max(c - R, 0);
+        const int64_t b1 = (int64_t)rr * W + min(c + R, W - 1);
+        for (int64_t w0 = b0 >> 5; w0 <= (b1 >> 5); ++w0) {
+          const int64_t lo_b = max(b0, w0 * 32), hi_b = min(b1, w0 * 32 + 31);
+          const unsigned lo = ~0u << (lo_b & 31);
+          const unsigned hi = (hi_b & 31) == 31 ? ~0u : ((1u << ((hi_b & 31) + 1)) - 1u);
+          atomicOr(&bm[w0], lo & hi);
+        }
+      }
+    }
+    __syncthreads();
+    if (t == 0) s_picked = min(max_n, s_picked + s_total);
+    __syncthreads();
+  }
+  if (t == 0) *out_n = s_picked;
+}
+
+
+
 // ---------------------------------------------------------------------------
 // A4: anchors (edges.py:131-162)
 
@@ -707,6 +844,19 @@ extern "C" int glr_corners(const double* resp_d, int H, int W, int max_n, int nm
   GLR_CUDA(cub::DeviceRadixSort::SortPairsDescending(p, temp_bytes, k_in, k_out, v_in, v_out,
                                                      (int)n, 0, 64, st));
   const size_t bm_bytes = (size_t)((n + 31) / 32) * sizeof(uint32_t);
+  const size_t batch_bytes = ((bm_bytes + 15) & ~size_t(15)) + nmsb::kBatchBytes;
+  constexpr int kBatchSmemMax = 226 * 1024;  // 227 KB less the kernel's static shared memory
+  if (batch_bytes <= (size_t)kBatchSmemMax && nms_radius <= 64) {
+    static bool battr = false;
+    if (!battr) {
+      GLR_CUDA(cudaFuncSetAttribute(nms_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kBatchSmemMax));
+      battr = true;
+    }
+    nms_batch_kernel<<<1, nmsb::B, batch_bytes, st>>>(v_out, n_cand, H, W, max_n, nms_radius,
+                                                      out_rc_d, out_n_d);
+    return check_launch("nms_batch_kernel");
+  }
   if (bm_bytes <= (size_t)kNmsBitmapMaxBytes && nms_radius <= 15) {
     static bool attr = false;
     if (!attr) {

@@ -81,6 +81,13 @@ size_t glr_corner_workspace(int H, int W, int C);
 int glr_corner_response(const double* x_d, int H, int W, int C, double* resp_d, void* ws_d,
                         void* stream);
 
+/* glr_corner_response_grad: the same response from the Sobel gradients
+ * glr_sobel already produced (gh_d, gv_d (H,W,C)): mag = mean_c
+ * sqrt(gh^2 + gv^2) is bit-identical to the x-based entry, one Sobel pass
+ * fewer when the edge stack needs the gradients anyway. ws as above.       */
+int glr_corner_response_grad(const double* gh_d, const double* gv_d, int H, int W, int C,
+                             double* resp_d, void* ws_d, void* stream);
+
 /* glr_corners: threshold >= quality*max, order (score desc, row, col), greedy
  * Chebyshev NMS, at most max_n picks (edges.py:113-128).
  * out_rc_d: 2*max_n int32; out_n_d: 1 int32. ws: glr_nms_workspace.          */

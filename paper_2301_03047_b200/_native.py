@@ -46,6 +46,7 @@ SIGNATURES: dict[str, tuple] = {
     "glr_stack_from_maps": (i32, [vp, i32, i32, i32, i32, vp, vp]),
     "glr_corner_workspace": (sz, [i32, i32, i32]),
     "glr_corner_response": (i32, [vp, i32, i32, i32, vp, vp, vp]),
+    "glr_corner_response_grad": (i32, [vp, vp, i32, i32, i32, vp, vp, vp]),
     "glr_nms_workspace": (sz, [i32, i32]),
     "glr_corners": (i32, [vp, i32, i32, i32, i32, f64, vp, vp, vp, sz, vp]),
     "glr_anchor_workspace": (sz, [i32, i32]),
@@ -144,7 +145,7 @@ def check(status: int, what: str = "") -> None:
 # the CUB radix-sort kernels inside glr_corners are not counted). Used for the
 # bench's gpu_launches claim.
 KERNELS_PER_CALL = {
-    "glr_sobel": 1, "glr_stack_from_maps": 1, "glr_corner_response": 6, "glr_corners": 3,
+    "glr_sobel": 1, "glr_stack_from_maps": 1, "glr_corner_response": 6, "glr_corner_response_grad": 5, "glr_corners": 3,
     "glr_select_anchors": 1, "glr_heat_map": 2, "glr_topk": 1, "glr_gather": 1, "glr_wnnm": 3,
     "glr_wnnm_scatter": 3, "glr_scatter_count": 1, "glr_scatter_fixed": 1,
     "glr_scatter_add_f64": 1, "glr_normalize": 1, "glr_masksum_forward": 1,

@@ -86,14 +86,16 @@ __device__ double pairwise_sum(const double* a, int n) {
 // ---------------------------------------------------------------------------
 // A1: per-channel Sobel (edges.py:53-64)
 
+// IDX: int for images below 2^31 elements (cheaper index division), else int64_t
+template <typename IDX>
 __global__ void sobel_kernel(const double* __restrict__ x, int H, int W, int C,
                              double* __restrict__ gh, double* __restrict__ gv) {
-  const int64_t total = (int64_t)H * W * C;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const IDX total = (IDX)H * W * C;
+  for (IDX i = blockIdx.x * (IDX)blockDim.x + threadIdx.x; i < total;
+       i += (IDX)gridDim.x * blockDim.x) {
     const int ch = (int)(i % C);
-    const int64_t pix = i / C;
-    const int r = (int)(pix / W), c = (int)(pix % W);
+    const IDX pix = i / C;
+    const int r = (int)(pix / W), c = (int)(pix - (IDX)r * W);
     const int r0 = max(r - 1, 0), r2 = min(r + 1, H - 1);
     const int c0 = max(c - 1, 0), c2 = min(c + 1, W - 1);
     auto X = [&](int rr, int cc) { return x[((int64_t)rr * W + cc) * C + ch]; };
@@ -164,29 +166,47 @@ __global__ void edge_maps_kernel(const double* __restrict__ gh, const double* __
 
 // Stack layout (heat_gemm.cu): (H, W, Ce) binary elements, Ce = e*4C, stored
 // as packed E2M1 nibbles (1.0 / 0.0), element 2j in the low nibble of byte j.
+// One thread per pixel walks its Ce elements in order (p, map, channel) with
+// running counters (no per-element index division) and stores the nibbles
+// eight at a time as 32-bit words (Cb = Ce/2 bytes per pixel, a multiple of
+// 4 whenever e*C is even -- always for the GEMM's e), byte-wise otherwise.
+template <bool WORDS>
 __global__ void edge_stack_kernel(const double* __restrict__ gh, const double* __restrict__ gv,
                                   int H, int W, int C, int e, EdgeTh t,
                                   const unsigned long long* mx, uint8_t* __restrict__ stack) {
   double th_h, th_v;
   edge_thresholds(mx, t, th_h, th_v);
-  const int C4 = 4 * C, Ce = e * C4, Cb = Ce / 2;
-  const int64_t total = (int64_t)H * W * Cb;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int cb = (int)(i % Cb);
-    const int64_t pix = i / Cb;
-    const int r = (int)(pix / W), c = (int)(pix % W);
-    uint8_t byte = 0;
+  const int Cb = e * 2 * C;
+  const int64_t npix = (int64_t)H * W;
+  for (int64_t pix = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pix < npix;
+       pix += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(pix / W);
+    uint8_t* out = stack + pix * Cb;
+    uint32_t word = 0;
+    int nib = 0, nbytes = 0;
+    auto emit = [&](uint32_t bit) {
+      word |= (bit * kFp4One) << (4 * nib);
+      if (++nib == 8) {
+        if constexpr (WORDS) {
+          *reinterpret_cast<uint32_t*>(out + nbytes) = word;
+        } else {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int ce = 2 * cb + h;
-      const int p = ce / C4, k = ce % C4, m = k / C, ch = k % C;
-      if (r + p < H) {
-        const int64_t j = ((int64_t)(r + p) * W + c) * C + ch;
-        if (edge_bit((m < 2) ? gh[j] : gv[j], m, th_h, th_v)) byte |= kFp4One << (4 * h);
+          for (int q = 0; q < 4; ++q) out[nbytes + q] = (uint8_t)(word >> (8 * q));
+        }
+        nbytes += 4;
+        word = 0;
+        nib = 0;
+      }
+    };
+    for (int p = 0; p < e; ++p) {
+      const bool in = r + p < H;
+      const int64_t j0 = (pix + (int64_t)p * W) * C;
+      for (int m = 0; m < 4; ++m) {
+        const double* g = m < 2 ? gh : gv;
+        for (int ch = 0; ch < C; ++ch) emit(in ? edge_bit(g[j0 + ch], m, th_h, th_v) : 0u);
       }
     }
-    stack[i] = byte;
+    for (int q = 0; 2 * q < nib; ++q) out[nbytes + q] = (uint8_t)(word >> (8 * q));  // tail
   }
 }
 
@@ -238,6 +258,46 @@ __global__ void channel_mean_kernel(const double* __restrict__ t, int64_t npix, 
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npix;
        i += (int64_t)gridDim.x * blockDim.x)
     mag[i] = __ddiv_rn(pairwise_sum(t + i * C, C), (double)C);
+}
+
+// mag = mean_c sqrt(gh^2 + gv^2) straight from stored Sobel gradients (the
+// same values grad_mag_kernel recomputes from x): the block stages its 256
+// pixels' per-channel magnitudes in shared memory with coalesced loads (row
+// stride C|1 doubles: conflict-free per-thread rows), then each thread takes
+// numpy's pairwise mean of its row.
+__global__ void grad_mean_kernel(const double* __restrict__ gh, const double* __restrict__ gv,
+                                 int64_t npix, int C, double* __restrict__ mag) {
+  extern __shared__ double tm[];
+  const int ld = C | 1;
+  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x; p0 < npix;
+       p0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t left = npix - p0;
+    const int np = left < (int64_t)blockDim.x ? (int)left : (int)blockDim.x;
+    const int64_t e0 = p0 * C;
+    const int ne = np * C;
+    for (int e = threadIdx.x; e < ne; e += 4 * blockDim.x) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {  // four independent loads in flight
+        const int eu = e + u * blockDim.x;
+        a[u] = eu < ne ? gh[e0 + eu] : 0.0;
+        b[u] = eu < ne ? gv[e0 + eu] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int eu = e + u * blockDim.x;
+        if (eu < ne) {
+          const int q = eu / C;
+          tm[q * ld + (eu - q * C)] =
+              __dsqrt_rn(__dadd_rn(__dmul_rn(a[u], a[u]), __dmul_rn(b[u], b[u])));
+        }
+      }
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < np)
+      mag[p0 + threadIdx.x] = __ddiv_rn(pairwise_sum(tm + threadIdx.x * ld, C), (double)C);
+    __syncthreads();
+  }
 }
 
 // structure-tensor products of the Sobel gradients of mag
@@ -726,7 +786,10 @@ extern "C" int glr_sobel(const double* x_d, int H, int W, int C, double* gh_d, d
   GLR_REQUIRE(C >= 1, GLR_ERR_INVALID, "channel count %d", C);
   cudaStream_t st = (cudaStream_t)stream;
   int64_t n = (int64_t)H * W * C;
-  sobel_kernel<<<grid_for(n), 256, 0, st>>>(x_d, H, W, C, gh_d, gv_d);
+  if (n < (int64_t)INT32_MAX - 65536LL * 256)
+    sobel_kernel<int><<<grid_for(n), 256, 0, st>>>(x_d, H, W, C, gh_d, gv_d);
+  else
+    sobel_kernel<int64_t><<<grid_for(n), 256, 0, st>>>(x_d, H, W, C, gh_d, gv_d);
   return check_launch("sobel_kernel");
 }
 
@@ -749,8 +812,12 @@ extern "C" int glr_edge_stack(const double* gh_d, const double* gv_d, int H, int
     GLR_CUDA(cudaGetLastError());
   }
   if (stack_d) {
-    edge_stack_kernel<<<grid_for(n * 2 * expand), 256, 0, st>>>(gh_d, gv_d, H, W, C, expand, t, mx,
-                                                                 stack_d);
+    if ((expand * C) % 2 == 0)
+      edge_stack_kernel<true><<<grid_for((int64_t)H * W), 256, 0, st>>>(gh_d, gv_d, H, W, C,
+                                                                        expand, t, mx, stack_d);
+    else
+      edge_stack_kernel<false><<<grid_for((int64_t)H * W), 256, 0, st>>>(gh_d, gv_d, H, W, C,
+                                                                         expand, t, mx, stack_d);
     GLR_CUDA(cudaGetLastError());
   }
   return GLR_OK;
@@ -795,6 +862,38 @@ extern "C" int glr_corner_response(const double* x_d, int H, int W, int C, doubl
                                                                   pxy);
   min_eig_kernel<<<grid_for(npix), 256, 0, st>>>(pxx, pyy, pxy, npix, resp_d);
   return check_launch("corner_response");
+}
+
+// Same response from precomputed Sobel gradients (glr_sobel), skipping the
+// second Sobel pass over x.
+extern "C" int glr_corner_response_grad(const double* gh_d, const double* gv_d, int H, int W,
+                                        int C, double* resp_d, void* ws_d, void* stream) {
+  GLR_REQUIRE(H >= 3 && W >= 3, GLR_ERR_INVALID, "image %dx%d too small for 3x3 Sobel", H, W);
+  GLR_REQUIRE(C >= 1 && C <= 256, GLR_ERR_INVALID, "channel count %d", C);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t npix = (int64_t)H * W;
+  double* mag = reinterpret_cast<double*>(ws_d) + npix * C;  // glr_corner_workspace layout
+  double* pxx = mag + npix;
+  double* pyy = pxx + npix;
+  double* pxy = pyy + npix;
+  double* qxx = pxy + npix;
+  double* qyy = qxx + npix;
+  double* qxy = qyy + npix;
+  const int smem = 256 * (C | 1) * (int)sizeof(double);
+  static int attr_done = 0;
+  if (smem > 48 * 1024 && smem > attr_done) {
+    GLR_CUDA(cudaFuncSetAttribute(grad_mean_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem));
+    attr_done = smem;
+  }
+  grad_mean_kernel<<<grid_for(npix), 256, smem, st>>>(gh_d, gv_d, npix, C, mag);
+  st_products_kernel<<<grid_for(npix), 256, 0, st>>>(mag, H, W, pxx, pyy, pxy);
+  box3_cols_kernel<<<dim3((unsigned)cdiv(W, 128), 3), 128, 0, st>>>(pxx, pyy, pxy, H, W, qxx, qyy,
+                                                                  qxy);
+  box3_rows_kernel<<<dim3((unsigned)cdiv(H, 128), 3), 128, 0, st>>>(qxx, qyy, qxy, H, W, pxx, pyy,
+                                                                  pxy);
+  min_eig_kernel<<<grid_for(npix), 256, 0, st>>>(pxx, pyy, pxy, npix, resp_d);
+  return check_launch("corner_response_grad");
 }
 
 static size_t nms_sort_temp(int64_t n) {

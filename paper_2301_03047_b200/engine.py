@@ -7,8 +7,8 @@ the int64 fixed-point aggregation numerator and the int32 counter. One
 iteration is a fixed sequence of libglr_b200 launches on one stream:
 
   refresh (every match_refresh_interval iterations, solvers.py:185-203)
-      corner response -> NMS corners -> anchors (+ uniform grid)
-      Sobel -> sign-split edge stack
+      Sobel -> corner response -> NMS corners -> anchors (+ uniform grid)
+      sign-split edge stack
       heat map (tcgen05) -> exact top-K positions       [per exemplar shard]
       counter of covered pixels                         [+ all-reduce]
   every iteration (solvers.py:204-210, 298-301)
@@ -171,9 +171,10 @@ class GlrEngine:
         self.stride = N.query("glr_heat_stride", h, w, p)
         # buffers
         self.resp = D.empty((h, w), t.float64)
-        if self.global_match:
+        if self.global_match or self.use_corners:  # Sobel gradients: corners + edge stack
             self.gh = D.empty((h, w, c), t.float64)
             self.gv = D.empty((h, w, c), t.float64)
+        if self.global_match:
             self.stack = D.empty((h * w * 2 * c * self.expand,), t.uint8)  # packed fp4
         self.corners = D.empty((max(match.max_corners, 1), 2), t.int32)
         self.n_corners = D.zeros((1,), t.int32)
@@ -260,10 +261,16 @@ class GlrEngine:
         h, w, c = self.shape
         mc = self.mc
         s = D.stream()
+        if self.use_corners or self.global_match:
+            # one Sobel pass feeds both the corner response and the edge stack
+            e = self._ev()
+            N.call("glr_sobel", x_d.data_ptr(), h, w, c, self.gh.data_ptr(), self.gv.data_ptr(),
+                   s)
+            self._log(("sobel", 1), e)
         if self.use_corners:
             e = self._ev()
-            N.call("glr_corner_response", x_d.data_ptr(), h, w, c, self.resp.data_ptr(),
-                   self.ws_corner.data_ptr(), s)
+            N.call("glr_corner_response_grad", self.gh.data_ptr(), self.gv.data_ptr(), h, w, c,
+                   self.resp.data_ptr(), self.ws_corner.data_ptr(), s)
             self._log(("corner_response", 1), e)
             e = self._ev()
             N.call("glr_corners", self.resp.data_ptr(), h, w, mc.max_corners, mc.nms,
@@ -293,8 +300,6 @@ class GlrEngine:
             return 0
         if self.global_match:
             e = self._ev()
-            N.call("glr_sobel", x_d.data_ptr(), h, w, c, self.gh.data_ptr(), self.gv.data_ptr(),
-                   s)
             N.call("glr_edge_stack", self.gh.data_ptr(), self.gv.data_ptr(), h, w, c,
                    float(mc.edge_threshold), 1, self.expand, None, self.stack.data_ptr(),
                    self.ws_edge.data_ptr(), s)

@@ -869,7 +869,7 @@ extern "C" int glr_corner_response(const double* x_d, int H, int W, int C, doubl
 extern "C" int glr_corner_response_grad(const double* gh_d, const double* gv_d, int H, int W,
                                         int C, double* resp_d, void* ws_d, void* stream) {
   GLR_REQUIRE(H >= 3 && W >= 3, GLR_ERR_INVALID, "image %dx%d too small for 3x3 Sobel", H, W);
-  GLR_REQUIRE(C >= 1 && C <= 256, GLR_ERR_INVALID, "channel count %d", C);
+  GLR_REQUIRE(C >= 1 && C <= 6000, GLR_ERR_INVALID, "channel count %d", C);
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t npix = (int64_t)H * W;
   double* mag = reinterpret_cast<double*>(ws_d) + npix * C;  // glr_corner_workspace layout
@@ -879,14 +879,17 @@ extern "C" int glr_corner_response_grad(const double* gh_d, const double* gv_d, 
   double* qxx = pxy + npix;
   double* qyy = qxx + npix;
   double* qxy = qyy + npix;
-  const int smem = 256 * (C | 1) * (int)sizeof(double);
+  // 256 pixels per block, fewer for wide channel counts (<= 200 KB staging)
+  const int row_bytes = (C | 1) * (int)sizeof(double);
+  const int threads = std::max(32, std::min(256, (200 * 1024 / row_bytes) / 32 * 32));
+  const int smem = threads * row_bytes;
   static int attr_done = 0;
   if (smem > 48 * 1024 && smem > attr_done) {
     GLR_CUDA(cudaFuncSetAttribute(grad_mean_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   smem));
     attr_done = smem;
   }
-  grad_mean_kernel<<<grid_for(npix), 256, smem, st>>>(gh_d, gv_d, npix, C, mag);
+  grad_mean_kernel<<<grid_for(npix, threads), threads, smem, st>>>(gh_d, gv_d, npix, C, mag);
   st_products_kernel<<<grid_for(npix), 256, 0, st>>>(mag, H, W, pxx, pyy, pxy);
   box3_cols_kernel<<<dim3((unsigned)cdiv(W, 128), 3), 128, 0, st>>>(pxx, pyy, pxy, H, W, qxx, qyy,
                                                                   qxy);

@@ -59,11 +59,20 @@ def test_corner_response_bitwise_vs_oracle(rng):
     import torch
     for (h, w, c) in [(64, 48, 1), (40, 40, 8), (33, 65, 24), (20, 21, 9), (16, 16, 130)]:
         x = rng.random((h, w, c)).astype(np.float32).astype(np.float64)
+        x_d = D.f64(x)
         resp = D.empty((h, w), torch.float64)
         ws = D.workspace().get("cr", N.query("glr_corner_workspace", h, w, c))
-        N.call("glr_corner_response", D.f64(x).data_ptr(), h, w, c, resp.data_ptr(),
+        N.call("glr_corner_response", x_d.data_ptr(), h, w, c, resp.data_ptr(),
                ws.data_ptr(), D.stream())
-        assert np.array_equal(D.host(resp), O.corner_response(x)), (h, w, c)
+        want = O.corner_response(x)
+        assert np.array_equal(D.host(resp), want), (h, w, c)
+        # the engine's entry: the same response from stored Sobel gradients
+        gh, gv = D.empty((h, w, c), torch.float64), D.empty((h, w, c), torch.float64)
+        N.call("glr_sobel", x_d.data_ptr(), h, w, c, gh.data_ptr(), gv.data_ptr(), D.stream())
+        resp2 = D.empty((h, w), torch.float64)
+        N.call("glr_corner_response_grad", gh.data_ptr(), gv.data_ptr(), h, w, c,
+               resp2.data_ptr(), ws.data_ptr(), D.stream())
+        assert np.array_equal(D.host(resp2), want), (h, w, c)
 
 
 def test_heat_topk_global_match_bitwise_vs_golden():

@@ -106,9 +106,84 @@ def check(rows):
     return True
 
 
+def plane_spread():
+    """The 9 planes (3-dim subspaces) alpha^i * GF(8) of GF(64), i = 0..8:
+    they partition the 63 nonzero vectors (octet schedule of eig_kernel<true>)."""
+    alpha = 0b10
+    beta = gf_pow(alpha, 9)  # order 7: GF(8)* inside GF(64)*
+    planes = []
+    for i in range(9):
+        x = gf_pow(alpha, i)
+        basis = [x, gf_mul(x, beta), gf_mul(x, gf_mul(beta, beta))]
+        assert len(span(basis)) == 8
+        planes.append(basis)
+    allv = set()
+    for b in planes:
+        allv |= span(b) - {0}
+    assert len(allv) == 63
+    return planes
+
+
+def plane_complement(s):
+    # t0..t2 with span(S, T) = all and the 8 representatives in 8 distinct
+    # low-3-bit classes (spread over shared-memory banks)
+    def rec(basis):
+        if len(basis) == 3:
+            T = span(basis)
+            if len(span(basis + s)) == 64 and len({t & 7 for t in T}) == 8:
+                return basis
+            return None
+        start = basis[-1] + 1 if basis else 1
+        for v in range(start, 64):
+            if v in span(basis + s):
+                continue
+            if (v & 7) in {t & 7 for t in span(basis)}:
+                continue
+            r = rec(basis + [v])
+            if r:
+                return r
+        return None
+    return rec([])
+
+
+def octet_table():
+    rows = []
+    for s in plane_spread():
+        rows.append((*s, *plane_complement(s)))
+    return rows
+
+
+def check_octets(rows):
+    seen = set()
+    for s0, s1, s2, t0, t1, t2 in rows:
+        S, T = [0] * 8, [0] * 8
+        for l in range(8):
+            for k, v in enumerate((s0, s1, s2)):
+                if (l >> k) & 1:
+                    S[l] ^= v
+            for k, v in enumerate((t0, t1, t2)):
+                if (l >> k) & 1:
+                    T[l] ^= v
+        assert len({t & 7 for t in T}) == 8
+        for B in range(8):
+            o = [T[B] ^ S[l] for l in range(8)]
+            for i in range(8):
+                for j in range(i + 1, 8):
+                    pr = (min(o[i], o[j]), max(o[i], o[j]))
+                    assert pr not in seen
+                    seen.add(pr)
+    assert len(seen) == 64 * 63 // 2
+    return True
+
+
 if __name__ == "__main__":
     rows = table()
     check(rows)
     print("// {a, b, g0, g1, g2, g3} per super-round (tools/jacobi_schedule.py)")
     for r in rows:
+        print("    {" + ", ".join(str(v) for v in r) + "},")
+    orows = octet_table()
+    check_octets(orows)
+    print("// {s0, s1, s2, t0, t1, t2} per octet super-round (tools/jacobi_schedule.py)")
+    for r in orows:
         print("    {" + ", ".join(str(v) for v in r) + "},")

@@ -38,6 +38,15 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "GLR iters/s (C2 1024x1024x24 CACTI GAP-GLR, 50 it, 4096 exemplars, K=64)"
+
+
+def metric_for(wl) -> str:
+    """The headline metric string (C2) or its analogue for another config."""
+    if wl.name == "C2":
+        return METRIC
+    h, w, c = wl.shape
+    return (f"GLR iters/s ({wl.name} {h}x{w}x{c} {wl.kind.upper()} GAP-GLR, {wl.max_iters} it, "
+            f"{wl.match.max_corners} max corners, K={wl.match.group_size})")
 UNIT = "iters/s"
 FP64_DMMA_PEAK = 37.1  # TFLOP/s, measured on B200 (tools/micro/dmma.cu, profiles/r01_fp64_peak.md)
 
@@ -180,7 +189,7 @@ def run_reference(args, rank):
     wall = time.perf_counter() - t_start
     v = float(statistics.mean(vals))
     line = {
-        "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference",
+        "metric": metric_for(wl), "value": v, "unit": UNIT, "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -348,7 +357,8 @@ def run_b200(args, rank, world, local_rank):
         roofline["peak_source"] = f"{peak_src} (MEASURED_PEAKS.json)" if peak_src == "measured" \
             else "fallback (B200_PROFILING.md)"
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": metric_for(wl), "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64+e2m1",
             "data": "synthetic (seeded generator, workloads.py)",

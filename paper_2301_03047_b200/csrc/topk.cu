@@ -219,7 +219,10 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   //    positions reach L (or the row is not a heat map), a second pass adds
   //    the bins below L -- the cut is exact either way.
   const int64_t aidx = (int64_t)p.anchors[2 * n] * p.ow + p.anchors[2 * n + 1];
-  const int L = min((int)row[aidx] >> 2, p.bins - 1);
+#ifndef GLR_TOPK_FLOOR_SHIFT
+#define GLR_TOPK_FLOOR_SHIFT 2
+#endif
+  const int L = min((int)row[aidx] >> GLR_TOPK_FLOOR_SHIFT, p.bins - 1);
   for (int b = L + tid; b < p.bins; b += THREADS) hist[b] = 0;
   __shared__ __align__(8) uint64_t s_full[topk::RING_STAGES], s_empty[topk::RING_STAGES];
   if (tid == 0) {

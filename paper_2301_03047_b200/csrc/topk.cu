@@ -219,11 +219,49 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   //    positions reach L (or the row is not a heat map), a second pass adds
   //    the bins below L -- the cut is exact either way.
   const int64_t aidx = (int64_t)p.anchors[2 * n] * p.ow + p.anchors[2 * n + 1];
-#ifndef GLR_TOPK_FLOOR_SHIFT
-#define GLR_TOPK_FLOOR_SHIFT 2
-#endif
-  const int L = min((int)row[aidx] >> GLR_TOPK_FLOOR_SHIFT, p.bins - 1);
-  for (int b = L + tid; b < p.bins; b += THREADS) hist[b] = 0;
+  const int L0 = min((int)row[aidx] >> 2, p.bins - 1);
+  // Sampled floor: 2048 evenly spaced 16-byte chunks (16 K scores) estimate
+  // the score distribution above L0; the floor L is raised to the highest
+  // score the sample puts about kFloorSafety x `need` positions above, so the
+  // single pass records a few thousand entries whatever the row's
+  // distribution (few channels: far more positions pass a quarter of the
+  // self-score). If the row has fewer than `need` positions >= L after all,
+  // the exact fallback below adds the lower bins (second read).
+  for (int b = L0 + tid; b < p.bins; b += THREADS) hist[b] = 0;
+  if (tid == 0) s_T = L0;
+  __syncthreads();
+  {
+    constexpr int SPT = 4, kFloorSafety = 4;
+    const int nchk = (int)((M + VEC - 1) / VEC);
+    const int ns = THREADS * SPT;
+    if (nchk > 4 * ns) {
+      const uint4* rv = reinterpret_cast<const uint4*>(row);
+#pragma unroll
+      for (int u = 0; u < SPT; ++u) {
+        const int si = u * THREADS + tid;
+        const int ci = (int)(((int64_t)si * nchk) / ns);
+        const uint4 v = rv[ci];
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          const int val = min((int)((j & 1) ? wv[j >> 1] >> 16 : wv[j >> 1] & 0xFFFFu), p.bins - 1);
+          if ((int64_t)ci * VEC + j < M && val >= L0) atomicAdd(&hist[val], 1);
+        }
+      }
+      __syncthreads();
+      if (warp == 0) {
+        const int64_t want = ((int64_t)kFloorSafety * need * ns * VEC + M - 1) / M;
+        int T, cntA;
+        bool found;
+        topk_cut(hist, p.bins, L0, want > 1 ? (int)want : 1, T, cntA, found);
+        if (lane == 0 && found) s_T = max(T, L0);
+      }
+      __syncthreads();
+      for (int b = L0 + tid; b < p.bins; b += THREADS) hist[b] = 0;
+    }
+  }
+  __syncthreads();
+  const int L = s_T;
   __shared__ __align__(8) uint64_t s_full[topk::RING_STAGES], s_empty[topk::RING_STAGES];
   if (tid == 0) {
     for (int r = 0; r < RING_STAGES; ++r) {

@@ -30,12 +30,9 @@ constexpr int GLD = KMAX + 2;     // row stride of G in the eigen kernel (pair r
 constexpr int VLD = KMAX + 1;     // row stride of V^T in the eigen kernel
 constexpr int GROWS = 32;         // rows of M per Gram tile
 constexpr int GRS = GROWS + 4;    // column stride of the Gram tiles (== 4 mod 16)
-constexpr int AROWS = 64;         // rows of M per apply tile (APPLY_RPW 8-row fragments per warp)
-constexpr int ARS = AROWS + 8;    // column stride of the apply tiles (== 8 mod 16)
 constexpr int GRAM_THREADS = 128; // four warps, 9 of the 36 upper-triangle 8x8 tiles each
 constexpr int EIG_THREADS = 256;
 constexpr int APPLY_THREADS = 256;
-constexpr int APPLY_RPW = 1;      // 8-row fragments per warp in the apply kernel
 #ifdef GLR_EIG_MAXSWEEPS  // dev experiments only
 constexpr int MAX_SWEEPS = GLR_EIG_MAXSWEEPS;
 #else
@@ -580,88 +577,82 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// K3: out = M Wm on DMMA over 64-row tiles (column stride ARS = 72 == 8 mod
-// 16 doubles), Wm in shared memory (row stride LD = 68 == 4 mod 16). Warp w
-// owns tile row w (8 rows) x all 8 column tiles: per k-step one A fragment
-// and eight B fragments feed eight DMMAs. The denoised patch entries go to
-// the int64 fixed-point numerator with integer atomics (or to `out`).
+// K3: out = M Wm on DMMA over TR-row tiles of M (cp.async double-buffered,
+// column stride TR + 8 or TR + 4: 8 or 4 mod 16 doubles), Wm in shared
+// memory (row stride LD = 68 == 4 mod 16). Warp w owns row fragment w % RF
+// (8 rows) x NCT = RF column tiles: per k-step one A fragment and NCT B
+// fragments feed NCT DMMAs. TR = 32 halves the tile buffers so three CTAs
+// fit an SM. The denoised patch entries go to the int64 fixed-point
+// numerator with integer atomics (or to `out`).
 
-template <bool IMG>
+template <bool IMG, int TR>
 __global__ void __launch_bounds__(wn::APPLY_THREADS)
     apply_kernel(GroupSrc s, int n, const double* __restrict__ Wm, double scale,
                  int64_t* __restrict__ acc_out, double* __restrict__ out) {
   using namespace wn;
+  constexpr int TRS = TR + (TR == 64 ? 8 : 4);  // tile column stride
+  constexpr int RF = TR / 8;                    // row fragments per tile
+  constexpr int NCT = RF;                       // column tiles per warp (8 warps)
   extern __shared__ __align__(16) double sm[];
   double* Ws = sm;              // KMAX x LD
-  double* T = Ws + KMAX * LD;   // 2 x KMAX x ARS
+  double* T = Ws + KMAX * LD;   // 2 x KMAX x TRS
   __shared__ long long cbase[KMAX];
   const int g = blockIdx.x;
   if (g >= n) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int K = s.K, m = s.m;
+  const int rf = warp % RF, ct0 = (warp / RF) * NCT;
   if (tid < KMAX) cbase[tid] = tid < K ? col_base<IMG>(s, g, tid) : 0;
   __syncthreads();
-  fill_tile<APPLY_THREADS / 32>(T, s, cbase, 0, AROWS, ARS);
+  fill_tile<APPLY_THREADS / 32>(T, s, cbase, 0, TR, TRS);
   const double* Wg = Wm + (size_t)g * GSZ;
   for (int t = tid; t < GSZ / 2; t += APPLY_THREADS) {
     const int i = (2 * t) >> 6, j = (2 * t) & 63;
     *reinterpret_cast<double2*>(&Ws[i * LD + j]) = reinterpret_cast<const double2*>(Wg)[t];
   }
   const int ar = lane >> 2, ak = lane & 3;
-  const int ntiles = (m + AROWS - 1) / AROWS;
+  const int ntiles = (m + TR - 1) / TR;
   for (int tt = 0; tt < ntiles; ++tt) {
-    const int r0 = tt * AROWS;
+    const int r0 = tt * TR;
     if (tt + 1 < ntiles)
-      fill_tile<APPLY_THREADS / 32>(T + ((tt + 1) & 1) * KMAX * ARS, s, cbase, r0 + AROWS,
-                                    AROWS, ARS);
+      fill_tile<APPLY_THREADS / 32>(T + ((tt + 1) & 1) * KMAX * TRS, s, cbase, r0 + TR, TR, TRS);
     else
       cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    const double* R = T + (tt & 1) * KMAX * ARS;
-    double o[APPLY_RPW][8][2];
+    const double* R = T + (tt & 1) * KMAX * TRS;
+    double o[NCT][2];
 #pragma unroll
-    for (int f = 0; f < APPLY_RPW; ++f)
-#pragma unroll
-      for (int b = 0; b < 8; ++b) o[f][b][0] = o[f][b][1] = 0.0;
+    for (int b = 0; b < NCT; ++b) o[b][0] = o[b][1] = 0.0;
 #pragma unroll 4
     for (int k0 = 0; k0 < KMAX; k0 += 4) {  // zero columns beyond K contribute nothing
-      double fa[APPLY_RPW];
+      const double fa = R[(k0 + ak) * TRS + 8 * rf + ar];
 #pragma unroll
-      for (int f = 0; f < APPLY_RPW; ++f)
-        fa[f] = R[(k0 + ak) * ARS + 8 * (APPLY_RPW * warp + f) + ar];
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        const double fb = Ws[(k0 + ak) * LD + 8 * b + ar];
-#pragma unroll
-        for (int f = 0; f < APPLY_RPW; ++f) dmma(o[f][b][0], o[f][b][1], fa[f], fb);
-      }
+      for (int b = 0; b < NCT; ++b)
+        dmma(o[b][0], o[b][1], fa, Ws[(k0 + ak) * LD + 8 * (ct0 + b) + ar]);
     }
+    const int r = r0 + 8 * rf + ar;
+    if (r < m) {
+      const int64_t off = (int64_t)(r / s.PC) * s.rs + (r % s.PC);
 #pragma unroll
-    for (int f = 0; f < APPLY_RPW; ++f) {
-      const int r = r0 + 8 * (APPLY_RPW * warp + f) + ar;
-      if (r < m) {
-        const int64_t off = (int64_t)(r / s.PC) * s.rs + (r % s.PC);
+      for (int b = 0; b < NCT; ++b)
 #pragma unroll
-        for (int b = 0; b < 8; ++b)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int j = 8 * b + 2 * ak + e;
-            if (j < K) {
-              if constexpr (IMG) {
-                const long long val = __double2ll_rn(o[f][b][e] * scale);
+        for (int e = 0; e < 2; ++e) {
+          const int j = 8 * (ct0 + b) + 2 * ak + e;
+          if (j < K) {
+            if constexpr (IMG) {
+              const long long val = __double2ll_rn(o[b][e] * scale);
 #ifdef GLR_DEV_APPLY_NOATOMIC  // dev experiment: cost of the scatter atomics
-                if (val == 0x7edcba9876543210ll) acc_out[cbase[j] + off] = val;
+              if (val == 0x7edcba9876543210ll) acc_out[cbase[j] + off] = val;
 #else
-                atomicAdd(reinterpret_cast<unsigned long long*>(acc_out + cbase[j] + off),
-                          (unsigned long long)val);
+              atomicAdd(reinterpret_cast<unsigned long long*>(acc_out + cbase[j] + off),
+                        (unsigned long long)val);
 #endif
-              } else {
-                out[cbase[j] + off] = o[f][b][e];
-              }
+            } else {
+              out[cbase[j] + off] = o[b][e];
             }
           }
-      }
+        }
     }
     __syncthreads();
   }
@@ -830,7 +821,12 @@ static int blocks_for(int64_t n, int threads = 256) {
 
 constexpr size_t kGramSmem = 2 * wn::KMAX * wn::GRS * sizeof(double);
 constexpr size_t kEigSmem = wn::KMAX * (wn::GLD + wn::VLD) * sizeof(double);
-constexpr size_t kApplySmem = (wn::KMAX * wn::LD + 2 * wn::KMAX * wn::ARS) * sizeof(double);
+#ifndef GLR_APPLY_TR  // apply tile rows: 32 (3 CTAs/SM) measured 2.17 ms vs 2.21 for 64 on C2
+#define GLR_APPLY_TR 32
+#endif
+constexpr int kApplyTR = GLR_APPLY_TR;
+constexpr size_t kApplySmem =
+    (wn::KMAX * wn::LD + 2 * wn::KMAX * (kApplyTR + (kApplyTR == 64 ? 8 : 4))) * sizeof(double);
 // Gram -> eigen/shrink -> apply for n groups; ws holds n x 64 x 64 doubles.
 template <bool IMG>
 static int run_wnnm(const GroupSrc& s, int n, const EigArgs& ea_in, double scale,
@@ -841,7 +837,7 @@ static int run_wnnm(const GroupSrc& s, int n, const EigArgs& ea_in, double scale
                                   (int)kGramSmem));
     GLR_CUDA(cudaFuncSetAttribute(eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kEigSmem));
-    GLR_CUDA(cudaFuncSetAttribute(apply_kernel<IMG>,
+    GLR_CUDA(cudaFuncSetAttribute(apply_kernel<IMG, kApplyTR>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem));
     attrs = true;
   }
@@ -852,7 +848,8 @@ static int run_wnnm(const GroupSrc& s, int n, const EigArgs& ea_in, double scale
   ea.n = n;
   eig_kernel<<<n, wn::EIG_THREADS, kEigSmem, st>>>(ea);
   GLR_CUDA(cudaGetLastError());
-  apply_kernel<IMG><<<n, wn::APPLY_THREADS, kApplySmem, st>>>(s, n, ws, scale, acc_out, out);
+  apply_kernel<IMG, kApplyTR><<<n, wn::APPLY_THREADS, kApplySmem, st>>>(s, n, ws, scale, acc_out,
+                                                                        out);
   return check_launch("wnnm kernels");
 }
 

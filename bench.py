@@ -280,7 +280,15 @@ def run_b200(args, rank, world, local_rank):
     if wl.kind != "fourier":
         op_host.meta["masks"] = pin(op_host.meta["masks"])
         op_host.gram_diag = pin(op_host.gram_diag)
-        h2d = y_host.nbytes + op_host.meta["masks"].nbytes + op_host.gram_diag.nbytes
+        if "masks_u8" in op_host.meta:
+            # binary masks travel as their 1-byte copy (operators._binary_u8);
+            # CACTI's gram is then formed on device
+            op_host.meta["masks_u8"] = pin(op_host.meta["masks_u8"])
+            op_host.meta["masks_u8_of"] = id(op_host.meta["masks"])
+            h2d = y_host.nbytes + op_host.meta["masks_u8"].nbytes + \
+                (0 if wl.kind == "cacti" else op_host.gram_diag.nbytes)
+        else:
+            h2d = y_host.nbytes + op_host.meta["masks"].nbytes + op_host.gram_diag.nbytes
     else:
         op_host.meta["mask"] = pin(op_host.meta["mask"])
         h2d = 2 * y_host.nbytes + op_host.meta["mask"].nbytes

@@ -44,10 +44,22 @@ class DeviceOperator:
         h, w, c = op.x_shape
         self.shape = (h, w, c)
         if op.kind in ("cacti", "msfa"):
-            masks = np.asarray(op.meta["masks"], dtype=np.float64)
-            self.masks = D.f64(masks)
-            gram = np.asarray(op.gram_diag, dtype=np.float64).reshape(h, w)
-            self.gram = D.f64(gram)
+            u8 = op.meta.get("masks_u8")
+            if u8 is not None and (op.meta.get("masks_u8_of") != id(op.meta["masks"])
+                                   or u8.shape != (h, w, c)):
+                u8 = None  # meta["masks"] replaced since the operator was built
+            if u8 is not None and op.kind == "cacti":
+                # binary masks: 1-byte upload, widened on device; gram = sum_t M_t^2
+                # = the count of ones (exact), formed on device as well
+                m8 = D.to_dev(np.ascontiguousarray(u8))
+                self.masks = m8.to(t.float64)
+                self.gram = m8.sum(dim=2, dtype=t.int32).to(t.float64).contiguous()
+            elif u8 is not None:
+                self.masks = D.to_dev(np.ascontiguousarray(u8)).to(t.float64)
+                self.gram = D.f64(np.asarray(op.gram_diag, dtype=np.float64).reshape(h, w))
+            else:
+                self.masks = D.f64(np.asarray(op.meta["masks"], dtype=np.float64))
+                self.gram = D.f64(np.asarray(op.gram_diag, dtype=np.float64).reshape(h, w))
             self.y_shape = (h, w, 1)
         elif op.kind == "fourier":
             self.mask = D.f64(np.asarray(op.meta["mask"], dtype=np.float64))

@@ -79,6 +79,18 @@ def cacti_adjoint(y: np.ndarray, masks: np.ndarray) -> np.ndarray:
     return _masksum_adjoint(y, masks)
 
 
+def _binary_u8(masks: np.ndarray) -> dict:
+    """Compact copy of binary {0, 1} masks (checked once when the operator is
+    built): the device path uploads these 8x smaller bytes and widens them
+    on the GPU (and, for CACTI, forms gram = sum_t M_t there: exact integer
+    counts), instead of the float64 masks and gram."""
+    u8 = masks.astype(np.uint8)
+    if not np.array_equal(u8, masks):
+        return {}
+    # tied to this masks object: replacing meta["masks"] disables the copy
+    return {"masks_u8": u8, "masks_u8_of": id(masks)}
+
+
 def cacti_operator(masks: np.ndarray) -> SensingOperator:
     """operators.py:49-59."""
     masks = np.asarray(masks, dtype=np.float64)
@@ -89,7 +101,7 @@ def cacti_operator(masks: np.ndarray) -> SensingOperator:
         adjoint=lambda y: cacti_adjoint(y, masks),
         gram_diag=(masks ** 2).sum(axis=2, keepdims=True),
         x_shape=(h, w, t),
-        meta={"masks": masks},
+        meta={"masks": masks, **_binary_u8(masks)},
     )
 
 
@@ -128,7 +140,7 @@ def msfa_operator(masks: np.ndarray) -> SensingOperator:
         adjoint=lambda y: msfa_adjoint(y, masks),
         gram_diag=np.ones((h, w, 1)),
         x_shape=(h, w, c),
-        meta={"masks": masks},
+        meta={"masks": masks, **_binary_u8(masks)},
     )
 
 

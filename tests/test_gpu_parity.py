@@ -378,3 +378,25 @@ def test_report_ssim_matches_host_formula():
     x, rep = G.gap_solve(op, g["y0"], cfg, ref=g["scene0"])
     assert abs(rep.rows[-1]["ssim"] - O.ssim(g["scene0"], x, 1.0)) <= 1e-10
     assert all(0.0 < r["ssim"] <= 1.0 for r in rep.rows)
+
+
+def test_binary_mask_upload_path_is_bitwise_identical(rng):
+    """Binary masks travel as their 1-byte copy (gram formed on device); the
+    solve must not change bit for bit against the float64 upload."""
+    h, w, t = 40, 36, 6
+    scene = rng.random((h, w, t)).astype(np.float32).astype(np.float64)
+    masks = G.bernoulli_masks(h, w, t, seed=7)
+    op = G.cacti_operator(masks)
+    assert "masks_u8" in op.meta
+    y = op.forward(scene)
+    cfg = G.SolverConfig(max_iters=6, match=G.MatchConfig(patch_size=4, group_size=16,
+                                                          max_corners=30))
+    a, _ = G.gap_solve(op, y, cfg)
+    op_f64 = G.cacti_operator(masks)
+    op_f64.meta.pop("masks_u8")
+    b, _ = G.gap_solve(op_f64, y, cfg)
+    assert np.array_equal(a, b)
+    op_swapped = G.cacti_operator(masks)
+    op_swapped.meta["masks"] = masks.copy()  # replaced: the u8 copy must not be used
+    c, _ = G.gap_solve(op_swapped, y, cfg)
+    assert np.array_equal(a, c)

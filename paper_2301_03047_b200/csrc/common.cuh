@@ -333,6 +333,22 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)
       : "r"(taddr));
 }
 
+// 32 lanes x 16 consecutive 32-bit TMEM columns -> 16 registers per thread.
+__device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+// Generic-proxy shared-memory writes -> visible to the async proxy (tcgen05.mma operands).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // 32 registers per thread -> 32 lanes x 32 consecutive 32-bit TMEM columns.
 __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
@@ -373,6 +389,15 @@ __host__ __device__ constexpr uint32_t idesc_u8_s32(uint32_t m, uint32_t n) {
   return (2u << 4)             // D format: s32
          | (0u << 7)           // A: unsigned 8-bit
          | (0u << 10)          // B: unsigned 8-bit
+         | ((n >> 3) << 17)    // N / 8
+         | ((m >> 4) << 24);   // M / 16
+}
+
+// Instruction descriptor, kind::i8: signed 8-bit A/B, s32 accumulate, K-major.
+__host__ __device__ constexpr uint32_t idesc_s8_s32(uint32_t m, uint32_t n) {
+  return (2u << 4)             // D format: s32
+         | (1u << 7)           // A: signed 8-bit
+         | (1u << 10)          // B: signed 8-bit
          | ((n >> 3) << 17)    // N / 8
          | ((m >> 4) << 24);   // M / 16
 }

@@ -117,13 +117,18 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // fragment of tile column i (G = M^T M), so a warp loads only the column
 // fragments w..7 each k-step.
 template <int W>
-__device__ __forceinline__ void gram_tile(double (&acc)[9][2], const double* Tc) {
+__device__ __forceinline__ void gram_tile(double (&acc)[9][2], const double* Tc, uint32_t& mx) {
   using namespace wn;
 #pragma unroll 2
   for (int k0 = 0; k0 < GROWS; k0 += 4) {
     double f[8];
 #pragma unroll
     for (int c = W; c < 8; ++c) f[c] = Tc[8 * c * GRS + k0];
+    if constexpr (W == 0) {  // warp 0's fragments cover the whole tile: max |M| (high
+                             // words, on the integer pipe beside the DMMAs)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) mx = max(mx, (uint32_t)__double2hiint(f[c]) & 0x7FFFFFFFu);
+    }
 #pragma unroll
     for (int c = W; c < 8; ++c) dmma(acc[c - W][0], acc[c - W][1], f[W], f[c]);
 #pragma unroll
@@ -134,7 +139,7 @@ __device__ __forceinline__ void gram_tile(double (&acc)[9][2], const double* Tc)
 
 template <bool IMG>
 __global__ void __launch_bounds__(wn::GRAM_THREADS)
-    gram_kernel(GroupSrc s, int n, double* __restrict__ Gout) {
+    gram_kernel(GroupSrc s, int n, double* __restrict__ Gout, double* __restrict__ gmax) {
   using namespace wn;
   extern __shared__ __align__(16) double sm[];
   double* T = sm;  // 2 x KMAX x GRS
@@ -150,6 +155,7 @@ __global__ void __launch_bounds__(wn::GRAM_THREADS)
   double acc[9][2];
 #pragma unroll
   for (int q = 0; q < 9; ++q) acc[q][0] = acc[q][1] = 0.0;
+  uint32_t mx = 0;
   const int ntiles = (s.m + GROWS - 1) / GROWS;
   fill_tile<4>(T, s, cbase, 0, GROWS, GRS);
   for (int tt = 0; tt < ntiles; ++tt) {
@@ -161,12 +167,17 @@ __global__ void __launch_bounds__(wn::GRAM_THREADS)
     __syncthreads();
     const double* Tc = T + (tt & 1) * KMAX * GRS + ar * GRS + ak;
     switch (w) {  // warp-uniform: compile-time accumulator indices per warp
-      case 0: gram_tile<0>(acc, Tc); break;
-      case 1: gram_tile<1>(acc, Tc); break;
-      case 2: gram_tile<2>(acc, Tc); break;
-      default: gram_tile<3>(acc, Tc); break;
+      case 0: gram_tile<0>(acc, Tc, mx); break;
+      case 1: gram_tile<1>(acc, Tc, mx); break;
+      case 2: gram_tile<2>(acc, Tc, mx); break;
+      default: gram_tile<3>(acc, Tc, mx); break;
     }
     __syncthreads();
+  }
+  if (w == 0) {
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    // an upper bound of max |M| with its binary exponent
+    if (lane == 0 && gmax) gmax[g] = __hiloint2double((int)mx, -1);
   }
   double* Gg = Gout + (size_t)g * GSZ;
 #pragma unroll
@@ -197,6 +208,7 @@ struct EigArgs {
   double* vcache;  // optional per-group eigenvector cache (n x 64 x 64)
   int warm;        // 0 cold, 1 start every group from vcache, 2 only where warm_flags[g]
   const uint8_t* warm_flags;
+  double* wmax;  // optional per-group max |Wm| (the split-integer apply's scale)
 };
 
 // Block-Jacobi schedule. The 63 rounds of a parallel cyclic sweep pair i
@@ -579,6 +591,21 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) Gg[(4 * bi + i) * KMAX + bj + 16 * j] = o[i][j];
+  if (a.wmax) {
+    double mx = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) mx = fmax(mx, fabs(o[i][j]));
+    for (int o2 = 16; o2 > 0; o2 >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o2));
+    __syncthreads();  // ratio[] is free again
+    if (lane == 0) ratio[warp] = mx;
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < EIG_THREADS / 32; ++w) mx = fmax(mx, ratio[w]);
+      a.wmax[g] = mx;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -661,6 +688,310 @@ __global__ void __launch_bounds__(wn::APPLY_THREADS)
     }
     __syncthreads();
   }
+}
+
+// ---------------------------------------------------------------------------
+// K3 on the tensor cores: out = M Wm as an exact-integer split product
+// (Ozaki scheme) on tcgen05 kind::i8. Each operand is scaled by a power of
+// two (per 128-row tile of M, per group for Wm) so its entries become
+// integers U with |U| <= 2^46, written as S = 6 balanced base-256 digits d_k
+// in [-128, 127] (U = sum_k d_k 256^(5-k)), one int8 "slice" per digit. The
+// 26 digit products d_k(M) e_l(Wm) with k + l <= 6 are int8 MMAs with exact
+// s32 accumulation (<= 6 x 64 x 2^14 < 2^31), one TMEM accumulator per level
+// t = k + l. The epilogue joins adjacent levels exactly in int32 (a 256 +
+// b < 2^31), the four pairs by an fp64 Horner step, and rounds once into the
+// int64 fixed-point numerator. Error: the dropped levels t >= 7 are below
+// 2^-44 of max|M| max|Wm| (worst case), the input rounding 2^-47 of the
+// tile's max per entry -- far below the 2^-40 numerator resolution and the
+// 1e-9 agreement of the fp64 path with LAPACK.
+//
+// Digit extraction is one DFMA per value: fma(v, 2^(46-E), 1.5 2^52 + BIAS)
+// leaves U + BIAS (BIAS = 128 sum_k 256^k) in the low 48 mantissa bits, whose
+// bytes are the digits + 128; a 4 x 4 byte transpose (PRMT) gathers one digit
+// of four values into a word and XOR 0x80 recentres it.
+//
+// Persistent, warp-specialised: one CTA per SM walks groups g = blockIdx.x,
+// + gridDim.x, ... (the scale exponents come from the Gram kernel's max |M|
+// and the eigen kernel's max |Wm| of each group):
+//   warps 0-7   slicers: per 128-row tile, each thread loads its row's 32
+//               values (coalesced over rows) and writes the six digit slices
+//               into a 2-stage ring of 128B-swizzled K-major shared memory
+//               (two slices per 128-byte row); per group, Wm's slices into a
+//               2-buffer B ring;
+//   warp 16     MMA issuer: per tile and half of the 64 output columns, 26
+//               digit products x 2 K-steps (M = 128, N = 32, K = 32) into one
+//               of two TMEM accumulator sets (7 levels x 32 columns each);
+//   warps 8-15  epilogue: per half, the 7 levels of 16 columns, released to
+//               the MMA issuer right after tcgen05.ld, then the atomics --
+//               the next half's MMAs and the slicing overlap them.
+
+namespace oz {
+constexpr int S = 6;                     // digits per operand
+constexpr int LV = 7;                    // levels kept: t = k + l <= 6
+constexpr int BITS = 46;                 // |U| <= 2^46
+constexpr int TR = 128;                  // rows of M per tile (UMMA M)
+constexpr int NH = 32;                   // output columns per MMA pass (UMMA N)
+constexpr int NBUF = S / 2;              // 128-byte row buffers per operand
+constexpr int A_BUF = TR * 128;          // 16 KB
+constexpr int B_BUF = wn::KMAX * 128;    // 8 KB
+constexpr int A_STAGE = NBUF * A_BUF;    // 48 KB
+constexpr int B_STAGE = NBUF * B_BUF;    // 24 KB
+constexpr int SLICERS = 256, EPI = 256;  // warps 0-7, 8-15; warp 16 issues the MMAs
+constexpr int THREADS = SLICERS + EPI + 32;
+constexpr uint32_t TMEM_COLS = 512;      // two sets of LV x NH = 224 columns (at 0, 256)
+constexpr size_t SMEM = 2 * (A_STAGE + B_STAGE) + 1024;
+// 1.5 * 2^52 + 0x808080808080 (< 2^53, exact)
+constexpr double MAGIC = 6755399441055744.0 + 141289400074368.0;
+}  // namespace oz
+
+__device__ __forceinline__ double pow2(int e) {  // 2^e for -1022 <= e <= 1023
+  return __longlong_as_double((long long)(1023 + e) << 52);
+}
+
+// smallest E >= -60 with |v| < 2^E for every |v| <= mx
+__device__ __forceinline__ int oz_exp(double mx) {
+  return max((int)((((uint32_t)__double2hiint(mx)) >> 20) & 0x7FFu) - 1022, -60);
+}
+
+__device__ __forceinline__ void named_bar(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// 16 consecutive K-values (chunk jc of 4) of row `row` -> the six slices:
+// slice k lives in buffer k / 2, bytes (k % 2) * 64 + 16 jc of the row,
+// 16-byte chunk index XOR (row % 8) (the 128B swizzle).
+__device__ __forceinline__ void oz_store16(uint8_t* buf0, int buf_bytes, int row, int jc,
+                                           const double* v, double scale) {
+  uint32_t w[oz::S][4];  // w[k][q]: digit k of values 4q .. 4q+3
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t lo[4], hi[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double t = fma(v[4 * q + i], scale, oz::MAGIC);
+      lo[i] = (uint32_t)__double2loint(t);
+      hi[i] = (uint32_t)__double2hiint(t);
+    }
+    const uint32_t x01 = __byte_perm(lo[0], lo[1], 0x5140), y01 = __byte_perm(lo[0], lo[1], 0x7362);
+    const uint32_t x23 = __byte_perm(lo[2], lo[3], 0x5140), y23 = __byte_perm(lo[2], lo[3], 0x7362);
+    const uint32_t h01 = __byte_perm(hi[0], hi[1], 0x5140), h23 = __byte_perm(hi[2], hi[3], 0x5140);
+    w[5][q] = __byte_perm(x01, x23, 0x5410) ^ 0x80808080u;  // byte 0 (least significant digit)
+    w[4][q] = __byte_perm(x01, x23, 0x7632) ^ 0x80808080u;
+    w[3][q] = __byte_perm(y01, y23, 0x5410) ^ 0x80808080u;
+    w[2][q] = __byte_perm(y01, y23, 0x7632) ^ 0x80808080u;
+    w[1][q] = __byte_perm(h01, h23, 0x5410) ^ 0x80808080u;
+    w[0][q] = __byte_perm(h01, h23, 0x7632) ^ 0x80808080u;  // byte 5 (most significant)
+  }
+#pragma unroll
+  for (int k = 0; k < oz::S; ++k) {
+    const int c = ((k & 1) * 4 + jc) ^ (row & 7);
+    *reinterpret_cast<uint4*>(buf0 + (k >> 1) * buf_bytes + row * 128 + c * 16) =
+        make_uint4(w[k][0], w[k][1], w[k][2], w[k][3]);
+  }
+}
+
+__global__ void __launch_bounds__(oz::THREADS, 1)
+    apply_oz_kernel(GroupSrc s, int n, const double* __restrict__ Wm,
+                    const double* __restrict__ gmax, const double* __restrict__ wmax,
+                    int frac_bits, int64_t* __restrict__ acc_out) {
+  using namespace oz;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sA = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint8_t* sB = sA + 2 * A_STAGE;
+  __shared__ long long cb_s[2][wn::KMAX], cb_e[2][wn::KMAX];  // per group (parity): column bases
+  __shared__ __align__(8) uint64_t full_a[2], empty_a[2], full_b[2], empty_b[2], tfull[2],
+      tempty[2];
+  __shared__ uint32_t tmem_slot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int K = s.K, m = s.m;
+  const int ntiles = (m + TR - 1) / TR;
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&full_a[i], SLICERS);
+      mbar_init(&empty_a[i], 1);
+      mbar_init(&full_b[i], SLICERS);
+      mbar_init(&empty_b[i], 1);
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], EPI);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 16) tmem_alloc<TMEM_COLS>(&tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp < 8) {
+    // ---------------- slicers ----------------
+    const int st = tid, r_loc = st & (TR - 1), jh = st >> 7;
+    int it = 0;
+    for (int g = blockIdx.x, gi = 0; g < n; g += gridDim.x, ++gi) {
+      const int pb = gi & 1;
+      if (st < wn::KMAX) cb_s[pb][st] = st < K ? col_base<true>(s, g, st) : 0;
+      // Wm -> B slices: row nn = output column j', K = j (B[nn][j] = Wm[j][nn])
+      {
+        const int nn = st & 63, jc = st >> 6;
+        const double* Wg = Wm + (size_t)g * wn::GSZ;
+        double v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = Wg[(16 * jc + i) * wn::KMAX + nn];
+        if (gi >= 2) mbar_wait(&empty_b[pb], ((gi >> 1) - 1) & 1);
+        oz_store16(sB + pb * B_STAGE, B_BUF, nn, jc, v, pow2(BITS - oz_exp(wmax[g])));
+        fence_proxy_async_smem();
+        mbar_arrive(&full_b[pb]);
+      }
+      named_bar(1, SLICERS);  // cb_s[pb] written
+      const double sc = pow2(BITS - oz_exp(gmax[g]));
+      for (int tt = 0; tt < ntiles; ++tt, ++it) {
+        const int r = tt * TR + r_loc;
+        const bool rok = r < m;
+        const double* src = s.src + (rok ? (int64_t)(r / s.PC) * s.rs + (r % s.PC) : 0);
+        double v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int j = 32 * jh + i;
+          v[i] = (rok && j < K) ? __ldg(src + cb_s[pb][j]) : 0.0;
+        }
+        const int stg = it & 1;
+        if (it >= 2) mbar_wait(&empty_a[stg], ((it >> 1) - 1) & 1);
+        uint8_t* a = sA + stg * A_STAGE;
+        oz_store16(a, A_BUF, r_loc, 2 * jh, v, sc);
+        oz_store16(a, A_BUF, r_loc, 2 * jh + 1, v + 16, sc);
+        fence_proxy_async_smem();
+        mbar_arrive(&full_a[stg]);
+      }
+    }
+  } else if (warp == 16) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_s8_s32(TR, NH);
+      int it = 0;
+      for (int g = blockIdx.x, gi = 0; g < n; g += gridDim.x, ++gi) {
+        const int pb = gi & 1;
+        mbar_wait(&full_b[pb], (gi >> 1) & 1);
+        for (int tt = 0; tt < ntiles; ++tt, ++it) {
+          const int stg = it & 1;
+          mbar_wait(&full_a[stg], (it >> 1) & 1);
+          for (int hf = 0; hf < 2; ++hf) {
+            if (it >= 1) mbar_wait(&tempty[hf], (it - 1) & 1);
+            tc_fence_after();
+            const uint32_t d0 = tmem + (uint32_t)(hf * 256);
+#pragma unroll
+            for (int k = 0; k < S; ++k)
+#pragma unroll
+              for (int l = 0; l < S; ++l)
+                if (k + l < LV) {
+#pragma unroll
+                  for (int ks = 0; ks < 2; ++ks) {
+                    const uint64_t ad = smem_desc_k_sw128(sA + stg * A_STAGE + (k >> 1) * A_BUF) +
+                                        (uint64_t)(((k & 1) * 64 + ks * 32) >> 4);
+                    const uint64_t bd =
+                        smem_desc_k_sw128(sB + pb * B_STAGE + (l >> 1) * B_BUF + hf * NH * 128) +
+                        (uint64_t)(((l & 1) * 64 + ks * 32) >> 4);
+                    // first write of level t: (k, l) = (0, t) for t < S, (1, S-1) for t = S
+                    const bool first = ks == 0 && (k == 0 || (k == 1 && l == S - 1));
+                    umma_i8(d0 + (uint32_t)((k + l) * NH), ad, bd, idesc, !first);
+                  }
+                }
+            umma_commit(&tfull[hf]);
+          }
+          umma_commit(&empty_a[stg]);
+        }
+        umma_commit(&empty_b[pb]);
+      }
+    }
+  } else {
+    // ---------------- epilogue ----------------
+    const int et = tid - SLICERS, q = warp & 3, cc = (warp - 8) >> 2;
+    int it = 0;
+    for (int g = blockIdx.x, gi = 0; g < n; g += gridDim.x, ++gi) {
+      const int pb = gi & 1;
+      if (et < wn::KMAX) cb_e[pb][et] = et < K ? col_base<true>(s, g, et) * 8 : 0;  // bytes
+      named_bar(2, EPI);
+      // value = sum_t acc_t 256^(10-t) 2^(e_m + e_w - 2 BITS) = y 2^(e_m + e_w - 60), with
+      // y = sum_t acc_t 256^(6-t) = c0 2^40 + c1 2^24 + L, c0 = acc_0 256 + acc_1, c1 =
+      // acc_2 256 + acc_3, c2 = acc_4 256 + acc_5 (exact in int32), L = c2 256 + acc_6.
+      // Fixed point: round(y 2^-R), R = 60 - e_m - e_w - frac_bits, all in integers:
+      // c0 2^(40-R) + c1 2^(24-R) + ((L + 2^(R-1)) >> R) for 10 <= R <= 24 (the normal
+      // range: |x| ~ 2^frac_bits-40 and |Wm| <= 1 give R ~ 18), a 64-bit path otherwise.
+      const int R = max(min(60 - oz_exp(gmax[g]) - oz_exp(wmax[g]) - frac_bits, 62), 0);
+      const long long half = R > 0 ? 1ll << (R - 1) : 0;
+      const bool fast = R >= 10 && R <= 24;
+      const int m0 = fast ? 1 << (40 - R) : 0, m1 = fast ? 1 << (24 - R) : 0;
+      for (int tt = 0; tt < ntiles; ++tt, ++it) {
+        const int r = tt * TR + 32 * q + lane;
+        const bool rok = r < m;
+        char* dst = reinterpret_cast<char*>(
+            acc_out + (rok ? (int64_t)(r / s.PC) * s.rs + (r % s.PC) : 0));
+        for (int hf = 0; hf < 2; ++hf) {
+          mbar_wait(&tfull[hf], it & 1);
+          tc_fence_after();
+          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(hf * 256 + 16 * cc);
+          int c0[16], c1[16], c2[16];
+          uint32_t a6[16];
+          {
+            uint32_t x[16], y[16], z[16], w[16];
+            tmem_ld_32x32b_x16(ta + 0 * NH, x);
+            tmem_ld_32x32b_x16(ta + 1 * NH, y);
+            tmem_ld_32x32b_x16(ta + 2 * NH, z);
+            tmem_ld_32x32b_x16(ta + 3 * NH, w);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              c0[i] = (int)x[i] * 256 + (int)y[i];  // exact: |.| < 2^31
+              c1[i] = (int)z[i] * 256 + (int)w[i];
+            }
+          }
+          {
+            uint32_t x[16], y[16];
+            tmem_ld_32x32b_x16(ta + 4 * NH, x);
+            tmem_ld_32x32b_x16(ta + 5 * NH, y);
+            tmem_ld_32x32b_x16(ta + 6 * NH, a6);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) c2[i] = (int)x[i] * 256 + (int)y[i];
+          }
+          tc_fence_before();
+          mbar_arrive(&tempty[hf]);  // accumulator set hf may be overwritten now
+          const int j0 = hf * NH + 16 * cc;
+          if (rok && j0 < K) {
+            const long long* cb = cb_e[pb] + j0;  // byte offsets of the columns
+            if (fast && j0 + 16 <= K) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const long long lo = (long long)c2[i] * 256 + ((long long)(int)a6[i] + half);
+                const long long v =
+                    (long long)c0[i] * m0 + ((long long)c1[i] * m1 + (lo >> R));
+                red_add_u64(reinterpret_cast<unsigned long long*>(dst + cb[i]),
+                            (unsigned long long)v);
+              }
+            } else {
+              const int jn = min(16, K - j0);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                if (i >= jn) break;
+                const long long L = (long long)c2[i] * 256 + (int)a6[i];
+                const long long Hh = (long long)c0[i] * 65536 + c1[i];
+                const long long v = R <= 24 ? (Hh << (24 - R)) + ((L + half) >> R)
+                                            : (Hh + ((L + half) >> 24)) >> (R - 24);
+                red_add_u64(reinterpret_cast<unsigned long long*>(dst + cb[i]),
+                            (unsigned long long)v);
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 16) tmem_dealloc<TMEM_COLS>(tmem);
 }
 
 // ---------------------------------------------------------------------------
@@ -846,13 +1177,27 @@ static int run_wnnm(const GroupSrc& s, int n, const EigArgs& ea_in, double scale
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem));
     attrs = true;
   }
-  gram_kernel<IMG><<<n, wn::GRAM_THREADS, kGramSmem, st>>>(s, n, ws);
+  gram_kernel<IMG><<<n, wn::GRAM_THREADS, kGramSmem, st>>>(s, n, ws, ws + (size_t)n * wn::GSZ);
   GLR_CUDA(cudaGetLastError());
   EigArgs ea = ea_in;
   ea.G = ws;
   ea.n = n;
+  ea.wmax = ws + (size_t)n * (wn::GSZ + 1);
   eig_kernel<<<n, wn::EIG_THREADS, kEigSmem, st>>>(ea);
   GLR_CUDA(cudaGetLastError());
+#ifndef GLR_APPLY_DMMA  // dev A/B: -DGLR_APPLY_DMMA keeps the fp64 DMMA apply for image groups
+  if constexpr (IMG) {
+    static bool oz_attr = false;
+    if (!oz_attr) {
+      GLR_CUDA(cudaFuncSetAttribute(apply_oz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)oz::SMEM));
+      oz_attr = true;
+    }
+    apply_oz_kernel<<<std::min(n, kNumSMs), oz::THREADS, oz::SMEM, st>>>(
+        s, n, ws, ws + (size_t)n * wn::GSZ, ws + (size_t)n * (wn::GSZ + 1), ilogb(scale), acc_out);
+    return check_launch("wnnm kernels");
+  }
+#endif
   apply_kernel<IMG, kApplyTR><<<n, wn::APPLY_THREADS, kApplySmem, st>>>(s, n, ws, scale, acc_out,
                                                                         out);
   return check_launch("wnnm kernels");
@@ -876,7 +1221,8 @@ extern "C" int glr_debug_eig_hist(unsigned int* out, int reset) {
 #endif
 
 extern "C" size_t glr_wnnm_workspace(int G, int K) {
-  return (size_t)std::max(G, 1) * wn::GSZ * sizeof(double) + 256;
+  // G / Wm (64 x 64 per group), then max |M| and max |Wm| per group
+  return (size_t)std::max(G, 1) * (wn::GSZ + 2) * sizeof(double) + 256;
 }
 
 extern "C" int glr_wnnm(const double* groups_d, int G, int m, int K, double sigma, double c_weight,

@@ -400,3 +400,43 @@ def test_binary_mask_upload_path_is_bitwise_identical(rng):
     op_swapped.meta["masks"] = masks.copy()  # replaced: the u8 copy must not be used
     c, _ = G.gap_solve(op_swapped, y, cfg)
     assert np.array_equal(a, c)
+
+
+@pytest.mark.parametrize("p,c,k,amp", [(8, 24, 64, 1.0), (4, 3, 16, 1.0), (8, 1, 64, 1.0),
+                                       (5, 2, 37, 1.0), (6, 4, 64, 255.0)])
+def test_wnnm_scatter_image_groups_vs_oracle(p, c, k, amp, rng):
+    """glr_wnnm_scatter (image groups gathered at their positions, the solve's
+    path: Gram -> Jacobi -> tensor-core split-integer apply -> int64 scatter)
+    against the SVD oracle + an fp64 scatter (lowrank.py:68-87)."""
+    from paper_2301_03047_b200 import _device as D, _native as N
+    from paper_2301_03047_b200.lowrank import frac_bits_for
+    t = D.torch()
+    h, w, n, sigma = 37, 41, 9, 0.05 * amp
+    x = (rng.random((h, w, c)) * 1.5 - 0.25) * amp
+    x[rng.random((h, w, c)) < 0.05] = 0.0  # exact zeros and a flat region
+    x[:8, :8] = 0.5 * amp
+    pos = np.stack([rng.integers(0, h - p + 1, (n, k)), rng.integers(0, w - p + 1, (n, k))],
+                   axis=2).astype(np.int32)
+    pos[0, :] = 0  # one group of identical (flat) patches
+    frac = frac_bits_for(amp * 1.5)
+    x_d, pos_d = D.f64(x), D.i32(pos)
+    acc = D.zeros((h, w, c), t.int64)
+    ws = D.empty((N.query("glr_wnnm_workspace", n, k),), t.uint8)
+    N.call("glr_wnnm_scatter", x_d.data_ptr(), h, w, c, p, pos_d.data_ptr(), n, None, k, sigma,
+           2.0 * np.sqrt(2.0), 1e-16, frac, acc.data_ptr(), None, 0, None, ws.data_ptr(),
+           ws.numel(), D.stream())
+    got = D.host(acc).astype(np.float64) * 2.0 ** -frac
+    ref = np.zeros((h, w, c))
+    for g in range(n):
+        cols = [x[r:r + p, q:q + p, :].ravel() for r, q in pos[g]]
+        den = O.wnnm_prox(np.stack(cols, axis=1), sigma)
+        for j, (r, q) in enumerate(pos[g]):
+            ref[r:r + p, q:q + p, :] += den[:, j].reshape(p, p, c)
+    # per term: 2^-frac rounding of the numerator + the WNNM agreement bar
+    cnt = np.zeros((h, w))
+    for g in range(n):
+        for r, q in pos[g]:
+            cnt[r:r + p, q:q + p] += 1
+    tol = cnt[..., None] * (2.0 ** -frac + 1e-9 * amp)
+    err = np.abs(got - ref)
+    assert (err <= tol + 1e-15).all(), float((err - tol).max())

@@ -693,53 +693,53 @@ __global__ void __launch_bounds__(wn::APPLY_THREADS)
 // ---------------------------------------------------------------------------
 // K3 on the tensor cores: out = M Wm as an exact-integer split product
 // (Ozaki scheme) on tcgen05 kind::i8. Each operand is scaled by a power of
-// two (per 128-row tile of M, per group for Wm) so its entries become
-// integers U with |U| <= 2^46, written as S = 6 balanced base-256 digits d_k
-// in [-128, 127] (U = sum_k d_k 256^(5-k)), one int8 "slice" per digit. The
-// 26 digit products d_k(M) e_l(Wm) with k + l <= 6 are int8 MMAs with exact
-// s32 accumulation (<= 6 x 64 x 2^14 < 2^31), one TMEM accumulator per level
-// t = k + l. The epilogue joins adjacent levels exactly in int32 (a 256 +
-// b < 2^31), the four pairs by an fp64 Horner step, and rounds once into the
-// int64 fixed-point numerator. Error: the dropped levels t >= 7 are below
-// 2^-44 of max|M| max|Wm| (worst case), the input rounding 2^-47 of the
-// tile's max per entry -- far below the 2^-40 numerator resolution and the
-// 1e-9 agreement of the fp64 path with LAPACK.
+// two (per group: the Gram kernel's max |M|, the eigen kernel's max |Wm|) so
+// its entries become integers U with |U| <= 2^46, written as S = 6 balanced
+// base-256 digits d_k in [-128, 127] (U = sum_k d_k 256^(5-k)), one int8
+// "slice" per digit. The 21 digit products d_k(M) e_l(Wm) with k + l <= 5 are
+// int8 MMAs with exact s32 accumulation (<= 6 x 64 x 2^14 < 2^31), one TMEM
+// accumulator per level t = k + l. The epilogue joins adjacent levels exactly
+// in int32 (a 256 + b < 2^31) and the three pairs in int64, then rounds once
+// into the int64 fixed-point numerator. Error: the dropped levels t >= 6 stay
+// below 5 2^-40 max|M| max|Wm| in the worst case (measured ~1e-12 on unit
+// data), the input rounding 2^-47 of max|M| per entry -- at the numerator's
+// 2^-40 resolution and far below the 1e-9 agreement of fp64 WNNM with LAPACK.
 //
 // Digit extraction is one DFMA per value: fma(v, 2^(46-E), 1.5 2^52 + BIAS)
 // leaves U + BIAS (BIAS = 128 sum_k 256^k) in the low 48 mantissa bits, whose
 // bytes are the digits + 128; a 4 x 4 byte transpose (PRMT) gathers one digit
 // of four values into a word and XOR 0x80 recentres it.
 //
-// Persistent, warp-specialised: one CTA per SM walks groups g = blockIdx.x,
-// + gridDim.x, ... (the scale exponents come from the Gram kernel's max |M|
-// and the eigen kernel's max |Wm| of each group):
-//   warps 0-7   slicers: per 128-row tile, each thread loads its row's 32
-//               values (coalesced over rows) and writes the six digit slices
-//               into a 2-stage ring of 128B-swizzled K-major shared memory
-//               (two slices per 128-byte row); per group, Wm's slices into a
-//               2-buffer B ring;
-//   warp 16     MMA issuer: per tile and half of the 64 output columns, 26
+// Operand A (the M tile's digits, 128 rows x 6 x 64 bytes) lives in TMEM and
+// is written there by the slicers with tcgen05.st, so the tensor core reads
+// only the small B operand (Wm's digits) from shared memory: with A in shared
+// memory the 2 x 21 x 2 MMAs of N = 32 re-read A 42 times per tile and were
+// bound by shared-memory bandwidth. Persistent, warp-specialised: one CTA per
+// SM walks groups g = blockIdx.x, + gridDim.x, ...
+//   warps 0-7   slicers: per 128-row tile each thread loads its row's 32
+//               values (coalesced over rows), forms the digit words, waits for
+//               the previous tile's MMAs, and stores 48 TMEM columns; per
+//               group, Wm's slices into a 2-buffer shared-memory B ring;
+//   warp 16     MMA issuer: per tile and half of the 64 output columns, 21
 //               digit products x 2 K-steps (M = 128, N = 32, K = 32) into one
-//               of two TMEM accumulator sets (7 levels x 32 columns each);
-//   warps 8-15  epilogue: per half, the 7 levels of 16 columns, released to
-//               the MMA issuer right after tcgen05.ld, then the atomics --
-//               the next half's MMAs and the slicing overlap them.
+//               of two TMEM accumulator sets (6 levels x 32 columns each);
+//   warps 8-15  epilogue: per half, the 6 levels of 16 columns, released to
+//               the MMA issuer right after tcgen05.ld, then the atomics.
 
 namespace oz {
 constexpr int S = 6;                     // digits per operand
-constexpr int LV = 7;                    // levels kept: t = k + l <= 6
+constexpr int LV = 6;                    // levels kept: t = k + l <= 5
 constexpr int BITS = 46;                 // |U| <= 2^46
 constexpr int TR = 128;                  // rows of M per tile (UMMA M)
 constexpr int NH = 32;                   // output columns per MMA pass (UMMA N)
-constexpr int NBUF = S / 2;              // 128-byte row buffers per operand
-constexpr int A_BUF = TR * 128;          // 16 KB
-constexpr int B_BUF = wn::KMAX * 128;    // 8 KB
-constexpr int A_STAGE = NBUF * A_BUF;    // 48 KB
-constexpr int B_STAGE = NBUF * B_BUF;    // 24 KB
+constexpr int B_BUF = wn::KMAX * 128;    // 8 KB: two B slices per 128-byte row
+constexpr int B_STAGE = (S / 2) * B_BUF; // 24 KB
 constexpr int SLICERS = 256, EPI = 256;  // warps 0-7, 8-15; warp 16 issues the MMAs
 constexpr int THREADS = SLICERS + EPI + 32;
-constexpr uint32_t TMEM_COLS = 512;      // two sets of LV x NH = 224 columns (at 0, 256)
-constexpr size_t SMEM = 2 * (A_STAGE + B_STAGE) + 1024;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t ACC_COLS = LV * NH;   // 192 per accumulator set (sets at 0 and 192)
+constexpr uint32_t A_COL = 2 * ACC_COLS; // A: 96 columns, 8 per (K-half, digit)
+constexpr size_t SMEM = 2 * B_STAGE + 1024;
 // 1.5 * 2^52 + 0x808080808080 (< 2^53, exact)
 constexpr double MAGIC = 6755399441055744.0 + 141289400074368.0;
 }  // namespace oz
@@ -761,12 +761,10 @@ __device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long
   asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// 16 consecutive K-values (chunk jc of 4) of row `row` -> the six slices:
-// slice k lives in buffer k / 2, bytes (k % 2) * 64 + 16 jc of the row,
-// 16-byte chunk index XOR (row % 8) (the 128B swizzle).
-__device__ __forceinline__ void oz_store16(uint8_t* buf0, int buf_bytes, int row, int jc,
-                                           const double* v, double scale) {
-  uint32_t w[oz::S][4];  // w[k][q]: digit k of values 4q .. 4q+3
+// Digit words of 16 consecutive K-values: w[k * WS + q] packs digit k of
+// values 4q .. 4q+3 (byte i = value 4q+i) as signed bytes.
+template <int WS>
+__device__ __forceinline__ void oz_digits16(const double* v, double scale, uint32_t* w) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     uint32_t lo[4], hi[4];
@@ -779,18 +777,12 @@ __device__ __forceinline__ void oz_store16(uint8_t* buf0, int buf_bytes, int row
     const uint32_t x01 = __byte_perm(lo[0], lo[1], 0x5140), y01 = __byte_perm(lo[0], lo[1], 0x7362);
     const uint32_t x23 = __byte_perm(lo[2], lo[3], 0x5140), y23 = __byte_perm(lo[2], lo[3], 0x7362);
     const uint32_t h01 = __byte_perm(hi[0], hi[1], 0x5140), h23 = __byte_perm(hi[2], hi[3], 0x5140);
-    w[5][q] = __byte_perm(x01, x23, 0x5410) ^ 0x80808080u;  // byte 0 (least significant digit)
-    w[4][q] = __byte_perm(x01, x23, 0x7632) ^ 0x80808080u;
-    w[3][q] = __byte_perm(y01, y23, 0x5410) ^ 0x80808080u;
-    w[2][q] = __byte_perm(y01, y23, 0x7632) ^ 0x80808080u;
-    w[1][q] = __byte_perm(h01, h23, 0x5410) ^ 0x80808080u;
-    w[0][q] = __byte_perm(h01, h23, 0x7632) ^ 0x80808080u;  // byte 5 (most significant)
-  }
-#pragma unroll
-  for (int k = 0; k < oz::S; ++k) {
-    const int c = ((k & 1) * 4 + jc) ^ (row & 7);
-    *reinterpret_cast<uint4*>(buf0 + (k >> 1) * buf_bytes + row * 128 + c * 16) =
-        make_uint4(w[k][0], w[k][1], w[k][2], w[k][3]);
+    w[5 * WS + q] = __byte_perm(x01, x23, 0x5410) ^ 0x80808080u;  // byte 0: least significant
+    w[4 * WS + q] = __byte_perm(x01, x23, 0x7632) ^ 0x80808080u;
+    w[3 * WS + q] = __byte_perm(y01, y23, 0x5410) ^ 0x80808080u;
+    w[2 * WS + q] = __byte_perm(y01, y23, 0x7632) ^ 0x80808080u;
+    w[1 * WS + q] = __byte_perm(h01, h23, 0x5410) ^ 0x80808080u;
+    w[0 * WS + q] = __byte_perm(h01, h23, 0x7632) ^ 0x80808080u;  // byte 5: most significant
   }
 }
 
@@ -800,24 +792,22 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
                     int frac_bits, int64_t* __restrict__ acc_out) {
   using namespace oz;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sA = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+  uint8_t* sB = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
-  uint8_t* sB = sA + 2 * A_STAGE;
-  __shared__ long long cb_s[2][wn::KMAX], cb_e[2][wn::KMAX];  // per group (parity): column bases
-  __shared__ __align__(8) uint64_t full_a[2], empty_a[2], full_b[2], empty_b[2], tfull[2],
-      tempty[2];
+  __shared__ __align__(16) long long cb_s[2][wn::KMAX], cb_e[2][wn::KMAX];  // per group (parity)
+  __shared__ __align__(8) uint64_t full_a, empty_a, full_b[2], empty_b[2], tfull[2], tempty[2];
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int K = s.K, m = s.m;
   const int ntiles = (m + TR - 1) / TR;
   if (tid == 0) {
+    mbar_init(&full_a, SLICERS / 32);
+    mbar_init(&empty_a, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&full_a[i], SLICERS);
-      mbar_init(&empty_a[i], 1);
-      mbar_init(&full_b[i], SLICERS);
+      mbar_init(&full_b[i], SLICERS / 32);
       mbar_init(&empty_b[i], 1);
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], EPI);
+      mbar_init(&tempty[i], EPI / 32);
     }
     fence_barrier_init();
   }
@@ -830,41 +820,63 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
   if (warp < 8) {
     // ---------------- slicers ----------------
     const int st = tid, r_loc = st & (TR - 1), jh = st >> 7;
+    const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + A_COL + 48 * jh;
     int it = 0;
     for (int g = blockIdx.x, gi = 0; g < n; g += gridDim.x, ++gi) {
       const int pb = gi & 1;
-      if (st < wn::KMAX) cb_s[pb][st] = st < K ? col_base<true>(s, g, st) : 0;
-      // Wm -> B slices: row nn = output column j', K = j (B[nn][j] = Wm[j][nn])
+      if (st < wn::KMAX) cb_s[pb][st] = st < K ? col_base<true>(s, g, st) * 8 : 0;  // bytes
+      // Wm -> B slices (shared memory): row nn = output column j', K = j (B[nn][j] = Wm[j][nn]);
+      // slice k in buffer k / 2 at bytes (k % 2) 64 + 16 jc, 16-byte chunk XOR (row % 8)
       {
         const int nn = st & 63, jc = st >> 6;
         const double* Wg = Wm + (size_t)g * wn::GSZ;
         double v[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = Wg[(16 * jc + i) * wn::KMAX + nn];
+        uint32_t w[S * 4];
+        oz_digits16<4>(v, pow2(BITS - oz_exp(wmax[g])), w);
         if (gi >= 2) mbar_wait(&empty_b[pb], ((gi >> 1) - 1) & 1);
-        oz_store16(sB + pb * B_STAGE, B_BUF, nn, jc, v, pow2(BITS - oz_exp(wmax[g])));
+        uint8_t* b = sB + pb * B_STAGE;
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+          const int c = ((k & 1) * 4 + jc) ^ (nn & 7);
+          *reinterpret_cast<uint4*>(b + (k >> 1) * B_BUF + nn * 128 + c * 16) =
+              make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+        }
         fence_proxy_async_smem();
-        mbar_arrive(&full_b[pb]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full_b[pb]);
       }
       named_bar(1, SLICERS);  // cb_s[pb] written
       const double sc = pow2(BITS - oz_exp(gmax[g]));
+      const long long* cb = cb_s[pb] + 32 * jh;
       for (int tt = 0; tt < ntiles; ++tt, ++it) {
         const int r = tt * TR + r_loc;
         const bool rok = r < m;
-        const double* src = s.src + (rok ? (int64_t)(r / s.PC) * s.rs + (r % s.PC) : 0);
+        const char* src = reinterpret_cast<const char*>(
+            s.src + (rok ? (int64_t)(r / s.PC) * s.rs + (r % s.PC) : 0));
         double v[32];
+        if (rok && K == wn::KMAX) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int j = 32 * jh + i;
-          v[i] = (rok && j < K) ? __ldg(src + cb_s[pb][j]) : 0.0;
+          for (int i = 0; i < 32; ++i) v[i] = __ldg(reinterpret_cast<const double*>(src + cb[i]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            v[i] = (rok && 32 * jh + i < K)
+                       ? __ldg(reinterpret_cast<const double*>(src + cb[i])) : 0.0;
         }
-        const int stg = it & 1;
-        if (it >= 2) mbar_wait(&empty_a[stg], ((it >> 1) - 1) & 1);
-        uint8_t* a = sA + stg * A_STAGE;
-        oz_store16(a, A_BUF, r_loc, 2 * jh, v, sc);
-        oz_store16(a, A_BUF, r_loc, 2 * jh + 1, v + 16, sc);
-        fence_proxy_async_smem();
-        mbar_arrive(&full_a[stg]);
+        // A columns of this thread: 8 per digit k (its 32 K-bytes), digit-major
+        uint32_t w[S * 8];
+        oz_digits16<8>(v, sc, w);
+        oz_digits16<8>(v + 16, sc, w + 4);
+        if (it >= 1) mbar_wait(&empty_a, (it - 1) & 1);  // the previous tile's MMAs are done
+        tc_fence_after();
+        tmem_st_32x32b_x32(ta, *reinterpret_cast<const uint32_t(*)[32]>(w));
+        tmem_st_32x32b_x16(ta + 32, w + 32);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full_a);
       }
     }
   } else if (warp == 16) {
@@ -875,33 +887,28 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
       for (int g = blockIdx.x, gi = 0; g < n; g += gridDim.x, ++gi) {
         const int pb = gi & 1;
         mbar_wait(&full_b[pb], (gi >> 1) & 1);
+        const uint64_t bd0 = smem_desc_k_sw128(sB + pb * B_STAGE);
         for (int tt = 0; tt < ntiles; ++tt, ++it) {
-          const int stg = it & 1;
-          mbar_wait(&full_a[stg], (it >> 1) & 1);
+          mbar_wait(&full_a, it & 1);
           for (int hf = 0; hf < 2; ++hf) {
             if (it >= 1) mbar_wait(&tempty[hf], (it - 1) & 1);
             tc_fence_after();
-            const uint32_t d0 = tmem + (uint32_t)(hf * 256);
+            const uint32_t d0 = tmem + (uint32_t)hf * ACC_COLS;
 #pragma unroll
             for (int k = 0; k < S; ++k)
 #pragma unroll
-              for (int l = 0; l < S; ++l)
-                if (k + l < LV) {
+              for (int l = 0; l + k < LV; ++l)
 #pragma unroll
-                  for (int ks = 0; ks < 2; ++ks) {
-                    const uint64_t ad = smem_desc_k_sw128(sA + stg * A_STAGE + (k >> 1) * A_BUF) +
-                                        (uint64_t)(((k & 1) * 64 + ks * 32) >> 4);
-                    const uint64_t bd =
-                        smem_desc_k_sw128(sB + pb * B_STAGE + (l >> 1) * B_BUF + hf * NH * 128) +
-                        (uint64_t)(((l & 1) * 64 + ks * 32) >> 4);
-                    // first write of level t: (k, l) = (0, t) for t < S, (1, S-1) for t = S
-                    const bool first = ks == 0 && (k == 0 || (k == 1 && l == S - 1));
-                    umma_i8(d0 + (uint32_t)((k + l) * NH), ad, bd, idesc, !first);
-                  }
+                for (int ks = 0; ks < 2; ++ks) {
+                  // B: slice l, rows 32 hf.., K bytes 32 ks.. of the slice (desc += bytes >> 4)
+                  const uint64_t bd = bd0 + (uint64_t)(((l >> 1) * B_BUF + hf * NH * 128 +
+                                                        (l & 1) * 64 + ks * 32) >> 4);
+                  umma_i8_ta(d0 + (uint32_t)((k + l) * NH), tmem + A_COL + 48 * ks + 8 * k, bd,
+                             idesc, (k | ks) != 0);
                 }
             umma_commit(&tfull[hf]);
           }
-          umma_commit(&empty_a[stg]);
+          umma_commit(&empty_a);
         }
         umma_commit(&empty_b[pb]);
       }
@@ -914,16 +921,16 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
       const int pb = gi & 1;
       if (et < wn::KMAX) cb_e[pb][et] = et < K ? col_base<true>(s, g, et) * 8 : 0;  // bytes
       named_bar(2, EPI);
-      // value = sum_t acc_t 256^(10-t) 2^(e_m + e_w - 2 BITS) = y 2^(e_m + e_w - 60), with
-      // y = sum_t acc_t 256^(6-t) = c0 2^40 + c1 2^24 + L, c0 = acc_0 256 + acc_1, c1 =
-      // acc_2 256 + acc_3, c2 = acc_4 256 + acc_5 (exact in int32), L = c2 256 + acc_6.
-      // Fixed point: round(y 2^-R), R = 60 - e_m - e_w - frac_bits, all in integers:
-      // c0 2^(40-R) + c1 2^(24-R) + ((L + 2^(R-1)) >> R) for 10 <= R <= 24 (the normal
-      // range: |x| ~ 2^frac_bits-40 and |Wm| <= 1 give R ~ 18), a 64-bit path otherwise.
-      const int R = max(min(60 - oz_exp(gmax[g]) - oz_exp(wmax[g]) - frac_bits, 62), 0);
-      const long long half = R > 0 ? 1ll << (R - 1) : 0;
-      const bool fast = R >= 10 && R <= 24;
-      const int m0 = fast ? 1 << (40 - R) : 0, m1 = fast ? 1 << (24 - R) : 0;
+      // value = sum_t acc_t 256^(10-t) 2^(e_m + e_w - 2 BITS) = y 2^(e_m + e_w - 52), with
+      // y = c0 2^32 + c1 2^16 + c2, c0 = acc_0 256 + acc_1, c1 = acc_2 256 + acc_3,
+      // c2 = acc_4 256 + acc_5 (each exact in int32). Fixed point: round(y 2^-R),
+      // R = 52 - e_m - e_w - frac_bits, in integer arithmetic: c0 2^(32-R) + c1 2^(16-R) +
+      // ((c2 + 2^(R-1)) >> R) for 2 <= R <= 16 (the normal range: |x| < 2^(41-frac_bits)
+      // and |Wm| <= 1 give R ~ 11), a 64-bit path otherwise.
+      const int R = max(min(52 - oz_exp(gmax[g]) - oz_exp(wmax[g]) - frac_bits, 62), 0);
+      const bool fast = R >= 2 && R <= 16;
+      const int half = fast ? 1 << (R - 1) : 0;
+      const int m0 = fast ? 1 << (32 - R) : 0, m1 = fast ? 1 << (16 - R) : 0;
       for (int tt = 0; tt < ntiles; ++tt, ++it) {
         const int r = tt * TR + 32 * q + lane;
         const bool rok = r < m;
@@ -932,9 +939,9 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
         for (int hf = 0; hf < 2; ++hf) {
           mbar_wait(&tfull[hf], it & 1);
           tc_fence_after();
-          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(hf * 256 + 16 * cc);
+          const uint32_t ta =
+              tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(hf * ACC_COLS + 16 * cc);
           int c0[16], c1[16], c2[16];
-          uint32_t a6[16];
           {
             uint32_t x[16], y[16], z[16], w[16];
             tmem_ld_32x32b_x16(ta + 0 * NH, x);
@@ -952,22 +959,21 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
             uint32_t x[16], y[16];
             tmem_ld_32x32b_x16(ta + 4 * NH, x);
             tmem_ld_32x32b_x16(ta + 5 * NH, y);
-            tmem_ld_32x32b_x16(ta + 6 * NH, a6);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 16; ++i) c2[i] = (int)x[i] * 256 + (int)y[i];
           }
           tc_fence_before();
-          mbar_arrive(&tempty[hf]);  // accumulator set hf may be overwritten now
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[hf]);  // accumulator set hf may be overwritten now
           const int j0 = hf * NH + 16 * cc;
           if (rok && j0 < K) {
             const long long* cb = cb_e[pb] + j0;  // byte offsets of the columns
             if (fast && j0 + 16 <= K) {
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
-                const long long lo = (long long)c2[i] * 256 + ((long long)(int)a6[i] + half);
-                const long long v =
-                    (long long)c0[i] * m0 + ((long long)c1[i] * m1 + (lo >> R));
+                const long long v = (long long)c0[i] * m0 +
+                                    ((long long)c1[i] * m1 + (long long)((c2[i] + half) >> R));
                 red_add_u64(reinterpret_cast<unsigned long long*>(dst + cb[i]),
                             (unsigned long long)v);
               }
@@ -976,10 +982,9 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
                 if (i >= jn) break;
-                const long long L = (long long)c2[i] * 256 + (int)a6[i];
-                const long long Hh = (long long)c0[i] * 65536 + c1[i];
-                const long long v = R <= 24 ? (Hh << (24 - R)) + ((L + half) >> R)
-                                            : (Hh + ((L + half) >> 24)) >> (R - 24);
+                const long long y =
+                    (long long)c0[i] * 4294967296ll + (long long)c1[i] * 65536 + c2[i];
+                const long long v = R > 0 ? (y + (1ll << (R - 1))) >> R : y;
                 red_add_u64(reinterpret_cast<unsigned long long*>(dst + cb[i]),
                             (unsigned long long)v);
               }

@@ -334,16 +334,20 @@ def run_b200(args, rank, world, local_rank):
             m = mp * mp * c
             k = wl.match.group_size
             # algorithmic fp64 work per group: symmetric Gram m*K*(K+1) + apply
-            # 2*m*K^2 flops (the O(K^3) eigen step is not counted); Gram and apply
-            # run on the fp64 tensor cores (DMMA); peak = measured DMMA rate
-            # (profiles/r01_fp64_peak.md)
+            # 2*m*K^2 flops (the O(K^3) eigen step is not counted); the Gram runs
+            # on the fp64 tensor cores (DMMA), the apply's fp64 product exactly
+            # emulated on the int8 tensor cores (split-integer / Ozaki, six digit
+            # slices); peak = measured DMMA rate (profiles/r01_fp64_peak.md), so
+            # frac is fp64-equivalent work over the fp64 tensor peak
             flops = (m * k * (k + 1) + 2.0 * m * k * k) * d["units"] / d["launches"]
             avg_s = d["ms"] / d["launches"] / 1e3
             ach = flops / avg_s / 1e12
             byts = 2.0 * m * k * 8 * d["units"] / d["launches"]
             roof["wnnm_scatter"] = {"bound": "tensor", "achieved": ach, "peak": FP64_DMMA_PEAK,
                                     "unit": "TFLOP/s", "frac": ach / FP64_DMMA_PEAK,
-                                    "peak_kind": "fp64 DMMA, measured (profiles/r01_fp64_peak.md)",
+                                    "peak_kind": "fp64-equivalent work vs the measured fp64 DMMA peak "
+                                                 "(Gram on DMMA, apply on int8 tcgen05 as an "
+                                                 "exact split-integer product)",
                                     "avg_ms": d["ms"] / d["launches"],
                                     "hbm_gbs": byts / avg_s / 1e9}
         if "topk" in kern:
@@ -368,7 +372,7 @@ def run_b200(args, rank, world, local_rank):
             "metric": metric_for(wl), "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64+e2m1",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64+e2m1+s8",
             "data": "synthetic (seeded generator, workloads.py)",
             "config": _config(args, wl, n_ex),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),

@@ -208,8 +208,31 @@ def _config(args, wl, n_exemplars):
                         f"exemplar_stride={wl.match.exemplar_stride}",
             "exemplars": n_exemplars, "iters_per_step": wl.max_iters,
             "parallelism": f"exemplar-shard x{args.gpus}",
-            "l2": "inputs > L2 (x, masks 201 MB each; heat map 8.5 GB per refresh)",
+            "l2": _l2_note(wl, n_exemplars),
             "seed": 0}
+
+
+L2_BYTES = 126 * 2 ** 20
+
+
+def _working_set(wl, n_exemplars):
+    """(x bytes, heat-map bytes per refresh) of a workload"""
+    h, w, c = wl.shape
+    p = wl.match.patch_size
+    return h * w * c * 8, n_exemplars * (h - p + 1) * (w - p + 1) * 2
+
+
+def _needs_flush(wl, n_exemplars):
+    xb, hb = _working_set(wl, n_exemplars)
+    return hb + 4 * xb < 2 * L2_BYTES
+
+
+def _l2_note(wl, n_exemplars):
+    xb, hb = _working_set(wl, n_exemplars)
+    if _needs_flush(wl, n_exemplars):
+        return (f"L2 flushed between timed steps (256 MB write outside the per-step events); "
+                f"x {xb / 1e6:.0f} MB, heat map {hb / 1e6:.0f} MB per refresh")
+    return f"inputs > L2 (x {xb / 1e6:.0f} MB, heat map {hb / 1e9:.2f} GB per refresh)"
 
 
 def run_b200(args, rank, world, local_rank):
@@ -246,17 +269,23 @@ def run_b200(args, rank, world, local_rank):
     if clocks:
         clocks.start()
     launches0 = N.launch_count
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device="cuda") \
+        if _needs_flush(wl, n_ex) else None
+    ev = []
     for _ in range(args.steps):
+        if flush is not None:
+            flush.fill_(1)  # evict the previous step's working set from L2
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
         runner.run(y_d)
-    e1.record()
+        e1.record()
+        ev.append((e0, e1))
     torch.cuda.synchronize()
     barrier()
-    launches = N.launch_count - launches0
+    launches = N.launch_count - launches0  # fill_ is a torch kernel, not counted
     ck = clocks.stop(local_rank) if clocks else None
-    ms = e0.elapsed_time(e1)
+    ms = sum(a.elapsed_time(b) for a, b in ev)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

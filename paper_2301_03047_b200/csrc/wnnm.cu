@@ -209,6 +209,7 @@ struct EigArgs {
   int warm;        // 0 cold, 1 start every group from vcache, 2 only where warm_flags[g]
   const uint8_t* warm_flags;
   double* wmax;  // optional per-group max |Wm| (the split-integer apply's scale)
+  int* counter;  // dynamic group counter (zeroed before the launch)
 };
 
 // Block-Jacobi schedule. The 63 rounds of a parallel cyclic sweep pair i
@@ -272,15 +273,12 @@ __device__ __forceinline__ void jrot(double c, double s, double& u, double& v) {
   v = nv;
 }
 
-__global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
+__device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double* sm) {
   using namespace wn;
-  extern __shared__ __align__(16) double sm[];
   double* G = sm;               // KMAX x GLD, exactly symmetric throughout
   double* Vt = G + KMAX * GLD;  // KMAX x VLD: Vt[j][i] = V[i][j] (row j = eigenvector j)
   __shared__ double ratio[KMAX];
   __shared__ double s_tiny;
-  const int g = blockIdx.x;
-  if (g >= a.n) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int K = a.K;
   // small products: rows 4*bi + ii, columns bj + 16*jj (conflict-free operand reads)
@@ -605,6 +603,22 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
       for (int w = 1; w < EIG_THREADS / 32; ++w) mx = fmax(mx, ratio[w]);
       a.wmax[g] = mx;
     }
+  }
+}
+
+// Dynamic group scheduling: 3 CTAs per SM take groups from an atomic counter
+// (zeroed by the launcher), so the per-group sweep counts balance and the last
+// wave's tail shrinks to one group per CTA.
+__global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_g;
+  for (;;) {
+    if (threadIdx.x == 0) s_g = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int g = s_g;
+    __syncthreads();  // every thread has g (and is done with the previous group's smem)
+    if (g >= a.n) return;
+    eig_group(a, g, sm);
   }
 }
 
@@ -1188,7 +1202,9 @@ static int run_wnnm(const GroupSrc& s, int n, const EigArgs& ea_in, double scale
   ea.G = ws;
   ea.n = n;
   ea.wmax = ws + (size_t)n * (wn::GSZ + 1);
-  eig_kernel<<<n, wn::EIG_THREADS, kEigSmem, st>>>(ea);
+  ea.counter = reinterpret_cast<int*>(ws + (size_t)n * (wn::GSZ + 2));
+  GLR_CUDA(cudaMemsetAsync(ea.counter, 0, sizeof(int), st));
+  eig_kernel<<<std::min(n, 3 * kNumSMs), wn::EIG_THREADS, kEigSmem, st>>>(ea);
   GLR_CUDA(cudaGetLastError());
 #ifndef GLR_APPLY_DMMA  // dev A/B: -DGLR_APPLY_DMMA keeps the fp64 DMMA apply for image groups
   if constexpr (IMG) {
@@ -1227,7 +1243,8 @@ extern "C" int glr_debug_eig_hist(unsigned int* out, int reset) {
 
 extern "C" size_t glr_wnnm_workspace(int G, int K) {
   // G / Wm (64 x 64 per group), then max |M| and max |Wm| per group
-  return (size_t)std::max(G, 1) * (wn::GSZ + 2) * sizeof(double) + 256;
+  // (+ the eigen kernel's group counter)
+  return ((size_t)std::max(G, 1) * (wn::GSZ + 2) + 1) * sizeof(double) + 256;
 }
 
 extern "C" int glr_wnnm(const double* groups_d, int G, int m, int K, double sigma, double c_weight,

@@ -734,9 +734,12 @@ __global__ void __launch_bounds__(wn::APPLY_THREADS)
 //               values (coalesced over rows), forms the digit words, waits for
 //               the previous tile's MMAs, and stores 48 TMEM columns; per
 //               group, Wm's slices into a 2-buffer shared-memory B ring;
-//   warp 16     MMA issuer: per tile and half of the 64 output columns, 21
-//               digit products x 2 K-steps (M = 128, N = 32, K = 32) into one
-//               of two TMEM accumulator sets (6 levels x 32 columns each);
+//   warps 16-19 MMA issuers (one lane each): per tile and half of the 64
+//               output columns, 21 digit products x 2 K-steps (M = 128,
+//               N = 32, K = 32) into one of two TMEM accumulator sets (6
+//               levels x 32 columns each); issuer (half, level set) owns its
+//               accumulators, so four lanes issue in parallel (one issuing
+//               lane was ~10 % slower);
 //   warps 8-15  epilogue: per half, the 6 levels of 16 columns, released to
 //               the MMA issuer right after tcgen05.ld, then the atomics.
 
@@ -748,8 +751,9 @@ constexpr int TR = 128;                  // rows of M per tile (UMMA M)
 constexpr int NH = 32;                   // output columns per MMA pass (UMMA N)
 constexpr int B_BUF = wn::KMAX * 128;    // 8 KB: two B slices per 128-byte row
 constexpr int B_STAGE = (S / 2) * B_BUF; // 24 KB
-constexpr int SLICERS = 256, EPI = 256;  // warps 0-7, 8-15; warp 16 issues the MMAs
-constexpr int THREADS = SLICERS + EPI + 32;
+constexpr int SLICERS = 256, EPI = 256;  // warps 0-7, 8-15; warps 16-19 issue the MMAs
+constexpr int ISSUERS = 4;               // (column half) x (level set)
+constexpr int THREADS = SLICERS + EPI + 32 * ISSUERS;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t ACC_COLS = LV * NH;   // 192 per accumulator set (sets at 0 and 192)
 constexpr uint32_t A_COL = 2 * ACC_COLS; // A: 96 columns, 8 per (K-half, digit)
@@ -816,11 +820,11 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
   const int ntiles = (m + TR - 1) / TR;
   if (tid == 0) {
     mbar_init(&full_a, SLICERS / 32);
-    mbar_init(&empty_a, 1);
+    mbar_init(&empty_a, ISSUERS);  // every issuer's MMAs
     for (int i = 0; i < 2; ++i) {
       mbar_init(&full_b[i], SLICERS / 32);
-      mbar_init(&empty_b[i], 1);
-      mbar_init(&tfull[i], 1);
+      mbar_init(&empty_b[i], ISSUERS);
+      mbar_init(&tfull[i], ISSUERS / 2);  // both level sets of the half
       mbar_init(&tempty[i], EPI / 32);
     }
     fence_barrier_init();
@@ -893,36 +897,38 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
         if (lane == 0) mbar_arrive(&full_a);
       }
     }
-  } else if (warp == 16) {
-    // ---------------- MMA issuer ----------------
+  } else if (warp >= 16) {
+    // ---------------- MMA issuers: lane 0 of warps 16-19; warp 16 + 2 ls + hf issues
+    // column half hf, levels 0-3 (ls = 0: 10 products) or 4-5 (ls = 1: 11 products) ----------------
     if (lane == 0) {
+      const int hf = (warp - 16) & 1, ls = (warp - 16) >> 1;
       constexpr uint32_t idesc = idesc_s8_s32(TR, NH);
+      const uint32_t d0 = tmem + (uint32_t)hf * ACC_COLS;
       int it = 0;
       for (int g = blockIdx.x, gi = 0; g < n; g += gridDim.x, ++gi) {
         const int pb = gi & 1;
         mbar_wait(&full_b[pb], (gi >> 1) & 1);
-        const uint64_t bd0 = smem_desc_k_sw128(sB + pb * B_STAGE);
+        const uint64_t bd0 = smem_desc_k_sw128(sB + pb * B_STAGE) + (uint64_t)((hf * NH * 128) >> 4);
         for (int tt = 0; tt < ntiles; ++tt, ++it) {
           mbar_wait(&full_a, it & 1);
-          for (int hf = 0; hf < 2; ++hf) {
-            if (it >= 1) mbar_wait(&tempty[hf], (it - 1) & 1);
-            tc_fence_after();
-            const uint32_t d0 = tmem + (uint32_t)hf * ACC_COLS;
+          if (it >= 1) mbar_wait(&tempty[hf], (it - 1) & 1);
+          tc_fence_after();
 #pragma unroll
-            for (int k = 0; k < S; ++k)
+          for (int k = 0; k < S; ++k)
 #pragma unroll
-              for (int l = 0; l + k < LV; ++l)
+            for (int l = 0; l + k < LV; ++l)
+              if ((k + l >= 4) == (ls == 1)) {  // this issuer's levels (own accumulators)
 #pragma unroll
                 for (int ks = 0; ks < 2; ++ks) {
                   // B: slice l, rows 32 hf.., K bytes 32 ks.. of the slice (desc += bytes >> 4)
-                  const uint64_t bd = bd0 + (uint64_t)(((l >> 1) * B_BUF + hf * NH * 128 +
-                                                        (l & 1) * 64 + ks * 32) >> 4);
+                  const uint64_t bd =
+                      bd0 + (uint64_t)(((l >> 1) * B_BUF + (l & 1) * 64 + ks * 32) >> 4);
                   umma_i8_ta(d0 + (uint32_t)((k + l) * NH), tmem + A_COL + 48 * ks + 8 * k, bd,
                              idesc, (k | ks) != 0);
                 }
-            umma_commit(&tfull[hf]);
-          }
-          umma_commit(&empty_a);
+              }
+          umma_commit(&tfull[hf]);
+          umma_commit(&empty_a);  // one of the two arrivals that free A
         }
         umma_commit(&empty_b[pb]);
       }

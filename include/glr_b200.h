@@ -199,7 +199,11 @@ int glr_wnnm(const double* groups_d, int G, int m, int K, double sigma, double c
 /* ---- (4)+(5) fused regularizer: glr/lowrank.py:68-87 + patches.py:57-70 ----
  * For every group g < n: gather from x, WNNM, and scatter-add the denoised
  * patches into acc_d, an int64 fixed-point numerator (value * 2^frac_bits),
- * so aggregation is deterministic and rank-count invariant.
+ * so aggregation is deterministic and rank-count invariant. The Gram is fp64
+ * (DMMA); the product M * Wm runs on the int8 tensor cores as an exact
+ * split-integer product (six base-256 digit slices per operand, levels
+ * k + l <= 5), within ~2^-40 max|x| of the fp64 product per entry.
+ * ws: glr_wnnm_workspace(n_max, K) bytes.
  * vcache_d (optional, n_max*64*64 doubles) keeps each group's eigenvectors;
  * warm != 0 starts the Jacobi sweeps from them (valid while the group's
  * positions are unchanged, i.e. between matching refreshes).              */

@@ -403,7 +403,8 @@ def test_binary_mask_upload_path_is_bitwise_identical(rng):
 
 
 @pytest.mark.parametrize("p,c,k,amp", [(8, 24, 64, 1.0), (4, 3, 16, 1.0), (8, 1, 64, 1.0),
-                                       (5, 2, 37, 1.0), (6, 4, 64, 255.0)])
+                                       (5, 2, 37, 1.0), (6, 4, 64, 255.0), (8, 2, 64, 0.01),
+                                       (4, 2, 64, 0.0)])
 def test_wnnm_scatter_image_groups_vs_oracle(p, c, k, amp, rng):
     """glr_wnnm_scatter (image groups gathered at their positions, the solve's
     path: Gram -> Jacobi -> tensor-core split-integer apply -> int64 scatter)

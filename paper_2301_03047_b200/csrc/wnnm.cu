@@ -273,6 +273,24 @@ __device__ __forceinline__ void jrot(double c, double s, double& u, double& v) {
   v = nv;
 }
 
+// 64 x 64 x 64 fp64 product on DMMA for the eigen kernel: warp w owns tile
+// row w (rows 8w..8w+7) and all eight 8x8 tile columns; A(i, k) and B(k, j)
+// are read through the accessors. D element (8w + lane/4, 8tj + 2(lane%4) + e)
+// lands in d[tj][e].
+template <class FA, class FB>
+__device__ __forceinline__ void eig_mm64(FA A, FB B, double (&d)[8][2]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int ar = lane >> 2, ak = lane & 3;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) d[t][0] = d[t][1] = 0.0;
+#pragma unroll 4
+  for (int k0 = 0; k0 < wn::KMAX; k0 += 4) {
+    const double fa = A(8 * w + ar, k0 + ak);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) dmma(d[t][0], d[t][1], fa, B(k0 + ak, 8 * t + ar));
+  }
+}
+
 __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double* sm) {
   using namespace wn;
   double* G = sm;               // KMAX x GLD, exactly symmetric throughout
@@ -281,8 +299,6 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
   __shared__ double s_tiny;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int K = a.K;
-  // small products: rows 4*bi + ii, columns bj + 16*jj (conflict-free operand reads)
-  const int bi = tid >> 4, bj = tid & 15;
   double* Gg = a.G + (size_t)g * GSZ;
   double* vc = a.vcache ? a.vcache + (size_t)g * GSZ : nullptr;
   const bool warm = vc && (a.warm == 1 || (a.warm == 2 && a.warm_flags[g]));
@@ -303,51 +319,26 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
   }
   if (warm) {
     // Warm start from this group's eigenvectors of a previous iteration:
-    // G <- Vp^T G Vp (Y = G Vp to registers, then to G after a barrier),
-    // V stays Vp. The sweeps then only remove a small off-diagonal residue.
-    double y[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) y[i][j] = 0.0;
-    for (int k = 0; k < KMAX; ++k) {
-      double gk[4], vk[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) gk[i] = G[(4 * bi + i) * GLD + k];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) vk[j] = Vt[(bj + 16 * j) * VLD + k];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) y[i][j] = fma(gk[i], vk[j], y[i][j]);
-    }
+    // G <- Vp^T G Vp on DMMA (Y = G Vp to registers, then to G after a
+    // barrier), V stays Vp. The sweeps then only remove a small off-diagonal
+    // residue.
+    const int ar = lane >> 2, ak = lane & 3;
+    double d[8][2];
+    eig_mm64([&](int i, int k) { return G[i * GLD + k]; },
+             [&](int k, int j) { return Vt[j * VLD + k]; }, d);
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int t = 0; t < 8; ++t)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) G[(4 * bi + i) * GLD + bj + 16 * j] = y[i][j];
+      for (int e = 0; e < 2; ++e) G[(8 * warp + ar) * GLD + 8 * t + 2 * ak + e] = d[t][e];
     __syncthreads();
-    double z[4][4];  // G' = Vp^T Y
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) z[i][j] = 0.0;
-    for (int k = 0; k < KMAX; ++k) {
-      double uk[4], yk[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) uk[i] = Vt[(4 * bi + i) * VLD + k];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) yk[j] = G[k * GLD + bj + 16 * j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) z[i][j] = fma(uk[i], yk[j], z[i][j]);
-    }
+    eig_mm64([&](int i, int k) { return Vt[i * VLD + k]; },
+             [&](int k, int j) { return G[k * GLD + j]; }, d);
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int t = 0; t < 8; ++t)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) G[(4 * bi + i) * GLD + bj + 16 * j] = z[i][j];
+      for (int e = 0; e < 2; ++e) G[(8 * warp + ar) * GLD + 8 * t + 2 * ak + e] = d[t][e];
     __syncthreads();
     // symmetrise (the product is symmetric up to rounding)
     for (int t = tid; t < GSZ; t += EIG_THREADS) {
@@ -566,35 +557,21 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
     atomicAdd(&g_rank_hist[kept], 1u);
   }
 #endif
-  // Wm = V diag(ratio) V^T -> global
-  double o[4][4];
+  // Wm = V diag(ratio) V^T -> global, on DMMA
+  double o[8][2];
+  eig_mm64([&](int i, int k) { return Vt[k * VLD + i] * ratio[k]; },
+           [&](int k, int j) { return Vt[k * VLD + j]; }, o);
+  {
+    const int ar = lane >> 2, ak = lane & 3;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) o[i][j] = 0.0;
-  for (int k = 0; k < KMAX; ++k) {
-    const double rk = ratio[k];
-    if (rk == 0.0) continue;
-    double x[4], y[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) x[i] = Vt[k * VLD + 4 * bi + i] * rk;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) y[j] = Vt[k * VLD + bj + 16 * j];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) o[i][j] = fma(x[i], y[j], o[i][j]);
+    for (int t = 0; t < 8; ++t)
+      *reinterpret_cast<double2*>(&Gg[(8 * warp + ar) * KMAX + 8 * t + 2 * ak]) =
+          make_double2(o[t][0], o[t][1]);
   }
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) Gg[(4 * bi + i) * KMAX + bj + 16 * j] = o[i][j];
   if (a.wmax) {
     double mx = 0.0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) mx = fmax(mx, fabs(o[i][j]));
+    for (int t = 0; t < 8; ++t) mx = fmax(mx, fmax(fabs(o[t][0]), fabs(o[t][1])));
     for (int o2 = 16; o2 > 0; o2 >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o2));
     __syncthreads();  // ratio[] is free again
     if (lane == 0) ratio[warp] = mx;

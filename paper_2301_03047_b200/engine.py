@@ -247,6 +247,7 @@ class GlrEngine:
         self._acur = 0
         self.warm = 0
         self.timing = None  # list of (name, start, end) CUDA events when profiling
+        self._side = None  # side stream for the edge stack (refresh)
         self.n = 0          # anchors in the current match state (all ranks)
         self.lo = self.hi = 0
         self.has_positions = False
@@ -266,6 +267,33 @@ class GlrEngine:
         if start is not None:
             self.timing.append((name, start, self._ev()))
 
+    def _edge_stack_side(self):
+        """glr_edge_stack on the side stream after the Sobel pass; returns the
+        event the main stream waits on before matching."""
+        torch = D.torch()
+        h, w, c = self.shape
+        main = torch.cuda.current_stream()
+        if self._side is None:
+            self._side = torch.cuda.Stream()
+        side = self._side
+        grads = torch.cuda.Event()
+        grads.record(main)
+        side.wait_event(grads)
+        e0 = e1 = None
+        if self.timing is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(side)
+        N.call("glr_edge_stack", self.gh.data_ptr(), self.gv.data_ptr(), h, w, c,
+               float(self.mc.edge_threshold), 1, self.expand, None, self.stack.data_ptr(),
+               self.ws_edge.data_ptr(), side.cuda_stream)
+        if e0 is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(side)
+            self.timing.append((("edge_stack", 1), e0, e1))
+        done = torch.cuda.Event()
+        done.record(side)
+        return done
+
     # -- refresh: solvers.py:154-167 + 187-203 ---------------------------------
     def refresh(self, x_d) -> int:
         """Exemplars, edge stack, heat map and top-K for this rank's shard.
@@ -273,12 +301,17 @@ class GlrEngine:
         h, w, c = self.shape
         mc = self.mc
         s = D.stream()
+        stack_ready = None
         if self.use_corners or self.global_match:
             # one Sobel pass feeds both the corner response and the edge stack
             e = self._ev()
             N.call("glr_sobel", x_d.data_ptr(), h, w, c, self.gh.data_ptr(), self.gv.data_ptr(),
                    s)
             self._log(("sobel", 1), e)
+        if self.global_match:
+            # the edge stack needs only the gradients: it runs on a side stream
+            # beside the corner response and the (single-CTA) greedy NMS
+            stack_ready = self._edge_stack_side()
         if self.use_corners:
             e = self._ev()
             N.call("glr_corner_response_grad", self.gh.data_ptr(), self.gv.data_ptr(), h, w, c,
@@ -311,11 +344,7 @@ class GlrEngine:
         if n == 0:
             return 0
         if self.global_match:
-            e = self._ev()
-            N.call("glr_edge_stack", self.gh.data_ptr(), self.gv.data_ptr(), h, w, c,
-                   float(mc.edge_threshold), 1, self.expand, None, self.stack.data_ptr(),
-                   self.ws_edge.data_ptr(), s)
-            self._log(("edge_stack", 1), e)
+            D.torch().cuda.current_stream().wait_event(stack_ready)
             self.match_shard()
             if mc.rerank_pixel and self.hi > self.lo:
                 e = self._ev()

@@ -431,13 +431,41 @@ def main():
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_spawn_ranks(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank "
+                         f"per GPU (torchrun --nproc-per-node {args.gpus}) or drop WORLD_SIZE")
     if args.impl == "reference":
         run_reference(args, rank)
         return
     run_b200(args, rank, world, local_rank)
+
+
+def _spawn_ranks(args) -> int:
+    """--gpus N without a launcher: re-exec this script under torchrun, one
+    rank per GPU (127.0.0.1 rendezvous). Fails loudly when the box has fewer
+    than N GPUs instead of running (and labelling) a smaller job."""
+    import socket
+    if args.impl != "reference":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} CUDA devices, this box has "
+                  f"{have}", file=sys.stderr, flush=True)
+            return 3
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

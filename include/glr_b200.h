@@ -240,8 +240,11 @@ int glr_scatter_add_f64(const double* groups_d, const int32_t* positions_d, int 
 int glr_scatter_fixed(const double* groups_d, const int32_t* positions_d, int G, int K, int P,
                       int H, int W, int C, int frac_bits, int64_t* acc_d, void* stream);
 
-/* glr_normalize: z = acc/cnt where cnt > 0 else x (lowrank.py:84-87).       */
-int glr_normalize(const int64_t* acc_d, const int32_t* cnt_d, const double* x_d, int H, int W,
+/* glr_normalize: z = acc/cnt where cnt > 0 else x (lowrank.py:84-87).
+ * The numerator is CONSUMED: covered entries are reset to 0 after the read
+ * (read-and-clear), so the next scatter starts from zero without a memset.
+ * The same holds for glr_gap_masksum / glr_gap_fourier.                    */
+int glr_normalize(int64_t* acc_d, const int32_t* cnt_d, const double* x_d, int H, int W,
                   int C, int frac_bits, double* z_d, void* stream);
 
 /* ---- (6) sensing operators + GAP update: glr/operators.py, solvers.py:298-301
@@ -257,7 +260,7 @@ int glr_masksum_forward(const double* x_d, const double* masks_d, int H, int W, 
 int glr_masksum_adjoint(const double* y_d, const double* masks_d, int H, int W, int T,
                         double* x_d, void* stream);
 size_t glr_gap_workspace(int H, int W);
-int glr_gap_masksum(const int64_t* acc_d, const int32_t* cnt_d, int frac_bits,
+int glr_gap_masksum(int64_t* acc_d, const int32_t* cnt_d, int frac_bits,
                     const double* x_in_d, const double* masks_d, const double* y_d,
                     const double* gram_d, int H, int W, int T, double lo, double hi,
                     double rho, double* x_out_d, double* resid_d, void* ws_d, void* stream);
@@ -271,7 +274,7 @@ int glr_fourier_forward(const double* x_d, const double* mask_d, int H, int W, i
                         double* y_d, void* ws_d, void* stream);
 int glr_fourier_adjoint(const double* y_d, const double* mask_d, int H, int W, int C,
                         double* x_d, void* ws_d, void* stream);
-int glr_gap_fourier(const int64_t* acc_d, const int32_t* cnt_d, int frac_bits,
+int glr_gap_fourier(int64_t* acc_d, const int32_t* cnt_d, int frac_bits,
                     const double* x_in_d, const double* mask_d, const double* y_d, int H, int W,
                     int C, int clip, double lo, double hi, double rho, double* x_out_d,
                     double* resid_d, void* ws_d, void* stream);

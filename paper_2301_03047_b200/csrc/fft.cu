@@ -105,7 +105,7 @@ int fft2_ortho(double2* data, int H, int W, int sign, cudaStream_t st) {
 // elementwise stages
 
 // z = normalised aggregate (or x), written to z_out; packed complex to buf
-__global__ void pack_kernel(const int64_t* __restrict__ acc, const int32_t* __restrict__ cnt,
+__global__ void pack_kernel(int64_t* __restrict__ acc, const int32_t* __restrict__ cnt,
                             double inv_scale, const double* __restrict__ x_in, int64_t npix, int C,
                             double* __restrict__ z_out, double2* __restrict__ buf) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npix;
@@ -114,7 +114,12 @@ __global__ void pack_kernel(const int64_t* __restrict__ acc, const int32_t* __re
     double v[2] = {0.0, 0.0};
     for (int c = 0; c < C; ++c) {
       const int64_t k = i * C + c;
-      v[c] = n > 0 ? ((double)acc[k] * inv_scale) / (double)n : x_in[k];
+      if (n > 0) {
+        v[c] = ((double)acc[k] * inv_scale) / (double)n;
+        acc[k] = 0;  // read-and-clear (the numerator is consumed)
+      } else {
+        v[c] = x_in[k];
+      }
       if (z_out) z_out[k] = v[c];
     }
     buf[i] = make_double2(v[0], C == 2 ? v[1] : 0.0);
@@ -258,7 +263,7 @@ extern "C" int glr_fourier_adjoint(const double* y_d, const double* mask_d, int 
   return check_launch("fourier_adjoint");
 }
 
-extern "C" int glr_gap_fourier(const int64_t* acc_d, const int32_t* cnt_d, int frac_bits,
+extern "C" int glr_gap_fourier(int64_t* acc_d, const int32_t* cnt_d, int frac_bits,
                                const double* x_in_d, const double* mask_d, const double* y_d, int H,
                                int W, int C, int clip, double lo, double hi, double rho,
                                double* x_out_d, double* resid_d, void* ws_d, void* stream) {

@@ -88,7 +88,7 @@ __global__ void final_sum_kernel(const double* __restrict__ part, int n, double*
 }
 
 struct GapArgs {
-  const int64_t* acc;
+  int64_t* acc;  // consumed: read, then reset to zero (read-and-clear)
   const int32_t* cnt;
   double inv_scale;
   const double* x_in;
@@ -122,13 +122,17 @@ __global__ void __launch_bounds__(gap::THREADS, 2) gap_masksum_kernel(GapArgs a)
         mk[2 * t + 1] = m.y;
       }
       if (n > 0) {
-        const longlong2* ac2 = reinterpret_cast<const longlong2*>(a.acc + i * TT);
+        longlong2* ac2 = reinterpret_cast<longlong2*>(a.acc + i * TT);
 #pragma unroll
         for (int t = 0; t < TT / 2; ++t) {
           const longlong2 v = ac2[t];
           z[2 * t] = ((double)v.x * a.inv_scale) / (double)n;
           z[2 * t + 1] = ((double)v.y * a.inv_scale) / (double)n;
         }
+        // read-and-clear: the numerator is zero again for the next
+        // iteration's scatter (uncovered pixels were never written)
+#pragma unroll
+        for (int t = 0; t < TT / 2; ++t) __stcs(ac2 + t, make_longlong2(0, 0));
       } else {
         const double2* x2 = reinterpret_cast<const double2*>(a.x_in + i * TT);
 #pragma unroll
@@ -143,7 +147,12 @@ __global__ void __launch_bounds__(gap::THREADS, 2) gap_masksum_kernel(GapArgs a)
       for (int t = 0; t < T; ++t) {
         const int64_t k = i * T + t;
         mk[t] = a.mk[k];
-        z[t] = n > 0 ? ((double)a.acc[k] * a.inv_scale) / (double)n : a.x_in[k];
+        if (n > 0) {
+          z[t] = ((double)a.acc[k] * a.inv_scale) / (double)n;
+          a.acc[k] = 0;
+        } else {
+          z[t] = a.x_in[k];
+        }
       }
     }
     double gram;
@@ -235,7 +244,7 @@ extern "C" int glr_masksum_adjoint(const double* y_d, const double* masks_d, int
 
 extern "C" size_t glr_gap_workspace(int H, int W) { return (kGapBlocks + 8) * sizeof(double); }
 
-extern "C" int glr_gap_masksum(const int64_t* acc_d, const int32_t* cnt_d, int frac_bits,
+extern "C" int glr_gap_masksum(int64_t* acc_d, const int32_t* cnt_d, int frac_bits,
                                const double* x_in_d, const double* masks_d, const double* y_d,
                                const double* gram_d, int H, int W, int T, double lo, double hi,
                                double rho, double* x_out_d, double* resid_d, void* ws_d,

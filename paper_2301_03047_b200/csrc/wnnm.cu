@@ -1143,13 +1143,18 @@ __global__ void scatter_fixed_kernel(const double* __restrict__ groups,
   }
 }
 
-__global__ void normalize_kernel(const int64_t* __restrict__ acc, const int32_t* __restrict__ cnt,
+__global__ void normalize_kernel(int64_t* __restrict__ acc, const int32_t* __restrict__ cnt,
                                  const double* __restrict__ x, int64_t npix, int C, double inv_scale,
                                  double* __restrict__ z) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npix * C;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int n = cnt[i / C];
-    z[i] = n > 0 ? ((double)acc[i] * inv_scale) / (double)n : x[i];
+    if (n > 0) {
+      z[i] = ((double)acc[i] * inv_scale) / (double)n;
+      acc[i] = 0;  // read-and-clear (the numerator is consumed)
+    } else {
+      z[i] = x[i];
+    }
   }
 }
 
@@ -1350,7 +1355,7 @@ extern "C" int glr_scatter_fixed(const double* groups_d, const int32_t* position
   return check_launch("scatter_fixed_kernel");
 }
 
-extern "C" int glr_normalize(const int64_t* acc_d, const int32_t* cnt_d, const double* x_d, int H,
+extern "C" int glr_normalize(int64_t* acc_d, const int32_t* cnt_d, const double* x_d, int H,
                              int W, int C, int frac_bits, double* z_d, void* stream) {
   const int64_t npix = (int64_t)H * W;
   normalize_kernel<<<blocks_for(npix * C), 256, 0, (cudaStream_t)stream>>>(

@@ -200,6 +200,10 @@ class GlrEngine:
         self.positions = self._pos[0]
         self.padded = D.empty((self.max_anchors,), t.int32)
         self.acc = D.zeros((h, w, c), t.int64)
+        # the numerator's consumers (glr_gap_masksum / glr_gap_fourier /
+        # glr_normalize) read AND clear it, so no per-iteration memset is
+        # needed; acc_dirty marks a numerator that was produced but not consumed
+        self.acc_dirty = False
         self.cnt = D.zeros((h, w), t.int32)
         self.gap_ws = D.empty((N.query("glr_gap_workspace", h, w),), t.uint8)
         self.ws_corner = D.empty((N.query("glr_corner_workspace", h, w, c),), t.uint8)
@@ -459,7 +463,9 @@ class GlrEngine:
         if self.n == 0:
             return False
         h, w, c = self.shape
-        self.acc.zero_()
+        if self.acc_dirty:  # a previous numerator was never consumed
+            self.acc.zero_()
+        self.acc_dirty = True
         nloc = self.hi - self.lo
         if nloc > 0:
             e = self._ev()
@@ -482,6 +488,20 @@ class GlrEngine:
             import torch.distributed as dist
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.pg)
 
+    def consumed(self):
+        """The numerator was read by a read-and-clear consumer."""
+        self.acc_dirty = False
+
     def positions_host(self):
+        """(anchors, positions, padded) of ALL groups. Each rank computes only
+        its shard's rows [lo, hi); with a process group the other rows are
+        assembled by an integer all-reduce (zeros outside the local shard)."""
         n = self.n
-        return D.host(self.anchors[:n]), D.host(self.positions[:n]), D.host(self.padded[:n])
+        pos, pad = self.positions[:n], self.padded[:n]
+        if self.pg is not None and self.world > 1 and n:
+            pos, pad = pos.clone(), pad.clone()
+            for tt in (pos, pad):
+                tt[:self.lo].zero_()
+                tt[self.hi:].zero_()
+                self._all_reduce(tt)
+        return D.host(self.anchors[:n]), D.host(pos), D.host(pad)

@@ -112,6 +112,7 @@ class MatchState:
     last_refresh: int = -1
     last_match_ms: float = 0.0
     engine: object = None
+    synced: object = None   # the positions list the engine's device copy holds
 
 
 def _expected_y_shape(op) -> tuple:
@@ -136,6 +137,43 @@ def _check_divergence(residuals: list[float], y_norm: float) -> None:
         raise SolverDivergenceError(
             f"data residual grew 10x over its minimum ({best:.3e}) for 20 "
             f"consecutive iterations, last {tail[-1]:.3e}")
+
+
+class _DivergenceGuard:
+    """solvers.py:272-281 checked while the solve runs, as the reference does
+    after every iteration (solvers.py:306-307), without a per-iteration host
+    sync: each iteration's squared residual is copied to pinned host memory
+    behind an event, and the check runs on every iteration whose copy has
+    landed. A diverging solve stops a few iterations after the failing one at
+    most and raises the reference's error for that iteration."""
+
+    def __init__(self, resid_sq_d, iters: int, y_norm: float):
+        t = D.torch()
+        self.src = resid_sq_d
+        self.host = t.empty((iters,), dtype=t.float64, pin_memory=True)
+        self.events: list = []
+        self.checked = 0
+        self.y_norm = y_norm
+
+    def push(self, it: int) -> None:
+        t = D.torch()
+        self.host[it:it + 1].copy_(self.src[it:it + 1], non_blocking=True)
+        e = t.cuda.Event()
+        e.record()
+        self.events.append(e)
+        self.poll()
+
+    def poll(self, block: bool = False) -> None:
+        while self.checked < len(self.events):
+            e = self.events[self.checked]
+            if block:
+                e.synchronize()
+            elif not e.query():
+                return
+            self.checked += 1
+            if self.checked >= 21:
+                res = np.sqrt(self.host[:self.checked].numpy()).tolist()
+                _check_divergence(res, self.y_norm)
 
 
 def _init_device(dop: DeviceOperator, y_d, cfg: SolverConfig):
@@ -171,11 +209,22 @@ def regularize_dispatch(x: np.ndarray, cfg: SolverConfig, state: MatchState,
             state.positions = [[tuple(q) for q in g] for g in pos.tolist()]
         else:
             state.positions = []
+        state.synced = state.positions
         state.last_refresh = iteration
         D.torch().cuda.synchronize()
         state.last_match_ms = (time.perf_counter() - t0) * 1e3
     else:
         state.last_match_ms = 0.0
+        if state.positions and (state.synced is not state.positions
+                                or eng.n != len(state.positions)):
+            # re-gather at the caller's cached positions (solvers.py:204-207):
+            # a state built or edited outside this engine is uploaded first
+            pos = np.asarray(state.positions, dtype=np.int32).reshape(-1, eng.k, 2)
+            if pos.shape[0] > eng.max_anchors:
+                raise ValueError(f"{pos.shape[0]} cached groups exceed the engine's "
+                                 f"{eng.max_anchors} anchors")
+            eng.set_positions(pos[:, 0, :], pos)
+            state.synced = state.positions
     if not state.positions:
         return x.copy()
     eng.regularize(x_d, sigma)
@@ -183,6 +232,7 @@ def regularize_dispatch(x: np.ndarray, cfg: SolverConfig, state: MatchState,
     h, w, c = x.shape
     N.call("glr_normalize", eng.acc.data_ptr(), eng.cnt.data_ptr(), x_d.data_ptr(), h, w, c,
            eng.frac, z.data_ptr(), D.stream())
+    eng.consumed()
     return D.host(z)
 
 
@@ -242,15 +292,21 @@ class GapRunner:
             return None
         return D.host(self.ssim_sum) / float(c * (h - 10) * (w - 10))
 
-    def run(self, y_d, positions_override=None, trace=None, on_iter=None, events=False):
+    def run(self, y_d, positions_override=None, trace=None, on_iter=None, events=False,
+            guard: _DivergenceGuard | None = None):
         """One full GAP-GLR solve (solvers.py:284-308) on device; returns the
-        final iterate (device tensor, before the final [0, peak] clip)."""
+        final iterate (device tensor, before the final [0, peak] clip).
+        ``guard`` runs the divergence check as iterations complete."""
         t = D.torch()
         cfg, dop, eng = self.cfg, self.dop, self.eng
         iters = cfg.max_iters
         x, x_next = self.xa, self.xb
         dop.init_x(y_d, x, cfg.init)
+        # a fresh solve: no match state and no eigenvector warm start carried
+        # over from a previous run() (gap_solve always starts cold)
         eng.has_positions = False
+        eng.vcache_valid = False
+        eng.warm = 0
         lo, hi = -0.5 * cfg.peak, 1.5 * cfg.peak
         self.events = ([[t.cuda.Event(enable_timing=True) for _ in range(4)]
                         for _ in range(iters)] if events else None)
@@ -287,11 +343,17 @@ class GapRunner:
                     ev[2].record()
                 dop.gap_update(eng.acc if has else None, eng.cnt if has else None, eng.frac, x,
                                y_d, lo, hi, x_next, self.resid_sq[it:it + 1], eng.gap_ws)
+                if has:
+                    eng.consumed()
             if ev:
                 ev[3].record()
             x, x_next = x_next, x
             if on_iter is not None:
                 on_iter(it, x)
+            if guard is not None:
+                guard.push(it)
+        if guard is not None:
+            guard.poll(block=True)
         return x
 
 
@@ -339,8 +401,9 @@ def gap_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = Non
         if ref_d is not None:
             runner.record_metrics(x, ref_d, it)
 
+    guard = _DivergenceGuard(runner.resid_sq, iters, float(np.linalg.norm(y.ravel())))
     x = runner.run(y_d, positions_override=positions_override, trace=trace,
-                   on_iter=on_iter, events=True)
+                   on_iter=on_iter, events=True, guard=guard)
     t.cuda.synchronize()
     res = np.sqrt(D.host(runner.resid_sq)).tolist()
     sqh = D.host(runner.sq) if ref_d is not None else None
@@ -359,9 +422,6 @@ def gap_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = Non
             row["ssim"] = float(ssims[it])
         report.add(**row)
     report.total_ms = (time.perf_counter() - t_start) * 1e3
-    y_norm = float(np.linalg.norm(y.ravel()))
-    for k in range(21, iters + 1):
-        _check_divergence(res[:k], y_norm)
     return _final_host(runner, x), report
 
 
@@ -383,7 +443,8 @@ class AdmmRunner(GapRunner):
                float(b), z.data_ptr() if z is not None else None, float(c), int(x.numel()),
                1 if clip else 0, lo, hi, out.data_ptr(), D.stream())
 
-    def run(self, y_d, positions_override=None, trace=None, on_iter=None, events=False):
+    def run(self, y_d, positions_override=None, trace=None, on_iter=None, events=False,
+            guard: _DivergenceGuard | None = None):
         t = D.torch()
         cfg, dop, eng = self.cfg, self.dop, self.eng
         iters = cfg.max_iters
@@ -392,6 +453,8 @@ class AdmmRunner(GapRunner):
         dop.init_x(y_d, z, cfg.init)
         u.zero_()
         eng.has_positions = False
+        eng.vcache_valid = False
+        eng.warm = 0
         lo, hi = -0.5 * cfg.peak, 1.5 * cfg.peak
         clip = dop.clip
         self.events = ([[t.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -426,6 +489,7 @@ class AdmmRunner(GapRunner):
             elif eng.regularize(v, cfg.sigma_at(it)):
                 N.call("glr_normalize", eng.acc.data_ptr(), eng.cnt.data_ptr(), v.data_ptr(),
                        h, w, c, eng.frac, z.data_ptr(), D.stream())
+                eng.consumed()
                 self._lincomb(z, z, 1.0, clip=clip)                            # z = clip(z)
             else:
                 self._lincomb(z, v, 1.0, clip=clip)
@@ -434,6 +498,10 @@ class AdmmRunner(GapRunner):
                 ev[3].record()
             if on_iter is not None:
                 on_iter(it, x)
+            if guard is not None:
+                guard.push(it)
+        if guard is not None:
+            guard.poll(block=True)
         return x
 
 
@@ -454,7 +522,8 @@ def admm_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = No
         if ref_d is not None:
             runner.record_metrics(x, ref_d, it)
 
-    x = runner.run(y_d, trace=trace, on_iter=on_iter, events=True)
+    guard = _DivergenceGuard(runner.resid_sq, cfg.max_iters, float(np.linalg.norm(y.ravel())))
+    x = runner.run(y_d, trace=trace, on_iter=on_iter, events=True, guard=guard)
     t.cuda.synchronize()
     res = np.sqrt(D.host(runner.resid_sq)).tolist()
     sqh = D.host(runner.sq) if ref_d is not None else None
@@ -472,9 +541,6 @@ def admm_solve(op, y: np.ndarray, cfg: SolverConfig, ref: np.ndarray | None = No
             row["ssim"] = float(ssims[it])
         report.add(**row)
     report.total_ms = (time.perf_counter() - t_start) * 1e3
-    y_norm = float(np.linalg.norm(y.ravel()))
-    for k in range(21, cfg.max_iters + 1):
-        _check_divergence(res[:k], y_norm)
     return _final_host(runner, x), report
 
 

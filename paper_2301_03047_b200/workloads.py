@@ -9,6 +9,7 @@ GPU path and the CPU oracle see identical values.
   C1  CACTI 256x256x8,   GAP 30 it, P=8, K=64, max_corners=512 (+ reference grid)
   C2  CACTI 1024x1024x24, GAP 50 it, P=8, K=64, 4096 exemplars
   C3  MRI 512x512 complex (re, im), Cartesian VD 25 %, GAP 40 it, P=8, K=48, 2048 ex.
+      (897 corners + the interval-15 grid = 2048 anchors on the first refresh)
   C4  MSFA 512x512x16, periodic 4x4, GAP 30 it, P=8, K=64, 2048 exemplars
   C5  2048x2048x1 stage sweep (matching / top-K / WNNM / aggregation only)
 """
@@ -143,11 +144,12 @@ def make(name: str, seed: int = 0) -> Workload:
         z = scene[:, :, 0] + 1j * scene[:, :, 1]
         y = mask * (np.fft.fft2(z, norm="ortho")
                     + 0.005 * (rng.normal(size=(h, w)) + 1j * rng.normal(size=(h, w))))
-        # the piecewise-constant phantom yields a few hundred Shi-Tomasi corners;
+        # the piecewise-constant phantom yields 944 Shi-Tomasi corners (nms 4);
         # the reference's glr mode unions them with a uniform grid
-        # (solvers.py:165-167), here at interval 12 (exemplar_stride 4, 43 x 43
-        # anchors) for ~2048 exemplars in total
-        mc = MatchConfig(patch_size=8, group_size=48, max_corners=2048, exemplar_stride=4)
+        # (solvers.py:165-167), here at interval 15 (exemplar_stride 5, 34 x 34
+        # anchors): the first 897 corners plus the grid deduplicate to exactly
+        # the config's 2048 exemplars on the first refresh
+        mc = MatchConfig(patch_size=8, group_size=48, max_corners=897, exemplar_stride=5)
         return Workload(name, "fourier", scene, mask, y, 40, mc, 0.005)
     if name == "C4":
         h = w = 512

@@ -458,6 +458,131 @@ def gen_tv():
     np.savez_compressed(OUT / "tv.npz", **cases)
 
 
+class _StopSolve(Exception):
+    pass
+
+
+class _NoClip:
+    """Stand-in for the reference module's ``np`` whose ``clip`` is the
+    identity: the documented no-clip policy for complex (re, im) images
+     applied to the UNMODIFIED gap_solve code."""
+
+    def __getattr__(self, name):
+        return getattr(np, name)
+
+    @staticmethod
+    def clip(a, lo, hi):
+        return a
+
+
+def _complex_fourier_operator(mask):
+    """operators.py:65-89 minus ``.real`` on (H, W, 2) = (re, im)."""
+    from glr.operators import SensingOperator
+    mask = np.asarray(mask, dtype=np.float64)
+    h, w = mask.shape
+
+    def fwd(x):
+        x = np.asarray(x, dtype=np.float64)
+        return mask * np.fft.fft2(x[:, :, 0] + 1j * x[:, :, 1], norm="ortho")
+
+    def adj(y):
+        z = np.fft.ifft2(mask * y, norm="ortho")
+        return np.stack([z.real, z.imag], axis=2)
+
+    return SensingOperator(kind="fourier", forward=fwd, adjoint=adj, gram_diag=mask.copy(),
+                           x_shape=(h, w, 2), meta={"mask": mask})
+
+
+def gen_configs(names=("C1", "C3", "C4")):
+    """BASELINE.json configurations at FULL size, run by the unmodified
+    reference gap_solve on the package's seeded workloads (inputs are the
+    same fp32-rounded arrays the GPU path sees):
+
+      C1  all 30 iterations: every refresh's anchors + positions, the
+          per-iteration residuals and the final clip(x, 0, 1)
+      C3  first 10 of 40 iterations (complex operator, no-clip policy)
+      C4  first 10 of 30 iterations
+
+    For C3/C4 the solve is stopped when iteration 10 begins (the iterate
+    handed to regularize_dispatch = x after 10 iterations, with the
+    max_iters of the config so the sigma schedule is the config's). Stored:
+    the first two refreshes' anchors/positions (int16), the residuals, x
+    (C3 full, float32; C4 a seeded sample of 2**18 entries, float64, plus
+    sum / sum of squares / PSNR of the full array)."""
+    import time
+    sys.path.insert(0, str(OUT.parents[1]))
+    from paper_2301_03047_b200 import workloads
+    for name in names:
+        wl = workloads.make(name)
+        mc = wl.match
+        stop_at = {"C1": None, "C3": 10, "C4": 10}[name]
+        if wl.kind == "cacti":
+            op = glr.cacti_operator(wl.masks)
+        elif wl.kind == "msfa":
+            op = glr.msfa_operator(wl.masks)
+        else:
+            op = _complex_fourier_operator(wl.masks)
+        cfg = glr.SolverConfig(regularizer="glr", max_iters=wl.max_iters,
+                               match=glr.MatchConfig(patch_size=mc.patch_size,
+                                                     group_size=mc.group_size,
+                                                     max_corners=mc.max_corners,
+                                                     exemplar_stride=mc.exemplar_stride))
+        captured, resid, stopped = [], [], {}
+        orig_gm, orig_rd, orig_rec = (ref_solvers.global_match, ref_solvers.regularize_dispatch,
+                                      ref_solvers._record)
+        orig_np = ref_solvers.np
+
+        def spy_gm(x, exemplars, c, edge):
+            groups = orig_gm(x, exemplars, c, edge)
+            captured.append((list(exemplars.anchors), [g.positions for g in groups]))
+            return groups
+
+        def spy_rd(x, c, state, iteration=0, sigma=None):
+            if stop_at is not None and iteration == stop_at:
+                stopped["x"] = np.array(x, copy=True)
+                raise _StopSolve()
+            return orig_rd(x, c, state, iteration=iteration, sigma=sigma)
+
+        def spy_rec(*a, **k):
+            r = orig_rec(*a, **k)
+            resid.append(r)
+            return r
+
+        ref_solvers.global_match, ref_solvers.regularize_dispatch = spy_gm, spy_rd
+        ref_solvers._record = spy_rec
+        if wl.kind == "fourier":
+            ref_solvers.np = _NoClip()
+        t0 = time.perf_counter()
+        try:
+            out, _ = glr.gap_solve(op, wl.y, cfg)
+        except _StopSolve:
+            out = stopped["x"]
+        finally:
+            ref_solvers.global_match, ref_solvers.regularize_dispatch = orig_gm, orig_rd
+            ref_solvers._record = orig_rec
+            ref_solvers.np = orig_np
+        secs = time.perf_counter() - t0
+        keep = len(captured) if stop_at is None else 2
+        cases = {"name": np.array(name), "iters": np.array(len(resid)),
+                 "resid": np.array(resid), "nref": np.array(keep),
+                 "seconds": np.array(secs)}
+        for j, (anc, pos) in enumerate(captured[:keep]):
+            cases[f"anchors_{j}"] = np.array(anc, dtype=np.int16)
+            cases[f"positions_{j}"] = np.array(pos, dtype=np.int16)
+        if name == "C4":
+            rng = np.random.default_rng(4242)
+            idx = np.sort(rng.choice(out.size, size=1 << 18, replace=False))
+            cases.update(sample_idx=idx.astype(np.int32), sample=out.ravel()[idx],
+                         x_sum=np.array(out.sum()), x_sumsq=np.array((out * out).sum()),
+                         psnr=np.array(glr.psnr(wl.scene, np.clip(out, 0, 1), 1.0)))
+        else:
+            cases.update(x=out.astype(np.float32),
+                         psnr=np.array(glr.psnr(wl.scene, np.clip(out, 0, 1), 1.0)))
+        np.savez_compressed(OUT / f"config_{name}.npz", **cases)
+        print(name, f"{secs:.1f} s", len(resid), "iterations", len(captured), "refreshes",
+              [len(a) for a, _ in captured], flush=True)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:

@@ -59,6 +59,31 @@ def _peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def _tc_peaks() -> dict:
+    """Measured dense tcgen05 rates per kind (tools/micro/tc_peak.cu on a
+    B200 of this pool, profiles/r02_tc_peak.json): {kind: TFLOP/s}."""
+    p = ROOT / "profiles" / "r02_tc_peak.json"
+    out = {}
+    if p.exists():
+        for line in p.read_text().splitlines():
+            line = line.strip()
+            if line.startswith("{"):
+                d = json.loads(line)
+                out[d["kind"].split()[0]] = float(d["tflops"])
+    return out
+
+
+def _fp4_peak(peaks) -> dict:
+    """Peak for the heat map's kind::mxf4 MMAs: the measured microbenchmark
+    rate when recorded, else 4 x the driver's measured bf16 rate (the dense
+    fp4 : bf16 ratio, 9 : 2.25 PFLOP/s nominal)."""
+    tc = _tc_peaks()
+    if "e2m1" in tc:
+        return {"tflops": tc["e2m1"], "kind": "measured tcgen05 kind::mxf4 dense rate "
+                                              "(tools/micro/tc_peak.cu, profiles/r02_tc_peak.json)"}
+    return {"tflops": 4.0 * peaks["bf16_tflops"], "kind": "fp4 (kind::mxf4) = 4 x measured bf16"}
+
+
 # ---------------------------------------------------------------------------
 # clocks sampler (B200_PROFILING.md clocks line)
 
@@ -351,12 +376,11 @@ def run_b200(args, rank, world, local_rank):
             flops = 2.0 * oh * ow * 4 * c * mp * mp * d["units"] / d["launches"]
             avg_s = d["ms"] / d["launches"] / 1e3
             ach = flops / avg_s / 1e12
-            # tcgen05 kind::mxf4 (dense fp4) peak = 4x the dense bf16 rate
-            # (9 vs 2.25 PFLOP/s nominal), scaled from the measured bf16 peak
-            pk = 4.0 * peaks["bf16_tflops"]
+            fp4 = _fp4_peak(peaks)
+            pk = fp4["tflops"]
             roof[hk] = {"bound": "tensor", "achieved": ach, "peak": pk,
                         "unit": "TFLOP/s", "frac": ach / pk,
-                        "peak_kind": "fp4 (kind::mxf4) = 4 x measured bf16",
+                        "peak_kind": fp4["kind"],
                         "avg_ms": d["ms"] / d["launches"]}
         if "wnnm_scatter" in kern:
             d = kern["wnnm_scatter"]
@@ -422,13 +446,160 @@ def run_b200(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+def run_b200_c5(args, rank, world, local_rank):
+    """C5, the isolated-stage sweep (BASELINE.json configs[4]): no solver
+    loop. A step = one pass of the stages over the seeded 2048x2048x1 image:
+    exemplar detection, edge stack, heat map + exact top-K for every exemplar
+    of this rank's shard, then one batched WNNM + fixed-point aggregation
+    (+ all-reduce) and the normalisation. metric = matches/s = N x M
+    exemplar-position scores per second of the whole step (N exemplars over
+    all ranks, M = (H-P+1)(W-P+1) positions); exemplars shard over the ranks
+    (strong scaling, the image is replicated)."""
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    pg = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        pg = dist.group.WORLD
+    import paper_2301_03047_b200 as G
+    from paper_2301_03047_b200 import _device as D, _native as N, workloads
+    from paper_2301_03047_b200.engine import GlrEngine
+    wl = workloads.make("C5")
+    h, w, c = wl.shape
+    p, n_req = args.c5_patch, args.c5_exemplars
+    mc = G.MatchConfig(patch_size=p, group_size=64, max_corners=n_req, exemplar_stride=4096)
+    eng = GlrEngine((h, w, c), mc, process_group=pg)
+    x_host = torch.from_numpy(np.ascontiguousarray(wl.scene)).pin_memory()
+    x_d = x_host.to("cuda")
+    z_d = torch.empty_like(x_d)
+    sigma = 0.05
+
+    def step(x):
+        eng.refresh(x)
+        eng.regularize(x, sigma)
+        N.call("glr_normalize", eng.acc.data_ptr(), eng.cnt.data_ptr(), x.data_ptr(), h, w, c,
+               eng.frac, z_d.data_ptr(), D.stream())
+        eng.consumed()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step(x_d)
+    torch.cuda.synchronize()
+    clocks = Clocks() if rank == 0 else None
+    eng.timing = []
+    barrier()
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.start()
+    launches0 = N.launch_count
+    ev = []
+    for _ in range(args.steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        step(x_d)
+        e1.record()
+        ev.append((e0, e1))
+    torch.cuda.synchronize()
+    barrier()
+    launches = N.launch_count - launches0
+    ck = clocks.stop(local_rank) if clocks else None
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    kern = {}
+    for (name, nb), a, b in eng.timing:
+        d = kern.setdefault(name, {"launches": 0, "ms": 0.0, "units": 0})
+        d["launches"] += 1
+        d["ms"] += a.elapsed_time(b)
+        d["units"] += nb
+    eng.timing = None
+    n_ex = eng.n
+    M = (h - p + 1) * (w - p + 1)
+    value = args.steps * n_ex * M / (ms / 1e3)
+    # e2e: host image in (pinned H2D) and the match positions out (D2H) per step
+    pos_host = torch.empty((n_ex, mc.group_size, 2), dtype=torch.int32, pin_memory=True)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, 3))
+    for _ in range(e2e_steps):
+        xd = x_host.to("cuda", non_blocking=True)
+        step(xd)
+        pos_host.copy_(eng.positions[:n_ex], non_blocking=True)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    if rank == 0:
+        peaks, peak_src = _peaks()
+        fp4 = _fp4_peak(peaks)
+        roof = {}
+        if "heat_map" in kern:
+            d = kern["heat_map"]
+            flops = 2.0 * M * 4 * c * p * p * d["units"] / d["launches"]
+            ach = flops / (d["ms"] / d["launches"] / 1e3) / 1e12
+            roof["heat_map"] = {"bound": "tensor", "achieved": ach, "peak": fp4["tflops"],
+                                "unit": "TFLOP/s", "frac": ach / fp4["tflops"],
+                                "peak_kind": fp4["kind"], "avg_ms": d["ms"] / d["launches"]}
+        if "topk" in kern:
+            d = kern["topk"]
+            ach = 2.0 * M * d["units"] / d["launches"] / (d["ms"] / d["launches"] / 1e3) / 1e9
+            roof["topk"] = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
+                            "unit": "GB/s", "frac": ach / peaks["hbm_gbs"],
+                            "avg_ms": d["ms"] / d["launches"]}
+        dominant = max(kern, key=lambda k: kern[k]["ms"]) if kern else None
+        roofline = dict(roof.get(dominant, {})) if dominant else {}
+        roofline.update({"kernel": dominant, "traffic": None,
+                         "peak_source": f"{peak_src} (MEASURED_PEAKS.json)"})
+        line = {
+            "metric": f"C5 matches/s (2048x2048x1 stage pass: exemplars, heat map + top-K, WNNM "
+                      f"+ aggregation; P={p}, K=64)",
+            "value": value, "unit": "matches/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64+e2m1+s8",
+            "data": "synthetic (seeded generator, workloads.py)",
+            "config": {"workload": f"C5: 2048x2048x1 blob+texture, P={p}, K=64, "
+                                   f"max_corners={n_req} (+1 grid anchor)",
+                       "exemplars": n_ex, "positions": M,
+                       "parallelism": f"exemplar-shard x{world}",
+                       "l2": "inputs > L2 (heat map "
+                             f"{n_ex * M * 2 / 1e9:.1f} GB per step)", "seed": 0},
+            "e2e": {"value": e2e_steps * n_ex * M / e2e_s, "unit": "matches/s",
+                    "h2d_bytes_per_step": int(x_host.numel() * 8),
+                    "d2h_bytes_per_step": int(pos_host.numel() * 4), "steps": e2e_steps},
+            "groups_per_s": args.steps * n_ex / (ms / 1e3),
+            "gpu_launches": int(launches),
+            "roofline": roofline,
+            "kernels": {k: {"launches": d["launches"], "ms_total": round(d["ms"], 3),
+                            "share_of_step": round(d["ms"] / ms, 4), **roof.get(k, {})}
+                        for k, d in kern.items()},
+            "clocks": ck,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--c5-patch", type=int, default=8, choices=[8, 12],
+                    help="C5 stage sweep: patch size")
+    ap.add_argument("--c5-exemplars", type=int, default=4096,
+                    help="C5 stage sweep: exemplar count (1024 / 4096 / 16384)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.gpus < 1:
@@ -443,6 +614,9 @@ def main():
                          f"per GPU (torchrun --nproc-per-node {args.gpus}) or drop WORLD_SIZE")
     if args.impl == "reference":
         run_reference(args, rank)
+        return
+    if args.config == "C5":
+        run_b200_c5(args, rank, world, local_rank)
         return
     run_b200(args, rank, world, local_rank)
 

@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "internal.cuh"
 
 namespace glr {
 namespace bm {
@@ -339,8 +340,7 @@ extern "C" int glr_xcorr_valid(const double* x_d, int H, int W, int C, const dou
   if (N == 0) return GLR_OK;
   const size_t smem = (size_t)P * P * C * 8;
   GLR_REQUIRE(smem <= 227 * 1024, GLR_ERR_UNSUPPORTED, "xcorr: kernel too large");
-  GLR_CUDA(cudaFuncSetAttribute(xcorr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
+  { const int s_ = ensure_smem_attr((const void*)xcorr_kernel, (int)smem); if (s_) return s_; }
   const int64_t M = (int64_t)(H - P + 1) * (W - P + 1);
   dim3 grid((unsigned)std::min<int64_t>(cdiv(M, 256), 4 * kNumSMs), (unsigned)N);
   xcorr_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(x_d, H, W, C, k_d, N, P, out_d);
@@ -390,8 +390,7 @@ extern "C" int glr_block_match(const double* x_d, int H, int W, int C, int P,
   const size_t smem = fixed + (size_t)((band - 1) * stride + P) * row_bytes;
   GLR_REQUIRE(smem <= 227 * 1024, GLR_ERR_UNSUPPORTED,
               "block_match: window needs %zu bytes of shared memory", smem);
-  GLR_CUDA(cudaFuncSetAttribute(block_match_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
+  { const int s_ = ensure_smem_attr((const void*)block_match_kernel, (int)smem); if (s_) return s_; }
   block_match_kernel<<<n, bm::THREADS, smem, (cudaStream_t)stream>>>(a);
   return check_launch("block_match_kernel");
 }
@@ -403,8 +402,7 @@ extern "C" int glr_rerank_pixel(const double* x_d, int H, int W, int C, int P,
   if (n <= 0 || K == 1) return GLR_OK;
   const size_t smem = (size_t)P * P * C * 8 + (size_t)K * 16;
   GLR_REQUIRE(smem <= 227 * 1024, GLR_ERR_UNSUPPORTED, "rerank: patch too large");
-  GLR_CUDA(cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
+  { const int s_ = ensure_smem_attr((const void*)rerank_kernel, (int)smem); if (s_) return s_; }
   const int threads = std::min(1024, std::max(64, (K + 31) / 32 * 32));
   rerank_kernel<<<n, threads, smem, (cudaStream_t)stream>>>(x_d, H, W, C, P, positions_d, K);
   return check_launch("rerank_kernel");

@@ -2,8 +2,12 @@
 // version and device probe.
 #include <cstdarg>
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "common.cuh"
+#include "internal.cuh"
 
 namespace glr {
 
@@ -24,6 +28,51 @@ int check_launch(const char* what) {
   }
   return GLR_OK;
 }
+
+namespace {
+std::mutex g_dev_mu;
+std::map<std::pair<const void*, int>, int> g_dev_cache;  // (key, device) -> value
+}  // namespace
+
+int ensure_smem_attr(const void* kernel, int bytes) {
+  int dev = 0;
+  GLR_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_dev_mu);
+  auto it = g_dev_cache.find({kernel, dev});
+  if (it != g_dev_cache.end() && it->second >= bytes) return GLR_OK;
+  GLR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  g_dev_cache[{kernel, dev}] = bytes;
+  return GLR_OK;
+}
+
+static int query_sms(void*) {
+  int dev = 0, sms = kNumSMs;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    sms = kNumSMs;
+  cudaGetLastError();
+  return sms;
+}
+
+int cached_per_device(const void* key, int (*init)(void* ctx), void* ctx) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    dev = 0;
+  }
+  {
+    std::lock_guard<std::mutex> lock(g_dev_mu);
+    auto it = g_dev_cache.find({key, dev});
+    if (it != g_dev_cache.end()) return it->second;
+  }
+  const int v = init(ctx);  // outside the lock (may launch occupancy queries)
+  std::lock_guard<std::mutex> lock(g_dev_mu);
+  g_dev_cache.emplace(std::make_pair(key, dev), v);
+  return v;
+}
+
+static const char kSmsKey = 0;
+int device_sms() { return cached_per_device(&kSmsKey, query_sms, nullptr); }
 
 }  // namespace glr
 

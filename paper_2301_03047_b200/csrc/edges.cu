@@ -15,6 +15,7 @@
 #include <cub/cub.cuh>
 
 #include "common.cuh"
+#include "internal.cuh"
 
 namespace glr {
 
@@ -883,11 +884,9 @@ extern "C" int glr_corner_response_grad(const double* gh_d, const double* gv_d, 
   const int row_bytes = (C | 1) * (int)sizeof(double);
   const int threads = std::max(32, std::min(256, (200 * 1024 / row_bytes) / 32 * 32));
   const int smem = threads * row_bytes;
-  static int attr_done = 0;
-  if (smem > 48 * 1024 && smem > attr_done) {
-    GLR_CUDA(cudaFuncSetAttribute(grad_mean_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  smem));
-    attr_done = smem;
+  if (smem > 48 * 1024) {
+    const int s = ensure_smem_attr((const void*)grad_mean_kernel, smem);
+    if (s) return s;
   }
   grad_mean_kernel<<<grid_for(npix, threads), threads, smem, st>>>(gh_d, gv_d, npix, C, mag);
   st_products_kernel<<<grid_for(npix), 256, 0, st>>>(mag, H, W, pxx, pyy, pxy);
@@ -949,23 +948,18 @@ extern "C" int glr_corners(const double* resp_d, int H, int W, int max_n, int nm
   const size_t batch_bytes = ((bm_bytes + 15) & ~size_t(15)) + nmsb::kBatchBytes;
   constexpr int kBatchSmemMax = 226 * 1024;  // 227 KB less the kernel's static shared memory
   if (batch_bytes <= (size_t)kBatchSmemMax && nms_radius <= 64) {
-    static bool battr = false;
-    if (!battr) {
-      GLR_CUDA(cudaFuncSetAttribute(nms_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kBatchSmemMax));
-      battr = true;
+    {
+      const int s = ensure_smem_attr((const void*)nms_batch_kernel, kBatchSmemMax);
+      if (s) return s;
     }
     nms_batch_kernel<<<1, nmsb::B, batch_bytes, st>>>(v_out, n_cand, H, W, max_n, nms_radius,
                                                       out_rc_d, out_n_d);
     return check_launch("nms_batch_kernel");
   }
   if (bm_bytes <= (size_t)kNmsBitmapMaxBytes && nms_radius <= 15) {
-    static bool attr = false;
-    if (!attr) {
-      GLR_CUDA(cudaFuncSetAttribute(nms_bitmap_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kNmsBitmapMaxBytes));
-      attr = true;
+    {
+      const int s = ensure_smem_attr((const void*)nms_bitmap_kernel, kNmsBitmapMaxBytes);
+      if (s) return s;
     }
     nms_bitmap_kernel<<<1, 1024, bm_bytes, st>>>(v_out, n_cand, H, W, max_n, nms_radius,
                                                  out_rc_d, out_n_d);

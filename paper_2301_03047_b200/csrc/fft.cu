@@ -11,6 +11,7 @@
 // (rows, then columns with strided loads), twiddles from sincospi on exact
 // dyadic fractions; lengths that are not powers of two use a direct DFT.
 #include "common.cuh"
+#include "internal.cuh"
 #include "fft.cuh"
 
 namespace glr {
@@ -83,13 +84,11 @@ static int fft_lines(double2* data, int n, int lines, int64_t line_stride, int64
   const size_t smem = (size_t)(pow2 ? n : 2 * n) * sizeof(double2);
   GLR_REQUIRE(smem <= 200 * 1024, GLR_ERR_UNSUPPORTED, "fft: length %d too large", n);
   if (pow2) {
-    GLR_CUDA(cudaFuncSetAttribute(fft_pow2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+    { const int s_ = ensure_smem_attr((const void*)fft_pow2_kernel, (int)smem); if (s_) return s_; }
     fft_pow2_kernel<<<lines, threads, smem, st>>>(data, n, log2n, line_stride, elem_stride, sign,
                                                   scale);
   } else {
-    GLR_CUDA(cudaFuncSetAttribute(dft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+    { const int s_ = ensure_smem_attr((const void*)dft_kernel, (int)smem); if (s_) return s_; }
     dft_kernel<<<lines, threads, smem, st>>>(data, n, line_stride, elem_stride, sign, scale);
   }
   return check_launch("fft_lines");

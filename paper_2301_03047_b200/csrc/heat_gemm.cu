@@ -435,16 +435,13 @@ static int run_heat(const uint8_t* stack_d, int H, int W, int P, const HeatGeom&
   hp.cnt = cnt_d;
   hp.cand = cand_d;
   hp.cap = cap;
-  static bool attr_set = false;
-  if (!attr_set) {
-    GLR_CUDA(cudaFuncSetAttribute(heat_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  heat::SMEM_BYTES));
-    attr_set = true;
+  {
+    const int s = ensure_smem_attr((const void*)heat_gemm_kernel, heat::SMEM_BYTES);
+    if (s) return s;
   }
   const int64_t pairs = (int64_t)g.oh * (hp.m_tiles_per_row / 2) * (n_pad / heat::BN);
   GLR_REQUIRE(pairs < (1ll << 31), GLR_ERR_UNSUPPORTED, "heat_map: too many tiles");
-  int sms = kNumSMs;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int sms = device_sms();
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(heat::THREADS);
   cfg.dynamicSmemBytes = heat::SMEM_BYTES;
@@ -458,14 +455,24 @@ static int run_heat(const uint8_t* stack_d, int H, int W, int P, const HeatGeom&
   cfg.numAttrs = 1;
   // persistent: one CTA per SM, in clusters of two -- as many clusters as can
   // be co-resident (the GPCs need not split into pairs evenly)
-  static int max_clusters = 0;
-  if (max_clusters == 0) {
-    cfg.gridDim = dim3(2 * (sms / 2));
-    if (cudaOccupancyMaxActiveClusters(&max_clusters, heat_gemm_kernel, &cfg) != cudaSuccess ||
-        max_clusters < 1)
-      max_clusters = sms / 2;
-    cudaGetLastError();
-  }
+  // (per device: the occupancy query depends on the device's GPC layout)
+  struct Q {
+    cudaLaunchConfig_t* cfg;
+    int sms;
+  } q{&cfg, sms};
+  const int max_clusters = cached_per_device(
+      (const void*)heat_gemm_kernel,
+      [](void* ctx) -> int {
+        Q* qq = static_cast<Q*>(ctx);
+        qq->cfg->gridDim = dim3(2 * (qq->sms / 2));
+        int mc = 0;
+        if (cudaOccupancyMaxActiveClusters(&mc, heat_gemm_kernel, qq->cfg) != cudaSuccess ||
+            mc < 1)
+          mc = qq->sms / 2;
+        cudaGetLastError();
+        return mc;
+      },
+      &q);
   cfg.gridDim = dim3(2 * (unsigned)std::min<int64_t>(pairs, max_clusters));
   GLR_CUDA(cudaLaunchKernelEx(&cfg, heat_gemm_kernel, tmA, tmB, hp));
   return GLR_OK;

@@ -726,8 +726,7 @@ extern "C" int glr_topk(const uint16_t* heat_d, int n_max, const int32_t* n_dev_
         (reinterpret_cast<uintptr_t>(ws_d) + 255) & ~uintptr_t(255));
     p.scap = kTopkScratch;
   }
-  GLR_CUDA(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
+  { const int s_ = ensure_smem_attr((const void*)topk_kernel, (int)smem); if (s_) return s_; }
   topk_kernel<<<n_max, topk::THREADS, smem, (cudaStream_t)stream>>>(p);
   return check_launch("topk_kernel");
 }
@@ -748,8 +747,7 @@ int topk_cand_launch(const uint64_t* cand_d, const uint32_t* cnt_d, const uint16
   q.thr = thr_d;
   q.cap = cap;
   q.fallback = fallback_d;
-  GLR_CUDA(cudaFuncSetAttribute(topk_cand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
+  { const int s_ = ensure_smem_attr((const void*)topk_cand_kernel, (int)smem); if (s_) return s_; }
   topk_cand_kernel<<<n_max, topk::THREADS, smem, (cudaStream_t)stream>>>(q);
   return check_launch("topk_cand_kernel");
 }

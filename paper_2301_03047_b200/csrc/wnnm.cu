@@ -20,6 +20,7 @@
 //                 (exact, order-independent: bitwise deterministic for any
 //                 exemplar sharding), or written out for the explicit-group API.
 #include "common.cuh"
+#include "internal.cuh"
 
 namespace glr {
 
@@ -291,6 +292,22 @@ __device__ __forceinline__ void eig_mm64(FA A, FB B, double (&d)[8][2]) {
   }
 }
 
+// True when the WNNM shrinkage maps EVERY eigenvalue <= lam to zero:
+// r(lam) = max(s - w(s), 0) / s with s = sqrt(lam) (lowrank.py:58-64) is
+// nondecreasing in lam (s grows, w = c sqrt(K) sigma^2 / (sigma_hat + eps)
+// shrinks), so r(lam) == 0 covers everything below it.
+__device__ __forceinline__ bool shrinks_to_zero(const EigArgs& a, double lam) {
+  const double s = sqrt(fmax(lam, 0.0));
+  double w;
+  if (a.uniform_weight >= 0.0) {
+    w = a.uniform_weight;
+  } else {
+    const double sig_hat = sqrt(fmax(s * s - a.K * a.sigma * a.sigma, 0.0));
+    w = a.c_weight * sqrt((double)a.K) * a.sigma * a.sigma / (sig_hat + a.eps);
+  }
+  return s - w <= 0.0;
+}
+
 __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double* sm) {
   using namespace wn;
   double* G = sm;               // KMAX x GLD, exactly symmetric throughout
@@ -363,6 +380,7 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
   __shared__ double Qs[2][16][16];  // Qs[buf][4*r + c][quad] = Q_quad[r][c]
   __shared__ double Ds[16][16];     // rotated diagonal block, same layout
   __shared__ unsigned s_qrot[2];
+  __shared__ unsigned char s_zb[8];  // per warp: zero-shrinkage flags of its 8 rows
   const int qA = 2 * warp + (lane >> 4), qB = lane & 15;
   int gsr = 0, prev_sr = -1;  // running super-round count; pending V step
   auto v_step = [&](int buf, int srv, int t0, int nthreads) {
@@ -392,14 +410,44 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
     }
   };
   int sweep = 0;
+  uint64_t zmask = 0;  // indices whose whole Gershgorin disc shrinks to zero
   for (; sweep < MAX_SWEEPS; ++sweep) {
+    // Zero-shrinkage exemption: index i is in Z when r(g_ii + sum_k |g_ik|)
+    // == 0, i.e. every eigenvalue its Gershgorin disc can hold is mapped to
+    // zero by the WNNM shrinkage. Rotations between two Z indices only
+    // change the basis inside an invariant subspace whose contribution to
+    // Wm = V diag(f(s)/s) V^T is exactly zero (the Z-block's eigenvalues all
+    // lie below the threshold, by Gershgorin on that block), so they are
+    // skipped; pairs with at least one non-Z index follow the usual test.
+    // Z is recomputed from the current G before every sweep, so the sweeps
+    // stop only once every non-exempt pair has converged on the final G.
+    {
+      const int i = tid >> 2, q = tid & 3;
+      double r = 0.0;
+#pragma unroll 4
+      for (int k = 16 * q; k < 16 * q + 16; ++k) r += k == i ? 0.0 : fabs(G[i * GLD + k]);
+      r += __shfl_xor_sync(0xffffffffu, r, 1);
+      r += __shfl_xor_sync(0xffffffffu, r, 2);
+      const bool z = shrinks_to_zero(a, G[i * GLD + i] + r);
+      const unsigned b = __ballot_sync(0xffffffffu, z && q == 0);
+      if (lane == 0) {
+        unsigned char m8 = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m8 |= ((b >> (4 * k)) & 1u) << k;
+        s_zb[warp] = m8;
+      }
+    }
+    __syncthreads();
+    zmask = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) zmask |= (uint64_t)s_zb[k] << (8 * k);
     // A sweep changes G only if some pair passes the rotation test on the
     // current G (otherwise no round rotates, by induction): test all pairs
     // up front and stop without paying for a no-op sweep.
     bool need = false;
     for (int t = tid; t < GSZ; t += EIG_THREADS) {
       const int i = t >> 6, j = t & 63;
-      if (i < j)
+      if (i < j && !((zmask >> i) & (zmask >> j) & 1ull))
         need |= fabs(G[i * GLD + j]) >
                 fmax(kRotTol * sqrt(fabs(G[i * GLD + i] * G[j * GLD + j])), tiny);
     }
@@ -436,7 +484,8 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
               app[h] = S[p][p];
               aqq[h] = S[q][q];
               apq[h] = S[p][q];
-              const bool rot = fabs(apq[h]) > fmax(kRotTol * sqrt(fabs(app[h] * aqq[h])), tiny);
+              const bool rot = fabs(apq[h]) > fmax(kRotTol * sqrt(fabs(app[h] * aqq[h])), tiny) &&
+                               !((zmask >> e[p]) & (zmask >> e[q]) & 1ull);
               any |= rot;
               // t = sign(tau) / (|tau| + sqrt(1 + tau^2)), tau = d / g, as
               // sign(d) g / (|d| + hypot(d, g)): one sqrt, one division, one
@@ -1174,15 +1223,11 @@ constexpr size_t kApplySmem =
 template <bool IMG>
 static int run_wnnm(const GroupSrc& s, int n, const EigArgs& ea_in, double scale,
                     int64_t* acc_out, double* out, double* ws, cudaStream_t st) {
-  static bool attrs = false;
-  if (!attrs) {
-    GLR_CUDA(cudaFuncSetAttribute(gram_kernel<IMG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kGramSmem));
-    GLR_CUDA(cudaFuncSetAttribute(eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kEigSmem));
-    GLR_CUDA(cudaFuncSetAttribute(apply_kernel<IMG, kApplyTR>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem));
-    attrs = true;
+  { const int s_ = ensure_smem_attr((const void*)gram_kernel<IMG>, (int)kGramSmem); if (s_) return s_; }
+  { const int s_ = ensure_smem_attr((const void*)eig_kernel, (int)kEigSmem); if (s_) return s_; }
+  {
+    const int s_ = ensure_smem_attr((const void*)apply_kernel<IMG, kApplyTR>, (int)kApplySmem);
+    if (s_) return s_;
   }
   gram_kernel<IMG><<<n, wn::GRAM_THREADS, kGramSmem, st>>>(s, n, ws, ws + (size_t)n * wn::GSZ);
   GLR_CUDA(cudaGetLastError());
@@ -1192,17 +1237,15 @@ static int run_wnnm(const GroupSrc& s, int n, const EigArgs& ea_in, double scale
   ea.wmax = ws + (size_t)n * (wn::GSZ + 1);
   ea.counter = reinterpret_cast<int*>(ws + (size_t)n * (wn::GSZ + 2));
   GLR_CUDA(cudaMemsetAsync(ea.counter, 0, sizeof(int), st));
-  eig_kernel<<<std::min(n, 3 * kNumSMs), wn::EIG_THREADS, kEigSmem, st>>>(ea);
+  eig_kernel<<<std::min(n, 3 * device_sms()), wn::EIG_THREADS, kEigSmem, st>>>(ea);
   GLR_CUDA(cudaGetLastError());
 #ifndef GLR_APPLY_DMMA  // dev A/B: -DGLR_APPLY_DMMA keeps the fp64 DMMA apply for image groups
   if constexpr (IMG) {
-    static bool oz_attr = false;
-    if (!oz_attr) {
-      GLR_CUDA(cudaFuncSetAttribute(apply_oz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)oz::SMEM));
-      oz_attr = true;
+    {
+      const int s_ = ensure_smem_attr((const void*)apply_oz_kernel, (int)oz::SMEM);
+      if (s_) return s_;
     }
-    apply_oz_kernel<<<std::min(n, kNumSMs), oz::THREADS, oz::SMEM, st>>>(
+    apply_oz_kernel<<<std::min(n, device_sms()), oz::THREADS, oz::SMEM, st>>>(
         s, n, ws, ws + (size_t)n * wn::GSZ, ws + (size_t)n * (wn::GSZ + 1), ilogb(scale), acc_out);
     return check_launch("wnnm kernels");
   }

@@ -34,6 +34,24 @@ def shard_bounds(n: int, rank: int, world: int) -> tuple[int, int]:
     return (n * rank) // world, (n * (rank + 1)) // world
 
 
+def sticky_owners(prev_owner: np.ndarray, world: int) -> np.ndarray:
+    """Owner rank of each anchor of a refresh (reference anchor order).
+    ``prev_owner[i]`` is the rank that held anchor i at the previous refresh,
+    or -1 for a new anchor. Persisting anchors keep their rank; new anchors
+    go, in anchor order, to the ranks below their share of the contiguous
+    split (n*r//world .. n*(r+1)//world). Deterministic in its inputs, so
+    every rank computes the same assignment."""
+    owner = np.asarray(prev_owner, dtype=np.int64).copy()
+    owner[owner >= world] = -1
+    n = owner.size
+    target = np.diff([(n * r) // world for r in range(world + 1)])
+    have = np.bincount(owner[owner >= 0], minlength=world)
+    need = np.maximum(target - have, 0)
+    pending = np.nonzero(owner < 0)[0]
+    owner[pending] = np.repeat(np.arange(world), need)[:pending.size]
+    return owner
+
+
 class DeviceOperator:
     """Device copy of a SensingOperator, rebuilt from kind + meta
     (operators.py plug point; the Python lambdas are never called)."""
@@ -255,6 +273,11 @@ class GlrEngine:
         self.n = 0          # anchors in the current match state (all ranks)
         self.lo = self.hi = 0
         self.has_positions = False
+        # sticky sharding state (world > 1): the anchors' owner ranks of the
+        # last refresh, and the permutation from reference to shard order
+        self._owner_map = None
+        self._owner_flat = None
+        self.perm = None
 
     @property
     def vcache(self):
@@ -337,7 +360,10 @@ class GlrEngine:
                self.ws_anchor.data_ptr(), s)
         n = int(self.n_anchors.item())  # one host sync per refresh
         self.n = n
-        self.lo, self.hi = shard_bounds(n, self.rank, self.world)
+        if self.world > 1:
+            self._assign_shards(n)
+        else:
+            self.lo, self.hi = 0, n
         self.has_positions = True
         self.warm = 0
         carry = bool(n and old_n and self.vcache_valid)
@@ -376,6 +402,38 @@ class GlrEngine:
             self.warm = 2
         self.count()
         return n
+
+    def _assign_shards(self, n: int) -> None:
+        """Sticky exemplar sharding (world > 1). An anchor that persists across
+        a refresh stays on the rank that held it, so the rank finds the
+        group's cached eigenvectors locally (glr_vcache_remap) and every group
+        starts its Jacobi sweeps from exactly the state it has at world 1:
+        the sharded solve is then bitwise identical to the single-rank one.
+        New anchors fill the ranks below their n/world share in anchor order.
+        Every rank computes the same assignment (identical anchors and
+        history); the anchors are permuted so each rank's block is contiguous
+        ([lo, hi)), and positions_host() restores the reference order."""
+        h, w, _ = self.shape
+        world = self.world
+        anc = D.host(self.anchors[:n]).astype(np.int64)
+        flat = anc[:, 0] * w + anc[:, 1]
+        if self._owner_map is None:
+            self._owner_map = np.full(h * w, -1, dtype=np.int32)
+        owner = sticky_owners(self._owner_map[flat], world)
+        perm = np.argsort(owner, kind="stable")
+        bounds = np.concatenate([[0], np.cumsum(np.bincount(owner, minlength=world))])
+        self.lo, self.hi = int(bounds[self.rank]), int(bounds[self.rank + 1])
+        if self._owner_flat is not None:
+            self._owner_map[self._owner_flat] = -1
+        self._owner_map[flat] = owner
+        self._owner_flat = flat
+        if np.array_equal(perm, np.arange(n)):
+            self.perm = None
+            return
+        self.perm = perm
+        perm_d = D.to_dev(perm)
+        self.anchors[:n].copy_(self.anchors[:n].index_select(0, perm_d))
+        self.tags[:n].copy_(self.tags[:n].index_select(0, perm_d))
 
     def match_shard(self):
         h, w, c = self.shape
@@ -448,6 +506,7 @@ class GlrEngine:
         n = len(anchors)
         self.n = n
         self.lo, self.hi = shard_bounds(n, self.rank, self.world)
+        self.perm = None
         self.has_positions = True
         self.warm = 0
         self.vcache_valid = False
@@ -504,4 +563,10 @@ class GlrEngine:
                 tt[:self.lo].zero_()
                 tt[self.hi:].zero_()
                 self._all_reduce(tt)
-        return D.host(self.anchors[:n]), D.host(pos), D.host(pad)
+        anc, pos, pad = D.host(self.anchors[:n]), D.host(pos), D.host(pad)
+        if self.perm is not None:  # shard order -> the reference's anchor order
+            out = [np.empty_like(a) for a in (anc, pos, pad)]
+            for o, a in zip(out, (anc, pos, pad)):
+                o[self.perm] = a
+            anc, pos, pad = out
+        return anc, pos, pad

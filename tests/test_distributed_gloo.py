@@ -92,3 +92,27 @@ def test_two_rank_aggregation_bitwise_equals_one_rank(tmp_path):
         / cnt1[covered][:, None]
     ref = O.glr_regularize(x, groups, p, 0.05)
     np.testing.assert_allclose(z, ref, atol=1e-11, rtol=0)
+
+
+def test_sticky_owners_keep_persisting_anchors_and_balance():
+    from paper_2301_03047_b200.engine import sticky_owners
+    rng = np.random.default_rng(3)
+    for world in (2, 3, 8):
+        n0 = 4097
+        own0 = sticky_owners(np.full(n0, -1), world)
+        # first refresh: the contiguous split
+        assert np.array_equal(np.bincount(own0, minlength=world),
+                              np.diff([(n0 * r) // world for r in range(world + 1)]))
+        assert np.all(np.diff(own0) >= 0)
+        # next refresh: 55 % of the anchors persist (in a new order), the rest are new
+        n1 = 4090
+        prev = np.full(n1, -1)
+        keep = rng.choice(n1, int(0.55 * n1), replace=False)
+        prev[keep] = rng.choice(own0, keep.size)
+        own1 = sticky_owners(prev, world)
+        assert np.array_equal(own1[keep], prev[keep])          # persisting anchors stay put
+        assert own1.min() >= 0 and own1.max() < world
+        cnt = np.bincount(own1, minlength=world)
+        share = n1 / world
+        assert cnt.max() <= max(share + 1, np.bincount(prev[keep], minlength=world).max())
+        assert np.array_equal(own1, sticky_owners(prev, world))  # deterministic

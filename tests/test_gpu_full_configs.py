@@ -93,7 +93,10 @@ def test_full_size_first_refreshes_and_10_iterations(name):
     assert int(gold["iters"]) == 10
     _, res, trace, x10 = _run(wl, capture_after=10)
     _check_traces(trace, gold, 2)
-    np.testing.assert_allclose(res[:10], gold["resid"], rtol=1e-6)
+    # C3's unclipped complex projection makes the data term exact: its
+    # residuals sit at rounding level, hence the ||y||-relative floor
+    ynorm = float(np.linalg.norm(np.abs(wl.y).ravel()))
+    np.testing.assert_allclose(res[:10], gold["resid"], rtol=1e-6, atol=1e-12 * ynorm)
     if name == "C3":
         assert len(trace[0][0]) == 2048  # the config's exemplar count
         gx = gold["x"].astype(np.float64)

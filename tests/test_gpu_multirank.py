@@ -64,13 +64,15 @@ def test_sharded_solve_bitwise_equals_single_rank(world, tmp_path):
     n0, n1 = len(trace[0][0]), len(trace[1][0])
     ranks = _run_ranks(world, tmp_path / "solve", "C1", iters)
     for r, d in enumerate(ranks):
-        assert np.array_equal(d["x"], x1), f"rank {r}: x differs from the single-rank solve"
-        assert np.array_equal(d["resid"], res1), f"rank {r}: residuals differ"
         assert int(d["nref"]) == 2
         for j, (a, p) in enumerate(trace):
             assert np.array_equal(d[f"anchors_{j}"], np.asarray(a)), (r, j)
             # positions_host assembles every rank's shard (integer all-reduce)
+            # and restores the reference anchor order (sticky shards permute it)
             assert np.array_equal(d[f"positions_{j}"], np.asarray(p)), (r, j)
+        bad = np.nonzero(d["resid"] != res1)[0]
+        assert bad.size == 0, f"rank {r}: residuals differ from iteration {bad[:1].tolist()}"
+        assert np.array_equal(d["x"], x1), f"rank {r}: x differs from the single-rank solve"
     # uneven shards that change across the refresh
     bounds = [[(n * q) // world for q in range(world + 1)] for n in (n0, n1)]
     sizes = [np.diff(b) for b in bounds]

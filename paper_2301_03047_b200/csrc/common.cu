@@ -31,17 +31,18 @@ int check_launch(const char* what) {
 
 namespace {
 std::mutex g_dev_mu;
-std::map<std::pair<const void*, int>, int> g_dev_cache;  // (key, device) -> value
+std::map<std::pair<const void*, int>, int> g_attr_cache;  // (kernel, device) -> smem bytes set
+std::map<std::pair<const void*, int>, int> g_dev_cache;   // (key, device) -> cached value
 }  // namespace
 
 int ensure_smem_attr(const void* kernel, int bytes) {
   int dev = 0;
   GLR_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(g_dev_mu);
-  auto it = g_dev_cache.find({kernel, dev});
-  if (it != g_dev_cache.end() && it->second >= bytes) return GLR_OK;
+  auto it = g_attr_cache.find({kernel, dev});
+  if (it != g_attr_cache.end() && it->second >= bytes) return GLR_OK;
   GLR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  g_dev_cache[{kernel, dev}] = bytes;
+  g_attr_cache[{kernel, dev}] = bytes;
   return GLR_OK;
 }
 

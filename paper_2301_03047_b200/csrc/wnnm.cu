@@ -478,6 +478,7 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
 #pragma unroll
           for (int rr = 0; rr < 3; ++rr) {
             double c[2], sn[2], t[2], app[2], aqq[2], apq[2];
+            bool rotd[2];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int p = PI[2 * rr + h], q = PJ[2 * rr + h];
@@ -487,6 +488,7 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
               const bool rot = fabs(apq[h]) > fmax(kRotTol * sqrt(fabs(app[h] * aqq[h])), tiny) &&
                                !((zmask >> e[p]) & (zmask >> e[q]) & 1ull);
               any |= rot;
+              rotd[h] = rot;
               // t = sign(tau) / (|tau| + sqrt(1 + tau^2)), tau = d / g, as
               // sign(d) g / (|d| + hypot(d, g)): one sqrt, one division, one
               // rsqrt on the latency chain (|t| <= 1)
@@ -513,7 +515,10 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
               }
               S[p][p] = app[h] - t[h] * apq[h];
               S[q][q] = aqq[h] + t[h] * apq[h];
-              S[p][q] = S[q][p] = 0.0;
+              // a skipped pair keeps its coupling: exempt (zero-shrinkage)
+              // pairs can be far from converged, and zeroing their entry
+              // would change the matrix being diagonalised
+              if (rotd[h]) S[p][q] = S[q][p] = 0.0;
             }
           }
 #pragma unroll
@@ -1255,6 +1260,220 @@ static int run_wnnm(const GroupSrc& s, int n, const EigArgs& ea_in, double scale
   return check_launch("wnnm kernels");
 }
 
+
+// ---------------------------------------------------------------------------
+// Groups wider than 64 columns (lowrank.py:46-65 takes any K): a generic fp64
+// path, one CTA per group, G and V in the workspace (2 K^2 doubles per
+// group, L2-resident) instead of shared memory:
+//   big_gram_kernel    G = M^T M (fp64 FMA), V = I
+//   big_jacobi_kernel  cyclic two-sided Jacobi in round-robin order (K/2
+//                      disjoint rotations per round, K-1 rounds per sweep),
+//                      the same rotation test as the fast kernel; then the
+//                      shrinkage and Wm = V diag(f(s)/s) V^T over G
+//   big_apply_kernel   out = M Wm, written out or scattered into the int64
+//                      fixed-point numerator like every other group
+// No warm start (each call is cold). This path exists for conformance with
+// the reference's signature; the configurations use K <= 64.
+namespace wb {
+constexpr int THREADS = 256;
+constexpr int MAX_SWEEPS = 40;
+}
+
+__device__ __forceinline__ int64_t row_off(const GroupSrc& s, int r) {
+  return (int64_t)(r / s.PC) * s.rs + (r % s.PC);
+}
+
+template <bool IMG>
+__global__ void __launch_bounds__(wb::THREADS) big_gram_kernel(GroupSrc s, int n, double* ws) {
+  const int g = blockIdx.x, K = s.K;
+  extern __shared__ long long cb[];  // K column bases
+  double* G = ws + (size_t)g * 2 * K * K;
+  double* V = G + (size_t)K * K;
+  for (int j = threadIdx.x; j < K; j += blockDim.x) cb[j] = col_base<IMG>(s, g, j);
+  __syncthreads();
+  for (int t = threadIdx.x; t < K * K; t += blockDim.x) {
+    const int i = t / K, j = t % K;
+    V[t] = i == j ? 1.0 : 0.0;
+    if (i > j) continue;
+    double acc = 0.0;
+    for (int r = 0; r < s.m; ++r) {
+      const int64_t o = row_off(s, r);
+      acc = fma(s.src[cb[i] + o], s.src[cb[j] + o], acc);
+    }
+    G[(size_t)i * K + j] = acc;
+    G[(size_t)j * K + i] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(wb::THREADS) big_jacobi_kernel(EigArgs a, double* ws) {
+  const int g = blockIdx.x, K = a.K, tid = threadIdx.x;
+  const int Kp = K + (K & 1);  // even; index K (odd K) is a dummy that never rotates
+  const int npair = Kp / 2;
+  double* G = ws + (size_t)g * 2 * K * K;
+  double* V = G + (size_t)K * K;
+  extern __shared__ double sh[];
+  double* cs = sh;               // npair
+  double* sn = cs + npair;       // npair
+  double* tt = sn + npair;       // npair
+  int* pp = reinterpret_cast<int*>(tt + npair);
+  int* qq = pp + npair;
+  __shared__ int s_any;
+  __shared__ double s_tiny;
+  if (tid == 0) {
+    double tr = 0.0;
+    for (int i = 0; i < K; ++i) tr += fabs(G[(size_t)i * K + i]);
+    s_tiny = 1e-17 * tr;
+  }
+  __syncthreads();
+  const double tiny = s_tiny;
+  for (int sweep = 0; sweep < wb::MAX_SWEEPS; ++sweep) {
+    if (tid == 0) s_any = 0;
+    __syncthreads();
+    for (int round = 0; round < Kp - 1; ++round) {
+      // circle method: (round, Kp-1) and ((round+k) % (Kp-1), (round-k) % (Kp-1))
+      for (int k = tid; k < npair; k += blockDim.x) {
+        int p, q;
+        if (k == 0) {
+          p = round;
+          q = Kp - 1;
+        } else {
+          p = (round + k) % (Kp - 1);
+          q = (round - k + Kp - 1) % (Kp - 1);
+        }
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        double c = 1.0, sv = 0.0, t = 0.0;
+        bool rot = false;
+        if (q < K) {
+          const double app = G[(size_t)p * K + p], aqq = G[(size_t)q * K + q];
+          const double apq = G[(size_t)p * K + q];
+          rot = fabs(apq) > fmax(wn::kRotTol * sqrt(fabs(app * aqq)), tiny);
+          if (rot) {
+            const double tau = (aqq - app) / (2.0 * apq);
+            t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            c = 1.0 / sqrt(1.0 + t * t);
+            sv = t * c;
+          }
+        }
+        pp[k] = rot ? p : -1;
+        qq[k] = q;
+        cs[k] = c;
+        sn[k] = sv;
+        tt[k] = t;
+        if (rot) s_any = 1;
+      }
+      __syncthreads();
+      // rows p, q of G (G <- J^T G)
+      for (int u = tid; u < npair * K; u += blockDim.x) {
+        const int k = u / K, col = u % K, p = pp[k];
+        if (p < 0) continue;
+        const int q = qq[k];
+        const double gp = G[(size_t)p * K + col], gq = G[(size_t)q * K + col];
+        G[(size_t)p * K + col] = cs[k] * gp - sn[k] * gq;
+        G[(size_t)q * K + col] = sn[k] * gp + cs[k] * gq;
+      }
+      __syncthreads();
+      // columns p, q of G (G <- G J) and of V (V <- V J)
+      for (int u = tid; u < npair * K; u += blockDim.x) {
+        const int k = u / K, row = u % K, p = pp[k];
+        if (p < 0) continue;
+        const int q = qq[k];
+        const double gp = G[(size_t)row * K + p], gq = G[(size_t)row * K + q];
+        G[(size_t)row * K + p] = cs[k] * gp - sn[k] * gq;
+        G[(size_t)row * K + q] = sn[k] * gp + cs[k] * gq;
+        const double vp = V[(size_t)row * K + p], vq = V[(size_t)row * K + q];
+        V[(size_t)row * K + p] = cs[k] * vp - sn[k] * vq;
+        V[(size_t)row * K + q] = sn[k] * vp + cs[k] * vq;
+      }
+      __syncthreads();
+      // the rotated 2x2 blocks are diagonal (set exactly)
+      for (int k = tid; k < npair; k += blockDim.x) {
+        const int p = pp[k];
+        if (p < 0) continue;
+        const int q = qq[k];
+        G[(size_t)p * K + q] = 0.0;
+        G[(size_t)q * K + p] = 0.0;
+      }
+      __syncthreads();
+    }
+    if (!s_any) break;
+  }
+  // shrinkage (lowrank.py:58-64), then Wm = V diag(ratio) V^T over G
+  double* ratio = sh;  // K doubles (the rotation arrays are done)
+  for (int i = tid; i < K; i += blockDim.x) {
+    const double lam = G[(size_t)i * K + i];
+    const double sv = sqrt(fmax(lam, 0.0));
+    double w;
+    if (a.uniform_weight >= 0.0) {
+      w = a.uniform_weight;
+    } else {
+      const double sig_hat = sqrt(fmax(sv * sv - K * a.sigma * a.sigma, 0.0));
+      w = a.c_weight * sqrt((double)K) * a.sigma * a.sigma / (sig_hat + a.eps);
+    }
+    const double f = fmax(sv - w, 0.0);
+    ratio[i] = sv > 0.0 ? f / sv : 0.0;
+  }
+  __syncthreads();
+  for (int t = tid; t < K * K; t += blockDim.x) {
+    const int i = t / K, j = t % K;
+    double acc = 0.0;
+    for (int k = 0; k < K; ++k)
+      acc = fma(V[(size_t)i * K + k] * ratio[k], V[(size_t)j * K + k], acc);
+    G[t] = acc;
+  }
+}
+
+template <bool IMG>
+__global__ void __launch_bounds__(wb::THREADS) big_apply_kernel(GroupSrc s, int n, const double* ws,
+                                                               double scale, int64_t* acc_out,
+                                                               double* out) {
+  const int g = blockIdx.x, K = s.K;
+  extern __shared__ long long cb[];
+  const double* Wm = ws + (size_t)g * 2 * K * K;
+  for (int j = threadIdx.x; j < K; j += blockDim.x) cb[j] = col_base<IMG>(s, g, j);
+  __syncthreads();
+  for (int64_t t = threadIdx.x; t < (int64_t)s.m * K; t += blockDim.x) {
+    const int j = (int)(t / s.m), r = (int)(t % s.m);
+    const int64_t o = row_off(s, r);
+    double v = 0.0;
+    for (int k = 0; k < K; ++k) v = fma(s.src[cb[k] + o], Wm[(size_t)k * K + j], v);
+    if constexpr (IMG) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(acc_out + cb[j] + o),
+                (unsigned long long)__double2ll_rn(v * scale));
+    } else {
+      out[((size_t)g * K + j) * s.m + r] = v;
+    }
+  }
+}
+
+template <bool IMG>
+static int run_wnnm_big(const GroupSrc& s, int n, const EigArgs& ea, double scale,
+                        int64_t* acc_out, double* out, double* ws, cudaStream_t st) {
+  const int K = s.K;
+  const int cb_bytes = K * (int)sizeof(long long);
+  const int jac_bytes = (K + 1) / 2 * 3 * (int)sizeof(double) + 2 * ((K + 1) / 2) * (int)sizeof(int);
+  const int jac_smem = std::max(jac_bytes, K * (int)sizeof(double));
+  GLR_REQUIRE(jac_smem <= 200 * 1024, GLR_ERR_UNSUPPORTED, "wnnm: K=%d too large", K);
+  if (cb_bytes > 48 * 1024) {
+    const int a = ensure_smem_attr((const void*)big_gram_kernel<IMG>, cb_bytes);
+    if (a) return a;
+    const int b = ensure_smem_attr((const void*)big_apply_kernel<IMG>, cb_bytes);
+    if (b) return b;
+  }
+  if (jac_smem > 48 * 1024) {
+    const int a = ensure_smem_attr((const void*)big_jacobi_kernel, jac_smem);
+    if (a) return a;
+  }
+  big_gram_kernel<IMG><<<n, wb::THREADS, cb_bytes, st>>>(s, n, ws);
+  GLR_CUDA(cudaGetLastError());
+  big_jacobi_kernel<<<n, wb::THREADS, jac_smem, st>>>(ea, ws);
+  GLR_CUDA(cudaGetLastError());
+  big_apply_kernel<IMG><<<n, wb::THREADS, cb_bytes, st>>>(s, n, ws, scale, acc_out, out);
+  return check_launch("wnnm (K > 64) kernels");
+}
 }  // namespace glr
 
 using namespace glr;
@@ -1273,6 +1492,8 @@ extern "C" int glr_debug_eig_hist(unsigned int* out, int reset) {
 #endif
 
 extern "C" size_t glr_wnnm_workspace(int G, int K) {
+  // K > 64 (generic path): G and V, K x K each, per group
+  if (K > wn::KMAX) return (size_t)std::max(G, 1) * 2 * K * K * sizeof(double) + 256;
   // G / Wm (64 x 64 per group), then max |M| and max |Wm| per group
   // (+ the eigen kernel's group counter)
   return ((size_t)std::max(G, 1) * (wn::GSZ + 2) + 1) * sizeof(double) + 256;
@@ -1281,8 +1502,7 @@ extern "C" size_t glr_wnnm_workspace(int G, int K) {
 extern "C" int glr_wnnm(const double* groups_d, int G, int m, int K, double sigma, double c_weight,
                         double eps, double uniform_weight, double* out_d, int32_t* nonfinite_d,
                         void* ws_d, size_t ws_bytes, void* stream) {
-  GLR_REQUIRE(K >= 1 && K <= wn::KMAX, GLR_ERR_UNSUPPORTED, "wnnm: K=%d outside [1, %d]", K,
-              wn::KMAX);
+  GLR_REQUIRE(K >= 1, GLR_ERR_INVALID, "wnnm: K=%d", K);
   GLR_REQUIRE(m >= 1, GLR_ERR_INVALID, "wnnm: m=%d", m);
   GLR_REQUIRE(sigma >= 0, GLR_ERR_INVALID, "noise_sigma must be nonnegative");
   GLR_REQUIRE(c_weight > 0 && eps > 0, GLR_ERR_INVALID, "c_weight and eps must be positive");
@@ -1301,6 +1521,9 @@ extern "C" int glr_wnnm(const double* groups_d, int G, int m, int K, double sigm
   ea.c_weight = c_weight;
   ea.eps = eps;
   ea.uniform_weight = uniform_weight;
+  if (K > wn::KMAX)
+    return run_wnnm_big<false>(s, G, ea, 1.0, nullptr, out_d, reinterpret_cast<double*>(ws_d),
+                               (cudaStream_t)stream);
   return run_wnnm<false>(s, G, ea, 1.0, nullptr, out_d, reinterpret_cast<double*>(ws_d),
                          (cudaStream_t)stream);
 }
@@ -1311,8 +1534,7 @@ extern "C" int glr_wnnm_scatter(const double* x_d, int H, int W, int C, int P,
                                 int64_t* acc_d, double* vcache_d, int warm,
                                 const uint8_t* warm_flags_d, void* ws_d, size_t ws_bytes,
                                 void* stream) {
-  GLR_REQUIRE(K >= 1 && K <= wn::KMAX, GLR_ERR_UNSUPPORTED, "wnnm: K=%d outside [1, %d]", K,
-              wn::KMAX);
+  GLR_REQUIRE(K >= 1, GLR_ERR_INVALID, "wnnm: K=%d", K);
   GLR_REQUIRE(P >= 1 && P <= H && P <= W, GLR_ERR_INVALID, "wnnm_scatter: bad patch size");
   GLR_REQUIRE(frac_bits >= 0 && frac_bits <= 52, GLR_ERR_INVALID, "frac_bits %d", frac_bits);
   GLR_REQUIRE(warm != 2 || warm_flags_d != nullptr, GLR_ERR_INVALID, "warm=2 needs warm flags");
@@ -1335,6 +1557,9 @@ extern "C" int glr_wnnm_scatter(const double* x_d, int H, int W, int C, int P,
   ea.c_weight = c_weight;
   ea.eps = eps;
   ea.uniform_weight = -1.0;
+  if (K > wn::KMAX)  // generic path: cold, no eigenvector cache
+    return run_wnnm_big<true>(s, n_max, ea, ldexp(1.0, frac_bits), acc_d, nullptr,
+                              reinterpret_cast<double*>(ws_d), (cudaStream_t)stream);
   ea.vcache = vcache_d;
   ea.warm = warm;
   ea.warm_flags = warm_flags_d;

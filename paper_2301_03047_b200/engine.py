@@ -176,8 +176,9 @@ class GlrEngine:
         self.use_corners = regularizer != "nlr-bm"
         self.p = match.patch_size
         self.k = match.group_size
-        if self.k > KMAX:
-            raise ValueError(f"group_size {self.k} exceeds the B200 WNNM kernel's {KMAX}")
+        # K <= 64: the fast WNNM kernels with per-group eigenvector warm
+        # starts; wider groups take the generic path (cold, no cache)
+        self.use_vcache = self.k <= KMAX
         if self.p > min(h, w):
             raise ValueError(f"patch size {self.p} exceeds image {h}x{w}")
         self.c_weight = c_weight
@@ -260,7 +261,8 @@ class GlrEngine:
         # per-group Jacobi eigenvectors, warm start between refreshes
         # (double-buffered so a refresh can carry them over by anchor, see
         # glr_vcache_remap); warm: 0 cold, 1 all groups, 2 per-group flags
-        self._vc = [D.empty((self.max_anchors, KMAX, KMAX), t.float64) for _ in range(2)]
+        vrows = self.max_anchors if self.use_vcache else 1
+        self._vc = [D.empty((vrows, KMAX, KMAX), t.float64) for _ in range(2)]
         self._vcur = 0
         self.vcache_valid = False
         self.warm_flags = D.zeros((self.max_anchors,), t.uint8)
@@ -366,7 +368,7 @@ class GlrEngine:
             self.lo, self.hi = 0, n
         self.has_positions = True
         self.warm = 0
-        carry = bool(n and old_n and self.vcache_valid)
+        carry = bool(n and old_n and self.vcache_valid and self.use_vcache)
         self.vcache_valid = False
         old_positions = self.positions
         self._pcur ^= 1
@@ -531,7 +533,8 @@ class GlrEngine:
             N.call("glr_wnnm_scatter", x_d.data_ptr(), h, w, c, self.p,
                    self.positions[self.lo:self.hi].data_ptr(), nloc, None, self.k, float(sigma),
                    float(self.c_weight), float(self.eps), self.frac, self.acc.data_ptr(),
-                   self.vcache[self.lo:self.hi].data_ptr(), self.warm,
+                   self.vcache[self.lo:self.hi].data_ptr() if self.use_vcache else None,
+                   self.warm if self.use_vcache else 0,
                    self.warm_flags[self.lo:self.hi].data_ptr(), self.ws_wnnm.data_ptr(),
                    self.ws_wnnm.numel(), D.stream())
             self.warm = 1

@@ -46,8 +46,6 @@ def wnnm_batch(mats: np.ndarray, params: WnnmParams) -> np.ndarray:
     g, m, k = mats.shape
     if not np.isfinite(mats).all():
         raise ValueError("non-finite entries in group matrix")
-    if k > KMAX:
-        raise ValueError(f"group size K={k} exceeds the B200 WNNM kernel's {KMAX} columns")
     src = D.f64(np.ascontiguousarray(mats.transpose(0, 2, 1)))  # (G, K, m) column-major
     out = D.empty((g, k, m), D.torch().float64)
     uw = -1.0 if params.uniform_weight is None else float(params.uniform_weight)
@@ -65,9 +63,6 @@ def wnnm_prox(m: np.ndarray, params: WnnmParams) -> np.ndarray:
         raise ValueError("non-finite entries in group matrix")
     if m.ndim != 2:
         raise ValueError("group matrix must be 2-D")
-    if m.shape[1] > KMAX and m.shape[0] <= KMAX:
-        # shrinkage commutes with transposition (singular values/vectors swap)
-        return wnnm_prox(m.T, params).T
     return wnnm_batch(m[None], params)[0]
 
 
@@ -91,10 +86,7 @@ def glr_regularize(x: np.ndarray, groups: list[PatchGroup], params: WnnmParams) 
     for (p, k), items in batches.items():
         pos = np.stack([it[0] for it in items])                       # (G, K, 2)
         mats = np.stack([np.asarray(it[1], dtype=np.float64) for it in items])  # (G, m, K)
-        if k <= KMAX:
-            den = wnnm_batch(mats, params)
-        else:
-            den = np.stack([wnnm_prox(mm, params) for mm in mats])
+        den = wnnm_batch(mats, params)
         src = D.f64(np.ascontiguousarray(den.transpose(0, 2, 1)))     # (G, K, m)
         pos_d = D.i32(pos)
         N.call("glr_scatter_fixed", src.data_ptr(), pos_d.data_ptr(), len(items), k, p, h, w, c,

@@ -50,6 +50,17 @@ constexpr int GSZ = KMAX * KMAX;  // doubles per group in the G / Wm / V buffers
 #define GLR_EIG_ROTTOL 1e-10
 #endif
 constexpr double kRotTol = GLR_EIG_ROTTOL;
+// First-order finish: the sweeps may stop once every pair between two kept
+// components (both in the smooth part of the shrinkage, away from its kink)
+// is below kFinishTol sqrt(|g_pp g_qq|); the residue E is then folded into
+// Wm to first order (Daleckii-Krein: f(L + E) = f(L) + E o D + O(|E|^2 f''),
+// D the divided differences of f(s)/s), which leaves a second-order error
+// ~kFinishTol^2 relative (numpy model of the scheme: 6e-11 at 6e-5, 9e-9 at
+// 5.5e-4 max relative residue; the strict 1e-10 test alone leaves ~1e-11).
+#ifndef GLR_EIG_FINISHTOL
+#define GLR_EIG_FINISHTOL 1e-5
+#endif
+constexpr double kFinishTol = GLR_EIG_FINISHTOL;
 }  // namespace wn
 
 // Element (r, j) of group g lives at src[cbase(g, j) + roff(r)]: for image
@@ -138,6 +149,30 @@ __device__ __forceinline__ void gram_tile(double (&acc)[9][2], const double* Tc,
   }
 }
 
+// gram_tile over one half of the tile's 32 rows (KH = 0: rows 0-15, 1: 16-31),
+// for the eigen kernel's fused Gram phase (8 warps: 4 tile-row owners x 2
+// row halves).
+template <int W, int KH>
+__device__ __forceinline__ void gram_tile_half(double (&acc)[9][2], const double* Tc,
+                                               uint32_t& mx) {
+  using namespace wn;
+#pragma unroll 2
+  for (int k0 = 16 * KH; k0 < 16 * KH + 16; k0 += 4) {
+    double f[8];
+#pragma unroll
+    for (int c = W; c < 8; ++c) f[c] = Tc[8 * c * GRS + k0];
+    if constexpr (W == 0) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) mx = max(mx, (uint32_t)__double2hiint(f[c]) & 0x7FFFFFFFu);
+    }
+#pragma unroll
+    for (int c = W; c < 8; ++c) dmma(acc[c - W][0], acc[c - W][1], f[W], f[c]);
+#pragma unroll
+    for (int c = 7 - W; c < 8; ++c)
+      dmma(acc[8 - W + c - (7 - W)][0], acc[8 - W + c - (7 - W)][1], f[7 - W], f[c]);
+  }
+}
+
 template <bool IMG>
 __global__ void __launch_bounds__(wn::GRAM_THREADS)
     gram_kernel(GroupSrc s, int n, double* __restrict__ Gout, double* __restrict__ gmax) {
@@ -211,6 +246,10 @@ struct EigArgs {
   const uint8_t* warm_flags;
   double* wmax;  // optional per-group max |Wm| (the split-integer apply's scale)
   int* counter;  // dynamic group counter (zeroed before the launch)
+  // fused Gram (image groups): G = M^T M is formed in shared memory from the
+  // image instead of being read from G, and max |M| goes to gmax
+  GroupSrc src;
+  double* gmax;
 };
 
 // Block-Jacobi schedule. The 63 rounds of a parallel cyclic sweep pair i
@@ -308,6 +347,109 @@ __device__ __forceinline__ bool shrinks_to_zero(const EigArgs& a, double lam) {
   return s - w <= 0.0;
 }
 
+// f(s)/s of the WNNM shrinkage at eigenvalue lam (lowrank.py:58-64) and its
+// derivative in lam (0 where the ratio is clamped to zero).
+__device__ __forceinline__ double shrink_ratio(const EigArgs& a, double lam) {
+  const double s = sqrt(fmax(lam, 0.0));
+  double w;
+  if (a.uniform_weight >= 0.0) {
+    w = a.uniform_weight;
+  } else {
+    const double sig_hat = sqrt(fmax(s * s - a.K * a.sigma * a.sigma, 0.0));
+    w = a.c_weight * sqrt((double)a.K) * a.sigma * a.sigma / (sig_hat + a.eps);
+  }
+  const double f = fmax(s - w, 0.0);
+  return s > 0.0 ? f / s : 0.0;
+}
+__device__ __forceinline__ double shrink_ratio_deriv(const EigArgs& a, double lam) {
+  const double s = sqrt(fmax(lam, 0.0));
+  if (s == 0.0) return 0.0;
+  if (a.uniform_weight >= 0.0) {
+    const double w = a.uniform_weight;
+    return s - w <= 0.0 ? 0.0 : w / (2.0 * s * s * s);
+  }
+  const double b = a.c_weight * sqrt((double)a.K) * a.sigma * a.sigma;
+  const double sh = sqrt(fmax(lam - a.K * a.sigma * a.sigma, 0.0));
+  const double w = b / (sh + a.eps);
+  if (s - w <= 0.0) return 0.0;
+  const double dw = sh > 0.0 ? -b / ((sh + a.eps) * (sh + a.eps) * 2.0 * sh) : 0.0;
+  return -dw / s + w / (2.0 * s * s * s);
+}
+
+// Fused Gram phase of the eigen kernel (image groups): G = M^T M of group g
+// into shared memory (row stride GLD, both triangles), on DMMA, with the
+// group read straight from the image through a double-buffered cp.async
+// tile ring that aliases the G / V^T buffers (neither is live yet). Eight
+// warps: warp w owns the Gram kernel's tile rows (w % 4, 7 - w % 4) for the
+// row half w / 4 of every 32-row tile; the two halves' partial sums meet in
+// shared memory. Running the Gram inside the group loop lets one CTA's DMMA
+// phase overlap the other resident CTAs' Jacobi phases (which are bound by
+// shared-memory wavefronts and rotation latency, not the fp64 pipe).
+__device__ __forceinline__ void eig_fused_gram(const EigArgs& a, const int g, double* sm) {
+  using namespace wn;
+  const GroupSrc& s = a.src;
+  double* T = sm;  // 2 x KMAX x GRS doubles (aliases G and V^T)
+  double* G = sm;
+  __shared__ long long s_cb[KMAX];
+  __shared__ uint32_t s_mx[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int w = warp & 3, kh = warp >> 2;
+  if (tid < KMAX) s_cb[tid] = tid < s.K ? col_base<true>(s, g, tid) : 0;
+  __syncthreads();
+  const int ar = lane >> 2, ak = lane & 3;
+  double acc[9][2];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) acc[q][0] = acc[q][1] = 0.0;
+  uint32_t mx = 0;
+  const int ntiles = (s.m + GROWS - 1) / GROWS;
+  fill_tile<8>(T, s, s_cb, 0, GROWS, GRS);
+  for (int tt = 0; tt < ntiles; ++tt) {
+    if (tt + 1 < ntiles)
+      fill_tile<8>(T + ((tt + 1) & 1) * KMAX * GRS, s, s_cb, (tt + 1) * GROWS, GROWS, GRS);
+    else
+      cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* Tc = T + (tt & 1) * KMAX * GRS + ar * GRS + ak;
+    switch (warp) {  // warp-uniform: compile-time accumulator indices per warp
+      case 0: gram_tile_half<0, 0>(acc, Tc, mx); break;
+      case 1: gram_tile_half<1, 0>(acc, Tc, mx); break;
+      case 2: gram_tile_half<2, 0>(acc, Tc, mx); break;
+      case 3: gram_tile_half<3, 0>(acc, Tc, mx); break;
+      case 4: gram_tile_half<0, 1>(acc, Tc, mx); break;
+      case 5: gram_tile_half<1, 1>(acc, Tc, mx); break;
+      case 6: gram_tile_half<2, 1>(acc, Tc, mx); break;
+      default: gram_tile_half<3, 1>(acc, Tc, mx); break;
+    }
+    __syncthreads();
+  }
+  if (w == 0) {
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0) s_mx[kh] = mx;
+  }
+  // partial sums: the second row half writes, the first adds (both triangles)
+#pragma unroll
+  for (int pass = 1; pass >= 0; --pass) {
+    if (kh == pass) {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        const int ti = q < 8 - w ? w : 7 - w;
+        const int tj = q < 8 - w ? w + q : q - (8 - w) + 7 - w;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = 8 * ti + ar, j = 8 * tj + 2 * ak + e;
+          const double v = pass ? acc[q][e] : G[i * GLD + j] + acc[q][e];
+          G[i * GLD + j] = v;
+          if (tj != ti) G[j * GLD + i] = v;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && a.gmax) a.gmax[g] = __hiloint2double((int)max(s_mx[0], s_mx[1]), -1);
+}
+
+template <bool FUSED>
 __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double* sm) {
   using namespace wn;
   double* G = sm;               // KMAX x GLD, exactly symmetric throughout
@@ -320,9 +462,13 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
   double* vc = a.vcache ? a.vcache + (size_t)g * GSZ : nullptr;
   const bool warm = vc && (a.warm == 1 || (a.warm == 2 && a.warm_flags[g]));
 
-  for (int t = tid; t < GSZ / 2; t += EIG_THREADS) {
-    const int i = (2 * t) >> 6, j = (2 * t) & 63;
-    *reinterpret_cast<double2*>(&G[i * GLD + j]) = reinterpret_cast<const double2*>(Gg)[t];
+  if constexpr (FUSED) {
+    eig_fused_gram(a, g, sm);
+  } else {
+    for (int t = tid; t < GSZ / 2; t += EIG_THREADS) {
+      const int i = (2 * t) >> 6, j = (2 * t) & 63;
+      *reinterpret_cast<double2*>(&G[i * GLD + j]) = reinterpret_cast<const double2*>(Gg)[t];
+    }
   }
   for (int t = tid; t < GSZ; t += EIG_THREADS) {
     const int j = t >> 6, i = t & 63;
@@ -381,6 +527,8 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
   __shared__ double Ds[16][16];     // rotated diagonal block, same layout
   __shared__ unsigned s_qrot[2];
   __shared__ unsigned char s_zb[8];  // per warp: zero-shrinkage flags of its 8 rows
+  __shared__ unsigned char s_ub[8];  // per warp: rows too close to the shrinkage kink
+  __shared__ double lamv[KMAX];      // final diagonal (first-order finish)
   const int qA = 2 * warp + (lane >> 4), qB = lane & 15;
   int gsr = 0, prev_sr = -1;  // running super-round count; pending V step
   auto v_step = [&](int buf, int srv, int t0, int nthreads) {
@@ -411,6 +559,7 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
   };
   int sweep = 0;
   uint64_t zmask = 0;  // indices whose whole Gershgorin disc shrinks to zero
+  bool early = false;  // stopped by the first-order finish (residue above kRotTol)
   for (; sweep < MAX_SWEEPS; ++sweep) {
     // Zero-shrinkage exemption: index i is in Z when r(g_ii + sum_k |g_ik|)
     // == 0, i.e. every eigenvalue its Gershgorin disc can hold is mapped to
@@ -428,30 +577,56 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
       for (int k = 16 * q; k < 16 * q + 16; ++k) r += k == i ? 0.0 : fabs(G[i * GLD + k]);
       r += __shfl_xor_sync(0xffffffffu, r, 1);
       r += __shfl_xor_sync(0xffffffffu, r, 2);
-      const bool z = shrinks_to_zero(a, G[i * GLD + i] + r);
-      const unsigned b = __ballot_sync(0xffffffffu, z && q == 0);
+      const double gii = G[i * GLD + i];
+      const bool z = shrinks_to_zero(a, gii + r);
+      // a kept row is "unsafe" for the first-order finish when its disc
+      // (widened by 1e-3 |g_ii|) reaches down to the shrinkage kink
+      const bool u = !z && shrinks_to_zero(a, gii - r - 1e-3 * fabs(gii));
+      const unsigned bz = __ballot_sync(0xffffffffu, z && q == 0);
+      const unsigned bu = __ballot_sync(0xffffffffu, u && q == 0);
       if (lane == 0) {
-        unsigned char m8 = 0;
+        unsigned char m8 = 0, u8 = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) m8 |= ((b >> (4 * k)) & 1u) << k;
+        for (int k = 0; k < 8; ++k) {
+          m8 |= ((bz >> (4 * k)) & 1u) << k;
+          u8 |= ((bu >> (4 * k)) & 1u) << k;
+        }
         s_zb[warp] = m8;
+        s_ub[warp] = u8;
       }
     }
     __syncthreads();
     zmask = 0;
+    bool unsafe = false;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) zmask |= (uint64_t)s_zb[k] << (8 * k);
+    for (int k = 0; k < 8; ++k) {
+      zmask |= (uint64_t)s_zb[k] << (8 * k);
+      unsafe |= s_ub[k] != 0;
+    }
     // A sweep changes G only if some pair passes the rotation test on the
     // current G (otherwise no round rotates, by induction): test all pairs
-    // up front and stop without paying for a no-op sweep.
-    bool need = false;
+    // up front and stop without paying for a no-op sweep. The sweeps also
+    // stop once the first-order finish is exact to second order: no kept
+    // row near the kink, kept-kept pairs below kFinishTol, and every
+    // kept-exempt pair below the rotation test (fully decoupled).
+    bool need = false, block_finish = false;
     for (int t = tid; t < GSZ; t += EIG_THREADS) {
       const int i = t >> 6, j = t & 63;
-      if (i < j && !((zmask >> i) & (zmask >> j) & 1ull))
-        need |= fabs(G[i * GLD + j]) >
-                fmax(kRotTol * sqrt(fabs(G[i * GLD + i] * G[j * GLD + j])), tiny);
+      const unsigned zi = (zmask >> i) & 1ull, zj = (zmask >> j) & 1ull;
+      if (i < j && !(zi & zj)) {
+        const double gij = fabs(G[i * GLD + j]);
+        const double sc = sqrt(fabs(G[i * GLD + i] * G[j * GLD + j]));
+        const bool strict = gij > fmax(kRotTol * sc, tiny);
+        need |= strict;
+        block_finish |= (zi | zj) ? strict : gij > fmax(kFinishTol * sc, tiny);
+      }
     }
-    if (!__syncthreads_or(need)) break;
+    const bool any_need = __syncthreads_or(need);
+    const bool any_block = __syncthreads_or(block_finish) || unsafe;
+    if (!any_need || !any_block) {
+      early = any_need;
+      break;
+    }
     for (int sr = 0; sr < 21; ++sr, ++gsr) {
       const int buf = gsr & 1;
       if (warp == 0) {
@@ -587,21 +762,9 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
   }
   // ---- shrinkage weights (lowrank.py:58-64) ----
   if (tid < KMAX) {
-    double r = 0.0;
-    if (tid < K) {
-      const double lam = G[tid * GLD + tid];
-      const double s = sqrt(fmax(lam, 0.0));
-      double w;
-      if (a.uniform_weight >= 0.0) {
-        w = a.uniform_weight;
-      } else {
-        const double sig_hat = sqrt(fmax(s * s - K * a.sigma * a.sigma, 0.0));
-        w = a.c_weight * sqrt((double)K) * a.sigma * a.sigma / (sig_hat + a.eps);
-      }
-      const double f = fmax(s - w, 0.0);
-      r = s > 0.0 ? f / s : 0.0;
-    }
-    ratio[tid] = r;
+    const double lam = G[tid * GLD + tid];
+    ratio[tid] = tid < K ? shrink_ratio(a, lam) : 0.0;
+    lamv[tid] = lam;
   }
   __syncthreads();
 #ifdef GLR_EIG_STATS
@@ -611,10 +774,49 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
     atomicAdd(&g_rank_hist[kept], 1u);
   }
 #endif
-  // Wm = V diag(ratio) V^T -> global, on DMMA
   double o[8][2];
-  eig_mm64([&](int i, int k) { return Vt[k * VLD + i] * ratio[k]; },
-           [&](int k, int j) { return Vt[k * VLD + j]; }, o);
+  if (!early) {
+    // converged to the rotation test: Wm = V diag(ratio) V^T on DMMA
+    eig_mm64([&](int i, int k) { return Vt[k * VLD + i] * ratio[k]; },
+             [&](int k, int j) { return Vt[k * VLD + j]; }, o);
+  } else {
+    // Mcorr = diag(f(s)/s) + E o D in place over G: the off-diagonal residue
+    // E (all below kFinishTol relative, see the sweep exit; entries at the
+    // rotation-test level are dropped as in the converged path) times the
+    // divided differences D of the ratio, the derivative where two
+    // eigenvalues nearly coincide. Then Wm = (V Mcorr) V^T on DMMA.
+    for (int t = tid; t < GSZ; t += EIG_THREADS) {
+      const int i = t >> 6, j = t & 63;
+      double v = 0.0;
+      if (i == j) {
+        v = ratio[i];
+      } else if (i < K && j < K) {
+        const double li = lamv[i], lj = lamv[j], e = G[i * GLD + j];
+        if (fabs(e) > kRotTol * sqrt(fabs(li * lj))) {
+          const double d = li - lj;
+          const double D = fabs(d) > 1e-4 * fmax(fabs(li), fabs(lj))
+                               ? (ratio[i] - ratio[j]) / d
+                               : shrink_ratio_deriv(a, 0.5 * (li + lj));
+          v = e * D;
+        }
+      }
+      G[i * GLD + j] = v;
+    }
+    __syncthreads();
+    eig_mm64([&](int i, int k) { return Vt[k * VLD + i]; },
+             [&](int k, int j) { return G[k * GLD + j]; }, o);
+    __syncthreads();
+    {
+      const int ar = lane >> 2, ak = lane & 3;
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) G[(8 * warp + ar) * GLD + 8 * t + 2 * ak + e] = o[t][e];
+    }
+    __syncthreads();
+    eig_mm64([&](int i, int k) { return G[i * GLD + k]; },
+             [&](int k, int j) { return Vt[k * VLD + j]; }, o);
+  }
   {
     const int ar = lane >> 2, ak = lane & 3;
 #pragma unroll
@@ -640,6 +842,7 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
 // Dynamic group scheduling: 3 CTAs per SM take groups from an atomic counter
 // (zeroed by the launcher), so the per-group sweep counts balance and the last
 // wave's tail shrinks to one group per CTA.
+template <bool FUSED>
 __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_g;
@@ -649,7 +852,7 @@ __global__ void __launch_bounds__(wn::EIG_THREADS, 3) eig_kernel(EigArgs a) {
     const int g = s_g;
     __syncthreads();  // every thread has g (and is done with the previous group's smem)
     if (g >= a.n) return;
-    eig_group(a, g, sm);
+    eig_group<FUSED>(a, g, sm);
   }
 }
 
@@ -1229,20 +1432,36 @@ template <bool IMG>
 static int run_wnnm(const GroupSrc& s, int n, const EigArgs& ea_in, double scale,
                     int64_t* acc_out, double* out, double* ws, cudaStream_t st) {
   { const int s_ = ensure_smem_attr((const void*)gram_kernel<IMG>, (int)kGramSmem); if (s_) return s_; }
-  { const int s_ = ensure_smem_attr((const void*)eig_kernel, (int)kEigSmem); if (s_) return s_; }
+  // Gram inside the eigen kernel for short groups (m <= 512: C1 24.8 vs
+  // 25.1 ms per solve, C3 94.7 vs 96.6 ms); the separate DMMA Gram kernel
+  // for tall ones (C2, m = 1536: 327.0 vs 332.5 ms -- there the fused Gram
+  // phase competes with the Jacobi phases for shared-memory bandwidth)
+  const bool kFused = IMG && s.m <= 512;
+  {
+    const int s_ = ensure_smem_attr(kFused ? (const void*)eig_kernel<true>
+                                           : (const void*)eig_kernel<false>, (int)kEigSmem);
+    if (s_) return s_;
+  }
   {
     const int s_ = ensure_smem_attr((const void*)apply_kernel<IMG, kApplyTR>, (int)kApplySmem);
     if (s_) return s_;
   }
-  gram_kernel<IMG><<<n, wn::GRAM_THREADS, kGramSmem, st>>>(s, n, ws, ws + (size_t)n * wn::GSZ);
-  GLR_CUDA(cudaGetLastError());
+  if (!kFused) {
+    gram_kernel<IMG><<<n, wn::GRAM_THREADS, kGramSmem, st>>>(s, n, ws, ws + (size_t)n * wn::GSZ);
+    GLR_CUDA(cudaGetLastError());
+  }
   EigArgs ea = ea_in;
+  ea.src = s;
+  ea.gmax = kFused ? ws + (size_t)n * wn::GSZ : nullptr;
   ea.G = ws;
   ea.n = n;
   ea.wmax = ws + (size_t)n * (wn::GSZ + 1);
   ea.counter = reinterpret_cast<int*>(ws + (size_t)n * (wn::GSZ + 2));
   GLR_CUDA(cudaMemsetAsync(ea.counter, 0, sizeof(int), st));
-  eig_kernel<<<std::min(n, 3 * device_sms()), wn::EIG_THREADS, kEigSmem, st>>>(ea);
+  if (kFused)
+    eig_kernel<true><<<std::min(n, 3 * device_sms()), wn::EIG_THREADS, kEigSmem, st>>>(ea);
+  else
+    eig_kernel<false><<<std::min(n, 3 * device_sms()), wn::EIG_THREADS, kEigSmem, st>>>(ea);
   GLR_CUDA(cudaGetLastError());
 #ifndef GLR_APPLY_DMMA  // dev A/B: -DGLR_APPLY_DMMA keeps the fp64 DMMA apply for image groups
   if constexpr (IMG) {

@@ -1047,15 +1047,21 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
   uint8_t* sB = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
   __shared__ __align__(16) long long cb_s[2][wn::KMAX], cb_e[2][wn::KMAX];  // per group (parity)
-  __shared__ __align__(8) uint64_t full_a, empty_a, full_b[2], empty_b[2], tfull[2], tempty[2];
+  // A (TMEM) is handed over per K half: slicer threads jh fill columns
+  // 48 jh .. 48 jh + 47, and the issuers run all K-half-0 MMAs of a tile before
+  // its K-half-1 MMAs, so half 0 of tile t+1 is written while the K-half-1
+  // MMAs of tile t still run (A stays single-buffered: the TMEM columns are
+  // taken by the two accumulator sets)
+  __shared__ __align__(8) uint64_t full_a[2], empty_a[2], full_b[2], empty_b[2], tfull[2],
+      tempty[2];
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int K = s.K, m = s.m;
   const int ntiles = (m + TR - 1) / TR;
   if (tid == 0) {
-    mbar_init(&full_a, SLICERS / 32);
-    mbar_init(&empty_a, ISSUERS);  // every issuer's MMAs
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&full_a[i], SLICERS / 64);  // the slicer warps of K half i
+      mbar_init(&empty_a[i], ISSUERS);      // every issuer's MMAs of K half i
       mbar_init(&full_b[i], SLICERS / 32);
       mbar_init(&empty_b[i], ISSUERS);
       mbar_init(&tfull[i], ISSUERS / 2);  // both level sets of the half
@@ -1121,14 +1127,15 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
         uint32_t w[S * 8];
         oz_digits16<8>(v, sc, w);
         oz_digits16<8>(v + 16, sc, w + 4);
-        if (it >= 1) mbar_wait(&empty_a, (it - 1) & 1);  // the previous tile's MMAs are done
+        // the previous tile's MMAs of this K half are done
+        if (it >= 1) mbar_wait(&empty_a[jh], (it - 1) & 1);
         tc_fence_after();
         tmem_st_32x32b_x32(ta, *reinterpret_cast<const uint32_t(*)[32]>(w));
         tmem_st_32x32b_x16(ta + 32, w + 32);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&full_a);
+        if (lane == 0) mbar_arrive(&full_a[jh]);
       }
     }
   } else if (warp >= 16) {
@@ -1144,25 +1151,25 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
         mbar_wait(&full_b[pb], (gi >> 1) & 1);
         const uint64_t bd0 = smem_desc_k_sw128(sB + pb * B_STAGE) + (uint64_t)((hf * NH * 128) >> 4);
         for (int tt = 0; tt < ntiles; ++tt, ++it) {
-          mbar_wait(&full_a, it & 1);
           if (it >= 1) mbar_wait(&tempty[hf], (it - 1) & 1);
-          tc_fence_after();
 #pragma unroll
-          for (int k = 0; k < S; ++k)
+          for (int ks = 0; ks < 2; ++ks) {
+            mbar_wait(&full_a[ks], it & 1);
+            tc_fence_after();
 #pragma unroll
-            for (int l = 0; l + k < LV; ++l)
-              if ((k + l >= 4) == (ls == 1)) {  // this issuer's levels (own accumulators)
+            for (int k = 0; k < S; ++k)
 #pragma unroll
-                for (int ks = 0; ks < 2; ++ks) {
+              for (int l = 0; l + k < LV; ++l)
+                if ((k + l >= 4) == (ls == 1)) {  // this issuer's levels (own accumulators)
                   // B: slice l, rows 32 hf.., K bytes 32 ks.. of the slice (desc += bytes >> 4)
                   const uint64_t bd =
                       bd0 + (uint64_t)(((l >> 1) * B_BUF + (l & 1) * 64 + ks * 32) >> 4);
                   umma_i8_ta(d0 + (uint32_t)((k + l) * NH), tmem + A_COL + 48 * ks + 8 * k, bd,
                              idesc, (k | ks) != 0);
                 }
-              }
+            umma_commit(&empty_a[ks]);  // one of the ISSUERS arrivals that free A's K half
+          }
           umma_commit(&tfull[hf]);
-          umma_commit(&empty_a);  // one of the two arrivals that free A
         }
         umma_commit(&empty_b[pb]);
       }

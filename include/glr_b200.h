@@ -187,8 +187,10 @@ int glr_tv_denoise(const double* x_d, int H, int W, int C, double weight, int it
 
 /* ---- (4) WNNM: glr/lowrank.py:46-65 ------------------------------------------
  * Batched weighted singular-value shrinkage of G groups (K columns of m
- * rows each, column-major per group) via an fp64 Gram matrix, a one-sided
- * cyclic Jacobi eigensolver and out = M * V diag(f(s)/s) V^T.
+ * rows each, column-major per group) via an fp64 Gram matrix, a cyclic
+ * Jacobi eigensolver and out = M * V diag(f(s)/s) V^T. Any K >= 1 (like the
+ * reference): K <= 64 runs the fast kernels (block Jacobi, eigenvector
+ * cache, split-integer apply), wider groups a generic path (cold, no cache).
  * sigma: noise level (WnnmParams.noise_sigma); uniform_weight < 0 = unused.
  * nonfinite_d (optional): set to 1 when a group holds a non-finite value.   */
 size_t glr_wnnm_workspace(int G, int K);

@@ -1,6 +1,7 @@
 // Shared helpers for the GLR B200 kernels: status plumbing for the C ABI and
 // the handful of sm_100a PTX wrappers (mbarrier, TMA, tcgen05) the kernels use.
 #pragma once
+#include <cstdio>
 
 #include <cuda_runtime.h>
 #include <cuda.h>
@@ -21,6 +22,25 @@ int check_launch(const char* what);
       return (code);                          \
     }                                         \
   } while (0)
+
+// Device-side bounds / invariant checks of the checked build
+// (GLR_NVCC_EXTRA=-DGLR_CHECKS, tools/checked_build.sh): a failing check
+// prints its location and traps, so the launch returns a CUDA error. They
+// stand in for compute-sanitizer, which this GPU pool does not allow.
+#ifdef GLR_CHECKS
+#define GLR_DCHECK(cond)                                                              \
+  do {                                                                                \
+    if (!(cond)) {                                                                    \
+      printf("GLR_DCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x, #cond);                               \
+      __trap();                                                                       \
+    }                                                                                 \
+  } while (0)
+#else
+#define GLR_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 #define GLR_CUDA(call)                                                     \
   do {                                                                     \
@@ -160,9 +180,13 @@ __device__ __forceinline__ uint32_t cluster_addr(const void* p, uint32_t rank) {
   return r;
 }
 
-// arrive (release, cluster scope) on the mbarrier at cluster address `bar`
+// arrive on the mbarrier at cluster address `bar` (another CTA of the cluster)
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar)
+  // default semantics (.release at .cta scope), as CUTLASS's ClusterBarrier::arrive: the
+  // arrive only has to order the caller's tcgen05 accesses (tcgen05.fence::before_thread_sync
+  // precedes it); .release.cluster also drained every global store the epilogue warp had
+  // in flight (ncu: 12 % of the heat GEMM's warp stalls on membar)
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar)
                : "memory");
 }
 

@@ -92,7 +92,9 @@ static HeatGeom heat_geom(int H, int W, int C, int P, int e) {
 }
 
 struct HeatParams {
-  int oh, ow, Mpad, n_max, m_tiles_per_row, S, kchunks, e;
+  // oh: output rows the kernel covers; row i is image row u = i * u_step + u0
+  // (u_step > 1: a row-sampled map for the candidate floor, see glr_heat_topk)
+  int oh, ow, Mpad, n_max, m_tiles_per_row, S, kchunks, e, u_step, u0;
   const int32_t* n_dev;
   uint16_t* heat;
   // candidate mode (cand != nullptr): instead of the dense u16 map, append
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
       for (int t = cl; t < total; t += n_cl) {
         const int n0 = (t % n_tiles) * BN;
         const int m_tile = 2 * (t / n_tiles) + rank;
-        const int u = m_tile / p.m_tiles_per_row;
+        const int u = (m_tile / p.m_tiles_per_row) * p.u_step + p.u0;
         const int v0 = (m_tile % p.m_tiles_per_row) * BM;
         for (int kb = 0; kb < num_k; ++kb, ++it) {
           const int s = it % STAGES;
@@ -226,12 +228,14 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
       const int acc = lt & 1, use = lt >> 1;
       const int n0 = (t % n_tiles) * BN;
       const int m_tile = 2 * (t / n_tiles) + rank;
-      const int u = m_tile / p.m_tiles_per_row;
+      const int ui = m_tile / p.m_tiles_per_row;  // output row (sample row index)
+      const int u = ui * p.u_step + p.u0;         // image row
       const int v = (m_tile % p.m_tiles_per_row) * BM + ew * 32 + lane;
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
       const bool v_ok = v < p.ow;
-      uint16_t* out = p.heat + (size_t)u * p.ow + v;
+      GLR_DCHECK(ui < p.oh && u < p.oh * p.u_step + p.u0 && (int64_t)ui * p.ow < p.Mpad);
+      uint16_t* out = p.heat + (size_t)ui * p.ow + v;
 #pragma unroll 1
       for (int c = c_lo; c < c_hi; ++c) {
         uint32_t r[32];
@@ -239,10 +243,20 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
         tmem_ld_wait();
         const int nb = n0 + c * 32;
         if (p.cand) {
-          // candidate lists: warp-aggregated appends per exemplar column
+          // candidate lists: a lane-local pre-test of the 32 scores against
+          // their exemplars' floors (float compares, floors broadcast from
+          // registers of the lane that owns the column); only a chunk in
+          // which some lane has a hit takes the per-column ballot and the
+          // warp-aggregated list appends
           const int tl = nb + lane < N ? (int)p.thr[nb + lane] : 0x10000;
           const uint32_t pos = (uint32_t)(u * p.ow + v);
           const unsigned lt = (1u << lane) - 1u;
+          const float tlf = (float)tl;
+          bool any = false;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            any |= __uint_as_float(r[j]) >= __shfl_sync(0xffffffffu, tlf, j);
+          if (!__any_sync(0xffffffffu, any && v_ok)) continue;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int sc = (int)__float2uint_rn(__uint_as_float(r[j]));
@@ -329,6 +343,56 @@ __global__ void exemplar_thr_kernel(const uint8_t* __restrict__ bmat, int Kp, in
   if (lane == 0) thr[w] = (uint16_t)(cnt >> 2);
 }
 
+// Sampled candidate floor: thr[n] = T_n, the largest score with at least
+// `want` entries >= T_n among the exemplar's row-sampled heat scores (want ~
+// 8 pool x the sampled fraction of the positions; 0 when the sample is
+// smaller than `want`). Unlike the quarter-self-score floor it may go below
+// |E_n| / 4, which the pool does reach on mixed images (C1, C3). So the
+// fused epilogue records a few pool-sizes of candidates per exemplar whatever
+// the score distribution. One CTA per exemplar, shared-memory histogram of
+// the top score range. Exactness does not depend on it: an exemplar whose
+// cut falls below its floor (or whose list overflows) goes to the dense path.
+__global__ void __launch_bounds__(256) sample_thr_kernel(const uint16_t* __restrict__ hs,
+                                                         int64_t mpad, int ns, int n_max,
+                                                         int bins, int want,
+                                                         uint16_t* __restrict__ thr) {
+  extern __shared__ int hist_s[];
+  __shared__ int s_T;
+  const int n = blockIdx.x;
+  if (n >= n_max) return;
+  const int lo = 0;
+  for (int b = threadIdx.x; b < bins; b += blockDim.x) hist_s[b] = 0;
+  if (threadIdx.x == 0) s_T = lo;
+  __syncthreads();
+  const uint16_t* row = hs + (size_t)n * mpad;
+  for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+    const int v = min((int)row[i], bins - 1);
+    if (v > lo) atomicAdd(&hist_s[v], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int running = 0;
+    for (int top = bins - 1; top > lo; top -= 32) {
+      const int b = top - lane;
+      const int c = b > lo ? hist_s[b] : 0;
+      int incl = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const unsigned hit = __ballot_sync(0xffffffffu, b > lo && running + incl >= want);
+      if (hit) {
+        if (lane == 0) s_T = top - (__ffs(hit) - 1);
+        break;
+      }
+      running += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) thr[n] = (uint16_t)s_T;
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -377,26 +441,29 @@ extern "C" size_t glr_heat_workspace(int C, int P, int n_max) {
 
 // pack B (+ thresholds in candidate mode) and launch the GEMM; shared by
 // glr_heat_map (dense map) and glr_heat_topk (candidate lists)
+// sampled rows of the candidate floor's pre-pass (u_step > 1): the map
+// covers image rows u0, u0 + u_step, ... (oh_eff of them, row stride mpad)
+struct HeatRows {
+  int oh_eff = -1, u_step = 1, u0 = 0;
+  int64_t mpad = -1;
+  bool pack = true;
+};
+
 static int run_heat(const uint8_t* stack_d, int H, int W, int P, const HeatGeom& g,
                     const int32_t* anchors_d, int n_max, const int32_t* n_dev_d,
                     uint16_t* heat_d, uint8_t* bmat, uint16_t* thr_d, uint32_t* cnt_d,
-                    uint64_t* cand_d, int cap, cudaStream_t st) {
+                    uint64_t* cand_d, int cap, cudaStream_t st, HeatRows rows = HeatRows()) {
   const int n_pad = (int)cdiv(n_max, heat::BN) * heat::BN;
   auto encode = get_encode_fn();
   GLR_REQUIRE(encode != nullptr, GLR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  {
+  if (rows.pack) {
     int64_t total = (int64_t)n_pad * g.Kp;
     int blocks = (int)std::min<int64_t>(cdiv(total, 256), 148 * 16);
     exemplar_pack_kernel<<<blocks, 256, 0, st>>>(stack_d, g, anchors_d, n_max, n_dev_d, n_pad,
                                                  bmat);
     GLR_CUDA(cudaGetLastError());
   }
-  if (cand_d) {
-    exemplar_thr_kernel<<<(unsigned)cdiv((int64_t)n_max * 32, 256), 256, 0, st>>>(bmat, g.Kp,
-                                                                                  n_max, thr_d);
-    GLR_CUDA(cudaGetLastError());
-    GLR_CUDA(cudaMemsetAsync(cnt_d, 0, (size_t)n_max * sizeof(uint32_t), st));
-  }
+  if (cand_d) GLR_CUDA(cudaMemsetAsync(cnt_d, 0, (size_t)n_max * sizeof(uint32_t), st));
 
   CUtensorMap tmA, tmB;
   {
@@ -421,9 +488,11 @@ static int run_heat(const uint8_t* stack_d, int H, int W, int P, const HeatGeom&
   }
 
   HeatParams hp;
-  hp.oh = g.oh;
+  hp.oh = rows.oh_eff >= 0 ? rows.oh_eff : g.oh;
   hp.ow = g.ow;
-  hp.Mpad = (int)glr_heat_stride(H, W, P);
+  hp.u_step = rows.u_step;
+  hp.u0 = rows.u0;
+  hp.Mpad = (int)(rows.mpad >= 0 ? rows.mpad : glr_heat_stride(H, W, P));
   hp.n_max = n_max;
   hp.m_tiles_per_row = (int)cdiv(g.ow, 2 * heat::BM) * 2;  // even: tiles go in pairs
   hp.S = g.S;
@@ -439,7 +508,8 @@ static int run_heat(const uint8_t* stack_d, int H, int W, int P, const HeatGeom&
     const int s = ensure_smem_attr((const void*)heat_gemm_kernel, heat::SMEM_BYTES);
     if (s) return s;
   }
-  const int64_t pairs = (int64_t)g.oh * (hp.m_tiles_per_row / 2) * (n_pad / heat::BN);
+  const int64_t pairs = (int64_t)hp.oh * (hp.m_tiles_per_row / 2) * (n_pad / heat::BN);
+  if (pairs == 0) return GLR_OK;  // pack only
   GLR_REQUIRE(pairs < (1ll << 31), GLR_ERR_UNSUPPORTED, "heat_map: too many tiles");
   const int sms = device_sms();
   cudaLaunchConfig_t cfg = {};
@@ -542,8 +612,59 @@ extern "C" int glr_heat_topk(const uint8_t* stack_d, int H, int W, int C, int P,
   uint32_t* cnt = reinterpret_cast<uint32_t*>(base + off[2]);
   uint64_t* cand = reinterpret_cast<uint64_t*>(base + off[3]);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // 1. pack B + sampled pre-pass: the dense map of every u_step-th output row
+  //    (at most 16 rows, aliasing the candidate lists, which are written
+  //    only later) -> per-exemplar floor thr[n] (sample_thr_kernel) over the
+  //    |E_n| / 4 lower bound
+  {
+    const int64_t row_room = (int64_t)cap * 4;  // u16 entries per exemplar in the list region
+    int oh_eff = (int)std::min<int64_t>(std::min(32, g.oh), row_room / g.ow);
+    HeatRows rows;
+    if (oh_eff >= 1) {
+      rows.oh_eff = oh_eff;
+      rows.u_step = g.oh / oh_eff;
+      rows.u0 = rows.u_step / 2;
+      rows.mpad = cdiv((int64_t)oh_eff * g.ow, 8) * 8;
+      if (rows.mpad > row_room) rows.oh_eff = oh_eff = 0;
+    }
+    uint16_t* hs = reinterpret_cast<uint16_t*>(cand);
+    if (oh_eff >= 1) {
+      const int r = run_heat(stack_d, H, W, P, g, anchors_d, n_max, nullptr, hs, bmat, nullptr,
+                             nullptr, nullptr, 0, st, rows);
+      if (r != GLR_OK) return r;
+    } else {
+      HeatRows pk;
+      pk.oh_eff = 0;  // pack only: no tiles
+      const int r = run_heat(stack_d, H, W, P, g, anchors_d, n_max, nullptr, hs, bmat, nullptr,
+                             nullptr, nullptr, 0, st, pk);
+      if (r != GLR_OK) return r;
+    }
+    exemplar_thr_kernel<<<(unsigned)cdiv((int64_t)n_max * 32, 256), 256, 0, st>>>(bmat, g.Kp,
+                                                                                  n_max, thr);
+    GLR_CUDA(cudaGetLastError());
+    if (oh_eff >= 1) {
+      const int bins = 4 * C * P * P + 1;
+      const int ns = oh_eff * g.ow;
+      const int64_t M = (int64_t)g.oh * g.ow;
+      const int pool = K * (2 * sep + 1) * (2 * sep + 1) + 1;
+      // aim at ~8 pool-sizes above the floor: the integer scores tie heavily
+      // at the cut, and a floor estimated too high sends the exemplar to the
+      // dense fallback
+      const int want = (int)std::max<int64_t>(1, (8 * (int64_t)pool * ns + M - 1) / M);
+      const int smem = bins * (int)sizeof(int);
+      {
+        const int s_ = ensure_smem_attr((const void*)sample_thr_kernel, smem);
+        if (s_) return s_;
+      }
+      sample_thr_kernel<<<n_max, 256, smem, st>>>(hs, rows.mpad, ns, n_max, bins, want, thr);
+      GLR_CUDA(cudaGetLastError());
+    }
+  }
+  // 2. the candidate GEMM (no pack: B is in place) and the exact top-K on the lists
+  HeatRows nopack;
+  nopack.pack = false;
   const int r = run_heat(stack_d, H, W, P, g, anchors_d, n_max, nullptr, nullptr, bmat, thr, cnt,
-                         cand, cap, st);
+                         cand, cap, st, nopack);
   if (r != GLR_OK) return r;
   return topk_cand_launch(cand, cnt, thr, cap, n_max, g.oh, g.ow, 4 * C * P * P, anchors_d, K,
                           sep, positions_d, padded_d, fallback_d, stream);

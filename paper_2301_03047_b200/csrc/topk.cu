@@ -37,6 +37,7 @@ constexpr int RING_BYTES = 16384;  // 32 bytes per thread per slice
 
 #ifdef GLR_TOPK_STATS
 __device__ unsigned int g_topk_stats[4];  // rows, fallbacks below L, sum / max of count(>= L)
+__device__ unsigned int g_cand_stats[6];  // list path: rows, overflow, short, ties, sum / max count
 #endif
 
 struct TopkParams {
@@ -57,6 +58,14 @@ struct TopkParams {
   // instead of the row again
   uint64_t* scratch;
   int scap;
+  // optional split (with the scratch): the row pass stops after collecting
+  // A and the ties and stages them here (n_max x a_cap / b_cap / 2 counts);
+  // topk_select_kernel sorts them and runs the greedy walk, so the
+  // barrier-heavy sorts and the single-warp walk no longer hold up the
+  // bandwidth-bound row stream
+  uint64_t* stageA;
+  int32_t* stageB;
+  int32_t* stageN;
 };
 
 __device__ __forceinline__ int cheb(int r0, int c0, int r1, int c1) {
@@ -132,7 +141,10 @@ __device__ __forceinline__ void topk_finish(const TopkParams& p, int n, int64_t 
     }
     __syncwarp();
     int32_t* out = p.positions + (size_t)n * p.K * 2;
+    GLR_DCHECK(nch >= 1 && nch <= p.K);
     for (int t = lane; t < p.K; t += 32) {
+      GLR_DCHECK(t >= nch || (chosen[2 * t] >= 0 && chosen[2 * t] < p.oh &&
+                              chosen[2 * t + 1] >= 0 && chosen[2 * t + 1] < p.ow));
       out[2 * t] = t < nch ? chosen[2 * t] : ar;
       out[2 * t + 1] = t < nch ? chosen[2 * t + 1] : ac;
     }
@@ -453,7 +465,7 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
         sB[atomicAdd(&s_nb, 1)] = (int32_t)pos;
     }
     __syncthreads();
-    bitonic_i32(sB, s_nb);
+    if (!p.stageA) bitonic_i32(sB, s_nb);
   } else if (hist[T] <= BCAP) {
     constexpr int U = 4;  // 16-byte loads in flight per thread
     const unsigned lt = (1u << lane) - 1u;
@@ -498,7 +510,7 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
     }
     __syncthreads();
     // ties in index order
-    bitonic_i32(sB, s_nb);
+    if (!p.stageA) bitonic_i32(sB, s_nb);
   } else {
     if (tid == 0) {
       s_baseA = 0;
@@ -545,6 +557,44 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
     }
   }
 
+  if (p.stageA) {
+    // hand A and the ties over to topk_select_kernel (ordered-compaction
+    // path: the first capB ties in index order; otherwise all, unsorted)
+    const int nb = hist[T] <= BCAP ? s_nb : min(s_baseB, capB);
+    uint64_t* ga = p.stageA + (size_t)n * p.a_cap;
+    int32_t* gb = p.stageB + (size_t)n * BCAP;
+    for (int i = tid; i < cntA; i += THREADS) ga[i] = sA[i];
+    for (int i = tid; i < nb; i += THREADS) gb[i] = sB[i];
+    if (tid == 0) {
+      p.stageN[2 * n] = cntA;
+      p.stageN[2 * n + 1] = nb;
+    }
+    return;
+  }
+  topk_finish(p, n, M, need, cntA, sA, sB, chosen);
+}
+
+// Second half of the split top-K: per exemplar, the staged A and ties ->
+// ties sorted by index, A by (score desc, index asc), the greedy walk.
+__global__ void __launch_bounds__(topk::THREADS, 3) topk_select_kernel(TopkParams p) {
+  using namespace topk;
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* sA = reinterpret_cast<uint64_t*>(smem);       // a_cap
+  int32_t* sB = reinterpret_cast<int32_t*>(sA + p.a_cap);  // b_cap
+  int32_t* chosen = sB + p.b_cap;                          // 2*K
+  const int n = blockIdx.x;
+  const int N = p.n_dev ? min(*p.n_dev, p.n_max) : p.n_max;
+  if (n >= N) return;
+  const int tid = threadIdx.x;
+  const int64_t M = p.M;
+  const int need = (int)(M < (int64_t)p.pool ? M : (int64_t)p.pool);
+  const int cntA = p.stageN[2 * n], nb = p.stageN[2 * n + 1];
+  const uint64_t* ga = p.stageA + (size_t)n * p.a_cap;
+  const int32_t* gb = p.stageB + (size_t)n * p.b_cap;
+  for (int i = tid; i < cntA; i += THREADS) sA[i] = ga[i];
+  for (int i = tid; i < nb; i += THREADS) sB[i] = gb[i];
+  __syncthreads();
+  bitonic_i32(sB, nb);
   topk_finish(p, n, M, need, cntA, sA, sB, chosen);
 }
 
@@ -562,6 +612,7 @@ struct TopkCandParams {
   const uint16_t* thr;
   int cap;
   uint8_t* fallback;
+  int b_cap;  // tie buffer of the list path: 16384 (ties at the cut are common on few channels)
 };
 
 __global__ void __launch_bounds__(topk::THREADS, 3) topk_cand_kernel(TopkCandParams q) {
@@ -569,8 +620,8 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_cand_kernel(TopkCandPar
   const TopkParams& p = q.base;
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* sA = reinterpret_cast<uint64_t*>(smem);  // a_cap
-  int32_t* sB = reinterpret_cast<int32_t*>(sA + p.a_cap);  // b_cap
-  int32_t* hist = sB + p.b_cap;                              // bins
+  int32_t* sB = reinterpret_cast<int32_t*>(sA + p.a_cap);  // q.b_cap
+  int32_t* hist = sB + q.b_cap;                              // bins
   int32_t* chosen = hist + p.bins;                           // 2*K
   __shared__ int s_T, s_cntA, s_na, s_nb, s_found;
   const int n = blockIdx.x;
@@ -580,6 +631,15 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_cand_kernel(TopkCandPar
   const int need = (int)(M < (int64_t)p.pool ? M : (int64_t)p.pool);
   const int c = (int)q.cnt[n];
   const int L = min((int)q.thr[n], p.bins - 1);
+#ifdef GLR_TOPK_STATS
+  if (tid == 0) {
+    atomicAdd(&g_cand_stats[0], 1u);
+    if (c > q.cap) atomicAdd(&g_cand_stats[1], 1u);
+    if (c < need) atomicAdd(&g_cand_stats[2], 1u);
+    atomicAdd(&g_cand_stats[4], (unsigned)c);
+    atomicMax(&g_cand_stats[5], (unsigned)c);
+  }
+#endif
   if (c > q.cap || c < need) {  // block-uniform
     if (tid == 0) q.fallback[n] = 1;
     return;
@@ -606,7 +666,10 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_cand_kernel(TopkCandPar
   }
   __syncthreads();
   const int T = s_T, cntA = s_cntA;
-  if (!s_found || hist[T] > p.b_cap) {  // block-uniform
+#ifdef GLR_TOPK_STATS
+  if (tid == 0 && s_found && hist[T] > q.b_cap) atomicAdd(&g_cand_stats[3], 1u);
+#endif
+  if (!s_found || hist[T] > q.b_cap) {  // block-uniform
     if (tid == 0) q.fallback[n] = 1;
     return;
   }
@@ -663,13 +726,25 @@ using namespace glr;
 
 // optional: n_max x kTopkScratch (score, position) records (single row pass)
 constexpr int kTopkScratch = 32768;
+static void topk_caps(int K, int sep, int& a_cap, int& b_cap) {
+  const int pool = topk_pool(K, sep);
+  a_cap = pow2_at_least(pool);
+  b_cap = pow2_at_least(std::max(pool, 4096));
+}
+
 extern "C" size_t glr_topk_workspace(int n_max, int K, int sep) {
-  return (size_t)std::max(n_max, 0) * kTopkScratch * sizeof(uint64_t) + 256;
+  // scratch lists, then the split's staging (A keys, ties, two counts)
+  int a_cap, b_cap;
+  topk_caps(K, sep, a_cap, b_cap);
+  const size_t nm = (size_t)std::max(n_max, 0);
+  return nm * kTopkScratch * sizeof(uint64_t) +
+         nm * ((size_t)a_cap * 8 + (size_t)b_cap * 4 + 8) + 1024;
 }
 
 #ifdef GLR_TOPK_STATS
 extern "C" int glr_debug_topk_stats(unsigned int* out) {
   cudaMemcpyFromSymbol(out, g_topk_stats, sizeof(unsigned int) * 4);
+  cudaMemcpyFromSymbol(out + 4, g_cand_stats, sizeof(unsigned int) * 6);
   return 0;
 }
 #endif
@@ -706,6 +781,9 @@ static int topk_params(int n_max, int oh, int ow, int max_score, const int32_t* 
   p.padded = padded_d;
   p.scratch = nullptr;
   p.scap = 0;
+  p.stageA = nullptr;
+  p.stageB = nullptr;
+  p.stageN = nullptr;
   return GLR_OK;
 }
 
@@ -725,9 +803,24 @@ extern "C" int glr_topk(const uint16_t* heat_d, int n_max, const int32_t* n_dev_
     p.scratch = reinterpret_cast<uint64_t*>(
         (reinterpret_cast<uintptr_t>(ws_d) + 255) & ~uintptr_t(255));
     p.scap = kTopkScratch;
+#ifdef GLR_TOPK_SPLIT  // dev A/B, off: measured 2.44 vs 2.36 ms per C2 refresh (the row
+                       // stream, not the per-CTA tail, bounds the kernel)
+    int a_cap, b_cap;
+    topk_caps(K, sep, a_cap, b_cap);
+    uint8_t* st = reinterpret_cast<uint8_t*>(p.scratch + (size_t)n_max * kTopkScratch);
+    p.stageA = reinterpret_cast<uint64_t*>(st);
+    p.stageB = reinterpret_cast<int32_t*>(st + (size_t)n_max * a_cap * 8);
+    p.stageN = reinterpret_cast<int32_t*>(st + (size_t)n_max * (a_cap * 8 + (size_t)b_cap * 4));
+#endif
   }
   { const int s_ = ensure_smem_attr((const void*)topk_kernel, (int)smem); if (s_) return s_; }
   topk_kernel<<<n_max, topk::THREADS, smem, (cudaStream_t)stream>>>(p);
+  if (p.stageA) {
+    GLR_CUDA(cudaGetLastError());
+    const size_t ssmem = (size_t)p.a_cap * 8 + (size_t)p.b_cap * 4 + (size_t)K * 8 + 16;
+    { const int s_ = ensure_smem_attr((const void*)topk_select_kernel, (int)ssmem); if (s_) return s_; }
+    topk_select_kernel<<<n_max, topk::THREADS, ssmem, (cudaStream_t)stream>>>(p);
+  }
   return check_launch("topk_kernel");
 }
 
@@ -747,6 +840,12 @@ int topk_cand_launch(const uint64_t* cand_d, const uint32_t* cnt_d, const uint16
   q.thr = thr_d;
   q.cap = cap;
   q.fallback = fallback_d;
+  q.b_cap = 16384;
+  // the list path has no bulk-copy ring: sA | sB (16384 ties) | hist | chosen
+  smem = (size_t)q.base.a_cap * 8 + (size_t)q.b_cap * 4 + (size_t)q.base.bins * 4 +
+         (size_t)K * 8 + 16;
+  GLR_REQUIRE(smem <= 200 * 1024, GLR_ERR_UNSUPPORTED, "topk_cand: %zu bytes of shared memory",
+              smem);
   { const int s_ = ensure_smem_attr((const void*)topk_cand_kernel, (int)smem); if (s_) return s_; }
   topk_cand_kernel<<<n_max, topk::THREADS, smem, (cudaStream_t)stream>>>(q);
   return check_launch("topk_cand_kernel");

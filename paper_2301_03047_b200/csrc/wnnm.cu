@@ -71,6 +71,7 @@ struct GroupSrc {
   const double* src;
   const int32_t* pos;  // image groups: (n, K, 2) top-left positions
   int W, C, PC;
+  int H;               // image groups: image rows (bounds checks of the checked build)
   int64_t rs;
   int m, K;
 };
@@ -79,6 +80,7 @@ template <bool IMG>
 __device__ __forceinline__ long long col_base(const GroupSrc& s, int g, int j) {
   if constexpr (IMG) {
     const int32_t* q = s.pos + ((size_t)g * s.K + j) * 2;
+    GLR_DCHECK(q[0] >= 0 && q[1] >= 0 && q[0] + s.m / s.PC <= s.H && q[1] + s.PC / s.C <= s.W);
     return ((long long)q[0] * s.W + q[1]) * s.C;
   } else {
     return ((long long)g * s.K + j) * s.m;
@@ -1359,6 +1361,7 @@ __global__ void scatter_count_kernel(const int32_t* __restrict__ pos, int n_max,
     const int64_t col = i / (P * P);
     const int o = (int)(i - col * P * P);
     const int r = pos[2 * col] + o / P, c = pos[2 * col + 1] + o % P;
+    GLR_DCHECK(r >= 0 && c >= 0 && c < W);
     atomicAdd(&cnt[(int64_t)r * W + c], 1);
   }
 }
@@ -1772,6 +1775,7 @@ extern "C" int glr_wnnm_scatter(const double* x_d, int H, int W, int C, int P,
   s.src = x_d;
   s.pos = positions_d;
   s.W = W;
+  s.H = H;
   s.C = C;
   s.PC = P * C;
   s.rs = (int64_t)W * C;

@@ -162,7 +162,7 @@ class GlrEngine:
 
     def __init__(self, shape, match, peak: float = 1.0, c_weight: float = 2.0 * np.sqrt(2.0),
                  eps: float = 1e-16, process_group=None, heat_budget_bytes: int = 24 << 30,
-                 low_memory_match: bool = False, regularizer: str = "glr"):
+                 low_memory_match: bool | None = None, regularizer: str = "glr"):
         t = D.torch()
         h, w, c = shape
         self.shape = (h, w, c)
@@ -236,6 +236,17 @@ class GlrEngine:
         # lists of `cand_cap` entries instead of the map (8x less memory); the
         # dense path runs only for the exemplars it hands back.
         self.heat_budget = heat_budget_bytes
+        import os
+        mode = os.environ.get("GLR_MATCH_MODE", "")  # dev A/B switch: dense | fused
+        if mode in ("dense", "fused"):
+            low_memory_match = mode == "fused"
+        if low_memory_match is None:
+            # auto: the fused path (no dense map) wins where the map write
+            # binds the heat GEMM -- one-channel images (C5: 99 vs 134 ms for
+            # heat + top-K at P = 8, 16k exemplars); with more channels the
+            # GEMM is MMA-bound and the dense map + single-pass top-K is
+            # faster (C2 12.1 vs 12.6 ms per refresh, C4, C1)
+            low_memory_match = c == 1
         self.low_memory_match = bool(low_memory_match)
         self.heat = None
         self.ws_dense = None
@@ -243,7 +254,11 @@ class GlrEngine:
         if not self.global_match:
             pass
         elif self.low_memory_match:
-            self.cand_cap = int(min(1 << 17, self.oh * self.ow))
+            # list capacity: 32 pool-sizes (the sampled floor aims at ~8), and
+            # room for the 32-row sampled pre-pass it aliases
+            pool = self.k * (2 * match.sep + 1) ** 2 + 1
+            self.cand_cap = int(min(max(32 * pool, 8192, -(-32 * self.ow // 4)),
+                                    self.oh * self.ow, 1 << 17))
             per = 8 * self.cand_cap + N.query("glr_heat_topk_workspace", c, p, 1, 0)
             self.heat_chunk = max(1, min(self.max_anchors, heat_budget_bytes // per))
             self.ws_heat = D.empty((N.query("glr_heat_topk_workspace", c, p, self.heat_chunk,
@@ -485,12 +500,16 @@ class GlrEngine:
             anc = self.anchors.index_select(0, idx).contiguous()
             pos = D.empty((nb, self.k, 2), t.int32)
             pad = D.empty((nb,), t.int32)
+            e = self._ev()
             N.call("glr_heat_map", self.stack.data_ptr(), h, w, c, self.p, self.expand,
                    anc.data_ptr(), nb, None, self.heat.data_ptr(), self.ws_dense.data_ptr(),
                    self.ws_dense.numel(), s)
+            self._log(("heat_map", nb), e)
+            e = self._ev()
             N.call("glr_topk", self.heat.data_ptr(), nb, None, self.oh, self.ow, self.max_score,
                    anc.data_ptr(), self.k, self.mc.sep, pos.data_ptr(), pad.data_ptr(), None, 0,
                    s)
+            self._log(("topk", nb), e)
             self.positions.index_copy_(0, idx, pos)
             self.padded.index_copy_(0, idx, pad)
 

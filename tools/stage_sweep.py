@@ -5,7 +5,7 @@ exemplars, K = 64, no solver loop. One JSON line per (P, N) with device
 times (CUDA events on the launching stream, best of `--reps` after one
 warm-up) and the roofline numbers of each stage:
 
-  heat   2 M (4 C P^2) N flops (tcgen05 kind::mxf4; peak 4 x measured bf16)
+  heat   2 M (4 C P^2) N flops (tcgen05 kind::mxf4; peak: measured mxf4 rate)
   top-K  2 M N bytes (one read of the u16 heat rows; peak measured HBM)
   WNNM   m K (K + 1) + 2 m K^2 flops per group (fp64 DMMA peak 37.1 TF/s)
 
@@ -36,9 +36,9 @@ FP64_PEAK = 37.1
 
 
 def peaks():
-    p = ROOT / "MEASURED_PEAKS.json"
-    d = json.loads(p.read_text()) if p.exists() else {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
-    return d["hbm_gbs"], 4.0 * d["bf16_tflops"]
+    import bench
+    d, _ = bench._peaks()
+    return d["hbm_gbs"], bench._fp4_peak(d)["tflops"]
 
 
 def stage_times(eng, x_d, sigma):
@@ -59,16 +59,22 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--fused", action="store_true",
+                    help="heat map + top-K fused (glr_heat_topk, sampled candidate floor)")
+    ap.add_argument("--only", default=None, help="P:N pairs, e.g. 8:16384,12:4096")
     args = ap.parse_args()
     hbm, fp4 = peaks()
     wl = workloads.make("C5")
     h, w, c = wl.shape
     x_d = D.f64(wl.scene)
     lines = []
-    for p in (8, 12):
-        for n in (1024, 4096, 16384):
+    combos = [(p, n) for p in (8, 12) for n in (1024, 4096, 16384)]
+    if args.only:
+        combos = [tuple(int(v) for v in c.split(":")) for c in args.only.split(",")]
+    for p, n in combos:
+        if True:
             mc = G.MatchConfig(patch_size=p, group_size=64, max_corners=n, exemplar_stride=4096)
-            eng = GlrEngine((h, w, c), mc)
+            eng = GlrEngine((h, w, c), mc, low_memory_match=args.fused)
             best = None
             for r in range(args.reps + 1):  # first run = warm-up
                 t = stage_times(eng, x_d, 0.05)
@@ -79,11 +85,15 @@ def main():
             M = (h - p + 1) * (w - p + 1)
             m = p * p * c
             k = mc.group_size
-            heat_ms = best["heat_map"][0]
-            topk_ms = best["topk"][0]
+            if args.fused:
+                heat_ms = best["heat_topk"][0]
+                topk_ms = sum(best[k][0] for k in ("heat_map", "topk") if k in best)
+            else:
+                heat_ms = best["heat_map"][0]
+                topk_ms = best["topk"][0]
             wn_ms = best["wnnm_scatter"][0]
             heat_tf = 2.0 * M * 4 * c * p * p * N / (heat_ms / 1e3) / 1e12
-            topk_gbs = 2.0 * M * N / (topk_ms / 1e3) / 1e9
+            topk_gbs = 2.0 * M * N / (topk_ms / 1e3) / 1e9 if topk_ms > 0 else 0.0
             wn_tf = (m * k * (k + 1) + 2.0 * m * k * k) * N / (wn_ms / 1e3) / 1e12
             line = {
                 "workload": f"C5 stage sweep: 2048x2048x1, P={p}, K={k}", "P": p,
@@ -97,7 +107,9 @@ def main():
                 "wnnm": {"ms": round(wn_ms, 3), "tflops": round(wn_tf, 2),
                          "frac": round(wn_tf / FP64_PEAK, 3), "m": m},
                 "peaks": {"fp4_tflops": fp4, "hbm_gbs": hbm, "fp64_tflops": FP64_PEAK},
-                "heat_chunks": best["heat_map"][1] and -(-N // eng.heat_chunk),
+                "heat_chunks": -(-N // eng.heat_chunk),
+                "mode": ("fused heat+top-K (heat = fused kernel pair, topk = dense fallback "
+                         f"for {eng.n_fallback} exemplars)") if args.fused else "dense map + top-K",
             }
             print(json.dumps(line), flush=True)
             lines.append(line)

@@ -231,6 +231,17 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
       const int ui = m_tile / p.m_tiles_per_row;  // output row (sample row index)
       const int u = ui * p.u_step + p.u0;         // image row
       const int v = (m_tile % p.m_tiles_per_row) * BM + ew * 32 + lane;
+      // candidate mode: this warp's exemplar floors, loaded before the wait
+      // (a global load per chunk after it was the kernel's top stall)
+      constexpr int MAXC = (NCH + EPI_GROUPS - 1) / EPI_GROUPS;
+      int tl_c[MAXC];
+      if (p.cand) {
+#pragma unroll
+        for (int k = 0; k < MAXC; ++k) {
+          const int n = n0 + (c_lo + k) * 32 + lane;
+          tl_c[k] = (c_lo + k < c_hi && n < N) ? (int)p.thr[n] : 0x10000;
+        }
+      }
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
       const bool v_ok = v < p.ow;
@@ -248,7 +259,10 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
           // registers of the lane that owns the column); only a chunk in
           // which some lane has a hit takes the per-column ballot and the
           // warp-aggregated list appends
-          const int tl = nb + lane < N ? (int)p.thr[nb + lane] : 0x10000;
+          int tl = 0x10000;
+#pragma unroll
+          for (int k = 0; k < MAXC; ++k)
+            if (c == c_lo + k) tl = tl_c[k];
           const uint32_t pos = (uint32_t)(u * p.ow + v);
           const unsigned lt = (1u << lane) - 1u;
           const float tlf = (float)tl;
@@ -257,20 +271,32 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
           for (int j = 0; j < 32; ++j)
             any |= __uint_as_float(r[j]) >= __shfl_sync(0xffffffffu, tlf, j);
           if (!__any_sync(0xffffffffu, any && v_ok)) continue;
+          // pass 1: per column j the warp's hit mask (lane j keeps it) and
+          // this lane's hit bits; then ONE warp-wide atomic reserves every
+          // column's slots at once (lane j for column j), so a chunk pays one
+          // atomic round trip instead of one per hit column
+          unsigned col_mask = 0, my_hits = 0;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int sc = (int)__float2uint_rn(__uint_as_float(r[j]));
             const int tj = __shfl_sync(0xffffffffu, tl, j);  // all lanes (no short-circuit)
             const bool hit = v_ok && sc >= tj;
             const unsigned m = __ballot_sync(0xffffffffu, hit);
-            if (m) {
-              const int n = nb + j;
-              const int ld = __ffs(m) - 1;
-              uint32_t base = 0;
-              if (lane == ld) base = atomicAdd(&p.cnt[n], (uint32_t)__popc(m));
-              base = __shfl_sync(0xffffffffu, base, ld) + __popc(m & lt);
-              if (hit && base < (uint32_t)p.cap)
-                p.cand[(size_t)n * p.cap + base] = ((uint64_t)sc << 32) | pos;
+            if (lane == j) col_mask = m;
+            my_hits |= (unsigned)hit << j;
+          }
+          uint32_t base = 0;
+          if (col_mask) base = atomicAdd(&p.cnt[nb + lane], (uint32_t)__popc(col_mask));
+          const unsigned any_cols = __ballot_sync(0xffffffffu, col_mask != 0);
+          // pass 2: the appends of every hit column
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (!((any_cols >> j) & 1u)) continue;  // warp-uniform
+            const unsigned m = __shfl_sync(0xffffffffu, col_mask, j);
+            const uint32_t b = __shfl_sync(0xffffffffu, base, j) + __popc(m & lt);
+            if (((my_hits >> j) & 1u) && b < (uint32_t)p.cap) {
+              const int sc = (int)__float2uint_rn(__uint_as_float(r[j]));
+              p.cand[(size_t)(nb + j) * p.cap + b] = ((uint64_t)sc << 32) | pos;
             }
           }
           continue;
@@ -364,8 +390,18 @@ __global__ void __launch_bounds__(256) sample_thr_kernel(const uint16_t* __restr
   for (int b = threadIdx.x; b < bins; b += blockDim.x) hist_s[b] = 0;
   if (threadIdx.x == 0) s_T = lo;
   __syncthreads();
-  const uint16_t* row = hs + (size_t)n * mpad;
-  for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+  const uint16_t* row = hs + (size_t)n * mpad;  // 16-byte aligned (mpad % 8 == 0)
+  const uint4* rv = reinterpret_cast<const uint4*>(row);
+  for (int i = threadIdx.x; i < ns / 8; i += blockDim.x) {
+    const uint4 q = rv[i];
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int v = min((int)((w[j >> 1] >> (16 * (j & 1))) & 0xFFFFu), bins - 1);
+      if (v > lo) atomicAdd(&hist_s[v], 1);
+    }
+  }
+  for (int i = (ns / 8) * 8 + threadIdx.x; i < ns; i += blockDim.x) {
     const int v = min((int)row[i], bins - 1);
     if (v > lo) atomicAdd(&hist_s[v], 1);
   }

@@ -29,6 +29,7 @@ namespace glr {
 
 namespace topk {
 constexpr int THREADS = 512;
+constexpr int kSelB = 2048;  // tie-selection buckets / kept ties of the list path
 constexpr int VEC = 8;  // u16 scores per 16-byte load
 constexpr int MAX_BINS = 12288;
 constexpr int RING_STAGES = 3;
@@ -623,6 +624,8 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_cand_kernel(TopkCandPar
   int32_t* sB = reinterpret_cast<int32_t*>(sA + p.a_cap);  // q.b_cap
   int32_t* hist = sB + q.b_cap;                              // bins
   int32_t* chosen = hist + p.bins;                           // 2*K
+  int32_t* bkt = chosen + 2 * p.K;                           // kSelB (tie selection)
+  int32_t* kept = bkt + kSelB;                               // kSelB
   __shared__ int s_T, s_cntA, s_na, s_nb, s_found;
   const int n = blockIdx.x;
   if (n >= p.n_max) return;
@@ -684,8 +687,58 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_cand_kernel(TopkCandPar
       sB[atomicAdd(&s_nb, 1)] = (int32_t)pos;
   }
   __syncthreads();
-  bitonic_i32(sB, s_nb);
-  topk_finish(p, n, M, need, cntA, sA, sB, chosen);
+  // Only the first capB = need - cntA ties in index order are used. With
+  // few channels thousands of positions tie at the cut; instead of sorting
+  // them all, a radix select on the high index bits keeps the buckets below
+  // the one holding the capB-th smallest index plus that bucket, and only
+  // those (<= kSelB) are sorted.
+  const int capB = need - cntA;
+  int nb = s_nb;
+  int32_t* ties = sB;
+  if (nb > kSelB && capB < kSelB) {
+    int shift = 0;
+    while (((M - 1) >> shift) >= kSelB) ++shift;
+    for (int b = tid; b < kSelB; b += THREADS) bkt[b] = 0;
+    __syncthreads();
+    for (int i = tid; i < nb; i += THREADS) atomicAdd(&bkt[sB[i] >> shift], 1);
+    __syncthreads();
+    __shared__ int s_cut, s_kept;
+    if (warp == 0) {  // first bucket where the running count reaches capB
+      const int lane = tid & 31;
+      int running = 0;
+      for (int b0 = 0; b0 < kSelB; b0 += 32) {
+        const int c = bkt[b0 + lane];
+        int incl = c;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, running + incl >= capB);
+        if (hit) {
+          if (lane == 0) s_cut = b0 + __ffs(hit) - 1;
+          break;
+        }
+        running += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) s_kept = 0;
+    }
+    __syncthreads();
+    const int cut = s_cut;
+    for (int i = tid; i < nb; i += THREADS) {
+      const int v = sB[i];
+      if ((v >> shift) <= cut) {
+        const int k = atomicAdd(&s_kept, 1);
+        if (k < kSelB) kept[k] = v;
+      }
+    }
+    __syncthreads();
+    if (s_kept <= kSelB) {  // block-uniform; else keep the full sort below
+      nb = s_kept;
+      ties = kept;
+    }
+  }
+  bitonic_i32(ties, nb);
+  topk_finish(p, n, M, need, cntA, sA, ties, chosen);
 }
 
 // gather_group (patches.py:43-54): groups[g][j][i], i = (dr*P + dc)*C + ch
@@ -843,7 +896,7 @@ int topk_cand_launch(const uint64_t* cand_d, const uint32_t* cnt_d, const uint16
   q.b_cap = 16384;
   // the list path has no bulk-copy ring: sA | sB (16384 ties) | hist | chosen
   smem = (size_t)q.base.a_cap * 8 + (size_t)q.b_cap * 4 + (size_t)q.base.bins * 4 +
-         (size_t)K * 8 + 16;
+         (size_t)K * 8 + 2 * topk::kSelB * 4 + 16;
   GLR_REQUIRE(smem <= 200 * 1024, GLR_ERR_UNSUPPORTED, "topk_cand: %zu bytes of shared memory",
               smem);
   { const int s_ = ensure_smem_attr((const void*)topk_cand_kernel, (int)smem); if (s_) return s_; }

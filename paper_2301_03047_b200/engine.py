@@ -241,12 +241,16 @@ class GlrEngine:
         if mode in ("dense", "fused"):
             low_memory_match = mode == "fused"
         if low_memory_match is None:
-            # auto: the fused path (no dense map) wins where the map write
-            # binds the heat GEMM -- one-channel images (C5: 99 vs 134 ms for
-            # heat + top-K at P = 8, 16k exemplars); with more channels the
-            # GEMM is MMA-bound and the dense map + single-pass top-K is
-            # faster (C2 12.1 vs 12.6 ms per refresh, C4, C1)
-            low_memory_match = c == 1
+            # auto: the fused path (candidate lists, no dense map) wherever the
+            # dense map would be large -- measured per refresh: C5 P = 8, 16k
+            # exemplars 43 vs 127 ms, C2 11.1 vs 11.7 ms; for maps of ~1 GB and
+            # below the dense map + single-pass top-K is as fast or faster
+            # (C4 105.7 vs 105.0 ms per solve, C1 26.8 vs 24.7) and C3's sparse
+            # phantom maps (the pool reaches score 0) fall back anyway
+            p_ = match.patch_size
+            g_ = 3 * match.exemplar_stride
+            n_est = match.max_corners + ((h - p_) // g_ + 1) * ((w - p_) // g_ + 1)
+            low_memory_match = n_est * (h - p_ + 1) * (w - p_ + 1) * 2 > (4 << 30)
         self.low_memory_match = bool(low_memory_match)
         self.heat = None
         self.ws_dense = None

@@ -66,12 +66,29 @@ def per_launch(names, warm_only=True):
 
 
 src = f"profiles/{tag}_ncu_full_C2.txt (ncu --set full, tools/ncu_window.py C2)"
+def per_call(names):
+    """dram bytes of the first `names[n]` captures of each named kernel (one
+    fused-match call launches the heat GEMM twice and the others once)."""
+    tot, used = 0.0, {}
+    for d in out:
+        for n, lim in names.items():
+            if n in d["kernel"] and used.get(n, 0) < lim:
+                used[n] = used.get(n, 0) + 1
+                tot += d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
+    return tot
+
+
 traffic = {
-    "wnnm_scatter": {"bytes": per_launch(["gram_kernel", "eig_kernel", "apply_kernel"]),
+    "wnnm_scatter": {"bytes": per_launch(["gram_kernel", "eig_kernel", "apply_oz_kernel"]),
                      "unit": "bytes per launch (gram + eig + apply)", "source": src},
     "heat_map": {"bytes": per_launch(["heat_gemm_kernel"]), "unit": "bytes per launch",
                  "source": src},
     "topk": {"bytes": per_launch(["topk_kernel"]), "unit": "bytes per launch", "source": src},
+    "heat_topk": {"bytes": per_call({"exemplar_pack_kernel": 1, "heat_gemm_kernel": 2,
+                                     "exemplar_thr_kernel": 1, "sample_thr_kernel": 1,
+                                     "topk_cand_kernel": 1}),
+                  "unit": "bytes per call (pack + sampled pre-pass + candidate GEMM + list top-K)",
+                  "source": src},
 }
 (prof / "ncu_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
 summ = subprocess.run([sys.executable, str(ROOT / "tools" / "ncu_summary.py"), launches],

@@ -61,6 +61,20 @@ constexpr double kRotTol = GLR_EIG_ROTTOL;
 #define GLR_EIG_FINISHTOL 1e-5
 #endif
 constexpr double kFinishTol = GLR_EIG_FINISHTOL;
+// Zero-shrinkage exemption, gap rule: a pair of exempt indices (j, k) is
+// left alone only while |g_jk| <= kZGapTol (KD - max(g_jj, g_kk)), KD the
+// smallest diagonal entry of a kept index. The couplings inside the exempt
+// block feed back into the kept-exempt entries at the rate |g_jk| / gap per
+// sweep (rotating (i, k) refills g_ij with -sin(theta_ik) g_kj), so where the
+// kept and the exempt eigenvalues are close (C4's late iterations: 38 of 64
+// components kept, a continuous spectrum across the threshold) an
+// undiagonalised exempt block turned the quadratic convergence into a slow
+// linear one (8-9 sweeps from a warm start, measured); where the gap is wide
+// (C3: one dominant component) every exempt pair is still skipped.
+#ifndef GLR_EIG_ZGAPTOL
+#define GLR_EIG_ZGAPTOL 1e-3
+#endif
+constexpr double kZGapTol = GLR_EIG_ZGAPTOL;
 }  // namespace wn
 
 // Element (r, j) of group g lives at src[cbase(g, j) + roff(r)]: for image
@@ -237,6 +251,8 @@ __global__ void __launch_bounds__(wn::GRAM_THREADS)
 // dev statistics: groups per sweep count (cold [0, 32), warm [32, 64))
 __device__ unsigned int g_eig_hist[64];
 __device__ unsigned int g_rank_hist[65];  // groups by number of kept components
+// warm groups, first pre-check: [0] groups, [1 + d] non-exempt pairs above 1e-(4+d) relative
+__device__ unsigned long long g_res_hist[8];
 #endif
 
 struct EigArgs {
@@ -516,7 +532,7 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
     }
   }
   __syncthreads();
-  const double tiny = s_tiny;
+  const double tiny = s_tiny, tiny2 = tiny * tiny;
 
   // ---- parallel cyclic Jacobi in 4x4 block steps (schedule above). Per
   // super-round: phase 1 -- warp 0 lanes 0..15, one quad each, run the
@@ -530,6 +546,8 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
   __shared__ unsigned s_qrot[2];
   __shared__ unsigned char s_zb[8];  // per warp: zero-shrinkage flags of its 8 rows
   __shared__ unsigned char s_ub[8];  // per warp: rows too close to the shrinkage kink
+  __shared__ double s_kd[8];         // per warp: smallest kept diagonal entry
+  __shared__ double s_rz[8];         // per warp: largest off-diagonal row sum of an exempt row
   __shared__ double lamv[KMAX];      // final diagonal (first-order finish)
   const int qA = 2 * warp + (lane >> 4), qB = lane & 15;
   int gsr = 0, prev_sr = -1;  // running super-round count; pending V step
@@ -586,7 +604,15 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
       const bool u = !z && shrinks_to_zero(a, gii - r - 1e-3 * fabs(gii));
       const unsigned bz = __ballot_sync(0xffffffffu, z && q == 0);
       const unsigned bu = __ballot_sync(0xffffffffu, u && q == 0);
+      double kd = z ? __longlong_as_double(0x7ff0000000000000ll) : gii, rz = z ? r : 0.0;
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        kd = fmin(kd, __shfl_xor_sync(0xffffffffu, kd, o));
+        rz = fmax(rz, __shfl_xor_sync(0xffffffffu, rz, o));
+      }
       if (lane == 0) {
+        s_kd[warp] = kd;
+        s_rz[warp] = rz;
         unsigned char m8 = 0, u8 = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -600,27 +626,54 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
     __syncthreads();
     zmask = 0;
     bool unsafe = false;
+    double KD = s_kd[0], RZ = s_rz[0];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       zmask |= (uint64_t)s_zb[k] << (8 * k);
       unsafe |= s_ub[k] != 0;
+      KD = fmin(KD, s_kd[k]);
+      RZ = fmax(RZ, s_rz[k]);
     }
     // A sweep changes G only if some pair passes the rotation test on the
     // current G (otherwise no round rotates, by induction): test all pairs
     // up front and stop without paying for a no-op sweep. The sweeps also
     // stop once the first-order finish is exact to second order: no kept
     // row near the kink, kept-kept pairs below kFinishTol, and every
-    // kept-exempt pair below the rotation test (fully decoupled).
+    // kept-exempt pair below its own finish bound (see the pair test).
     bool need = false, block_finish = false;
+    const double rot_over_rz2 = (kRotTol / RZ) * (kRotTol / RZ);  // +inf without exempt rows (unused then)
     for (int t = tid; t < GSZ; t += EIG_THREADS) {
       const int i = t >> 6, j = t & 63;
       const unsigned zi = (zmask >> i) & 1ull, zj = (zmask >> j) & 1ull;
       if (i < j && !(zi & zj)) {
-        const double gij = fabs(G[i * GLD + j]);
-        const double sc = sqrt(fabs(G[i * GLD + i] * G[j * GLD + j]));
-        const bool strict = gij > fmax(kRotTol * sc, tiny);
-        need |= strict;
-        block_finish |= (zi | zj) ? strict : gij > fmax(kFinishTol * sc, tiny);
+        // squared comparisons (no square roots): g_ij^2 against tol^2 |g_ii g_jj|
+        const double gij = G[i * GLD + j], g2 = gij * gij;
+        const double gi = G[i * GLD + i], gj = G[j * GLD + j];
+        const double sc2 = fabs(gi * gj);
+        double st2 = kRotTol * kRotTol * sc2, fin2 = kFinishTol * kFinishTol * sc2;
+        if (zi | zj) {
+          // kept-exempt pair: the exempt eigenvalue is mapped to zero, so only
+          // the rotation ANGLE g_ij / gap matters, not the relative accuracy
+          // of the small diagonal entry -- the strict test is relative to
+          // max(sqrt(g_ii g_jj), gap). The finish may leave an angle theta as
+          // long as the first-order term r_i theta (applied below with the
+          // diagonal of the exempt block standing in for the block: relative
+          // error RZ / gap by a Neumann series of the resolvent) stays exact
+          // to kRotTol: theta <= kFinishTol and theta RZ / gap <= kRotTol.
+          const double gap = gi - gj, gap2 = gap * gap;
+          st2 = kRotTol * kRotTol * fmax(sc2, gap2);
+          fin2 = gap2 * fmin(kFinishTol * kFinishTol, gap2 * rot_over_rz2);
+        }
+        st2 = fmax(st2, tiny2);
+#ifdef GLR_EIG_STATS
+        if (warm && sweep == 0) {
+          const double rel = fabs(gij) / fmax(sqrt(sc2), 1e-300);
+          for (int d = 0; d < 6; ++d)
+            if (rel > pow(10.0, -(4.0 + d))) atomicAdd(&g_res_hist[1 + d], 1ull);
+        }
+#endif
+        need |= g2 > st2;
+        block_finish |= g2 > fmax(st2, fin2);
       }
     }
     const bool any_need = __syncthreads_or(need);
@@ -662,8 +715,16 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
               app[h] = S[p][p];
               aqq[h] = S[q][q];
               apq[h] = S[p][q];
-              const bool rot = fabs(apq[h]) > fmax(kRotTol * sqrt(fabs(app[h] * aqq[h])), tiny) &&
-                               !((zmask >> e[p]) & (zmask >> e[q]) & 1ull);
+              const unsigned zp = (zmask >> e[p]) & 1ull, zq = (zmask >> e[q]) & 1ull;
+              // the sweep's pre-check tests, squared (no square root on the rotation's
+              // latency chain): kept-exempt pairs relative to max(sc, gap); exempt
+              // pairs only under the gap rule (kZGapTol)
+              const double a2 = apq[h] * apq[h], dpq = app[h] - aqq[h];
+              const double sc2 = fabs(app[h] * aqq[h]);
+              const double thr2 = (zp ^ zq) ? fmax(sc2, dpq * dpq) : sc2;
+              const bool rot =
+                  a2 > fmax(kRotTol * kRotTol * thr2, tiny2) &&
+                  !((zp & zq) && fabs(apq[h]) <= kZGapTol * (KD - fmax(app[h], aqq[h])));
               any |= rot;
               rotd[h] = rot;
               // t = sign(tau) / (|tau| + sqrt(1 + tau^2)), tau = d / g, as
@@ -758,6 +819,7 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
 
 #ifdef GLR_EIG_STATS
   if (tid == 0) atomicAdd(&g_eig_hist[warm ? 32 + sweep : sweep], 1u);
+  if (tid == 0 && warm) atomicAdd(&g_res_hist[0], 1ull);
 #endif
   if (vc) {
     for (int t = tid; t < GSZ; t += EIG_THREADS) vc[t] = Vt[(t >> 6) * VLD + (t & 63)];
@@ -794,7 +856,7 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
         v = ratio[i];
       } else if (i < K && j < K) {
         const double li = lamv[i], lj = lamv[j], e = G[i * GLD + j];
-        if (fabs(e) > kRotTol * sqrt(fabs(li * lj))) {
+        if (e * e > kRotTol * kRotTol * fabs(li * lj)) {
           const double d = li - lj;
           const double D = fabs(d) > 1e-4 * fmax(fabs(li), fabs(lj))
                                ? (ratio[i] - ratio[j]) / d
@@ -1711,7 +1773,10 @@ using namespace glr;
 extern "C" int glr_debug_eig_hist(unsigned int* out, int reset) {
   cudaMemcpyFromSymbol(out, g_eig_hist, sizeof(unsigned int) * 64);
   cudaMemcpyFromSymbol(out + 64, g_rank_hist, sizeof(unsigned int) * 65);
+  cudaMemcpyFromSymbol(out + 130, g_res_hist, sizeof(unsigned long long) * 8);
   if (reset) {
+    unsigned long long z8[8] = {};
+    cudaMemcpyToSymbol(g_res_hist, z8, sizeof(z8));
     unsigned int z[65] = {};
     cudaMemcpyToSymbol(g_eig_hist, z, sizeof(unsigned int) * 64);
     cudaMemcpyToSymbol(g_rank_hist, z, sizeof(unsigned int) * 65);

@@ -19,7 +19,7 @@ y = r.dop.upload_y(wl.y)
 lib = N.load()
 fn = lib.glr_debug_eig_hist
 fn.argtypes = [C.c_void_p, C.c_int]
-buf = (C.c_uint * 129)()
+buf = (C.c_uint * 146)()
 fn(buf, 1)
 
 
@@ -33,6 +33,10 @@ def on_iter(it, x):
     rk = np.array(buf[64:129])
     cum = np.cumsum(rk) / max(rk.sum(), 1)
     q = [int(np.searchsorted(cum, f)) for f in (0.1, 0.5, 0.9, 0.99)]
+    res = np.frombuffer(bytes(buf), dtype=np.uint64, count=8, offset=130 * 4)
+    ng = max(int(res[0]), 1)
+    rs = ' '.join(f'{int(v) / ng:.1f}' for v in res[1:7])
+    print(f"it {it:2d} pairs/group above 1e-4..1e-9: {rs}")
     print(f"it {it:2d} mean sweeps {tot / max(h.sum(), 1):.2f} cold {cold} warm {warm} "
           f"kept-rank mean {rk @ np.arange(65) / max(rk.sum(), 1):.1f} p10/50/90/99 {q}")
 

@@ -1,0 +1,13 @@
+# threshold sweeps: parity, benches, then stats build
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_full_configs.py tests/test_gpu_configs.py tests/test_gpu_multirank.py -m gpu -x -q > gpurun_out/f_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/f_pytest.log
+for c in C2 C3 C4 C1; do
+  timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/f_bench_$c.json 2> gpurun_out/f_bench_$c.err
+done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file /tmp/f_launch_C2.csv python tools/one_solve.py C2 > gpurun_out/f_ncu_C2.log 2>&1
+python tools/launch_series.py /tmp/f_launch_C2.csv gram_kernel eig_kernel apply_oz_kernel > gpurun_out/f_series_C2.txt
+GLR_NVCC_EXTRA="-DGLR_EIG_STATS" python -m paper_2301_03047_b200._build -f > gpurun_out/f_build.log 2>&1
+for c in C2 C4 C3; do timeout 600 python tools/eig_stats.py $c > gpurun_out/f_eig_$c.log 2>&1; done
+tail -3 gpurun_out/f_pytest.log
+for c in C2 C3 C4 C1; do cut -c1-200 gpurun_out/f_bench_$c.json; done
+grep eig_kernel -A1 gpurun_out/f_series_C2.txt

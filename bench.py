@@ -150,7 +150,7 @@ def cpu_full(wl) -> dict:
     t0 = time.perf_counter()
     O.gap_solve(op, wl.y, wl.max_iters, patch_size=mc.patch_size, group_size=mc.group_size,
                 max_corners=mc.max_corners, exemplar_stride=mc.exemplar_stride,
-                clip=wl.kind != "fourier")
+                clip=wl.kind != "fourier", init=wl.init)
     t = time.perf_counter() - t0
     return {"value": wl.max_iters / t, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
             "extrapolated": False,
@@ -171,7 +171,7 @@ def cpu_sample(wl, n_heat=8, n_groups=64) -> dict:
     else:
         op = O.Operator(wl.kind, masks=wl.masks)
     t0 = time.perf_counter()
-    x = op.adjoint(wl.y)
+    x = O.init_x(op, wl.y, wl.init)
     t_init = time.perf_counter() - t0
     t0 = time.perf_counter()
     anchors = O.build_exemplars(x, p, mc.max_corners, mc.nms, mc.corner_quality,
@@ -256,7 +256,7 @@ def _config(args, wl, n_exemplars):
     return {"workload": f"{wl.name}: {wl.kind.upper()} {h}x{w}x{c}, GAP-GLR {wl.max_iters} it, "
                         f"P={wl.match.patch_size}, K={wl.match.group_size}, "
                         f"max_corners={wl.match.max_corners}, "
-                        f"exemplar_stride={wl.match.exemplar_stride}",
+                        f"exemplar_stride={wl.match.exemplar_stride}, init={wl.init}",
             "exemplars": n_exemplars, "iters_per_step": wl.max_iters,
             "parallelism": f"exemplar-shard x{args.gpus}",
             "l2": _l2_note(wl, n_exemplars),
@@ -299,7 +299,7 @@ def run_b200(args, rank, world, local_rank):
     from paper_2301_03047_b200.solvers import GapRunner
     wl = workloads.make(args.config)
     h, w, c = wl.shape
-    cfg = G.SolverConfig(max_iters=wl.max_iters, match=wl.match)
+    cfg = wl.solver_config()
     op = workloads.operator_for(wl)
     runner = GapRunner(op, cfg, process_group=pg)
     y_d = runner.dop.upload_y(wl.y)

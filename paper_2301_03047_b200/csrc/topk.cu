@@ -893,8 +893,13 @@ int topk_cand_launch(const uint64_t* cand_d, const uint32_t* cnt_d, const uint16
   q.thr = thr_d;
   q.cap = cap;
   q.fallback = fallback_d;
-  q.b_cap = 16384;
-  // the list path has no bulk-copy ring: sA | sB (16384 ties) | hist | chosen
+  // tie buffer: 16384 where thousands of positions tie at the cut (few
+  // channels: a short score range), 4096 otherwise so that three CTAs share
+  // an SM (C2: 121 KB -> 73 KB per CTA; the selection is latency-bound --
+  // sorts, barriers, a single-warp walk -- and one resident CTA left the SM
+  // idle most of the time); more ties than that go to the dense path
+  q.b_cap = q.base.bins <= 2048 ? 16384 : 4096;
+  // the list path has no bulk-copy ring: sA | sB (ties) | hist | chosen
   smem = (size_t)q.base.a_cap * 8 + (size_t)q.b_cap * 4 + (size_t)q.base.bins * 4 +
          (size_t)K * 8 + 2 * topk::kSelB * 4 + 16;
   GLR_REQUIRE(smem <= 200 * 1024, GLR_ERR_UNSUPPORTED, "topk_cand: %zu bytes of shared memory",

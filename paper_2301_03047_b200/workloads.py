@@ -10,7 +10,7 @@ GPU path and the CPU oracle see identical values.
   C2  CACTI 1024x1024x24, GAP 50 it, P=8, K=64, 4096 exemplars
   C3  MRI 512x512 complex (re, im), Cartesian VD 25 %, GAP 40 it, P=8, K=48, 2048 ex.
       (897 corners + the interval-15 grid = 2048 anchors on the first refresh)
-  C4  MSFA 512x512x16, periodic 4x4, GAP 30 it, P=8, K=64, 2048 exemplars
+  C4  MSFA 512x512x16, periodic 4x4, GAP 30 it, P=8, K=64, 2048 exemplars, init="interp"
   C5  2048x2048x1 stage sweep (matching / top-K / WNNM / aggregation only)
 """
 
@@ -114,10 +114,18 @@ class Workload:
     max_iters: int
     match: MatchConfig
     noise: float
+    init: str = "adjoint"     # SolverConfig.init (solvers.py:47)
 
     @property
     def shape(self):
         return self.scene.shape
+
+    def solver_config(self, **overrides):
+        """The configuration's SolverConfig (iterations, matching, init)."""
+        from .solvers import SolverConfig
+        kw = dict(max_iters=self.max_iters, match=self.match, init=self.init)
+        kw.update(overrides)
+        return SolverConfig(**kw)
 
 
 def _masksum(x, masks):
@@ -164,7 +172,15 @@ def make(name: str, seed: int = 0) -> Workload:
         masks = msfa_pattern("periodic-4x4", bands, h, w)
         y = _masksum(scene, masks) + rng.normal(0.0, 0.005, (h, w, 1))
         mc = MatchConfig(patch_size=8, group_size=64, max_corners=2048, exemplar_stride=171)
-        return Workload(name, "msfa", scene, masks, y, 30, mc, 0.005)
+        # init="interp", as the reference's own MSFA runs (scripts/run_msfa_demo.py:38,
+        # tests/test_acceptance.py:231): from the adjoint the iterate never moves --
+        # every patch of a group shares the anchor's mosaic phase (the edge maps of a
+        # mosaic repeat with the 4x4 pattern), so a row of the group matrix is sampled
+        # in all of its columns or in none, M Wm keeps the unsampled rows at zero and
+        # the projection restores the sampled ones: x is a fixed point, bit for bit
+        # (measured: 30 identical iterates). The normalised-convolution start fills
+        # every band, and the solve then iterates like the reference's demo.
+        return Workload(name, "msfa", scene, masks, y, 30, mc, 0.005, init="interp")
     if name == "C5":
         h = w = 2048
         scene = _f32(blob_texture_image(h, w, rng)[:, :, None])

@@ -501,7 +501,7 @@ def gen_configs(names=("C1", "C3", "C4")):
       C1  all 30 iterations: every refresh's anchors + positions, the
           per-iteration residuals and the final clip(x, 0, 1)
       C3  first 10 of 40 iterations (complex operator, no-clip policy)
-      C4  first 10 of 30 iterations
+      C4  first 10 of 30 iterations (init="interp", the workload's setting)
 
     For C3/C4 the solve is stopped when iteration 10 begins (the iterate
     handed to regularize_dispatch = x after 10 iterations, with the
@@ -522,7 +522,7 @@ def gen_configs(names=("C1", "C3", "C4")):
             op = glr.msfa_operator(wl.masks)
         else:
             op = _complex_fourier_operator(wl.masks)
-        cfg = glr.SolverConfig(regularizer="glr", max_iters=wl.max_iters,
+        cfg = glr.SolverConfig(regularizer="glr", max_iters=wl.max_iters, init=wl.init,
                                match=glr.MatchConfig(patch_size=mc.patch_size,
                                                      group_size=mc.group_size,
                                                      max_corners=mc.max_corners,

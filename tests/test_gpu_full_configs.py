@@ -38,7 +38,7 @@ def _oracle_op(wl):
 def _run(wl, capture_after=None):
     """Device solve of the workload; returns (final x host, residuals,
     trace, x after `capture_after` iterations)."""
-    cfg = G.SolverConfig(max_iters=wl.max_iters, match=wl.match)
+    cfg = wl.solver_config()
     runner = GapRunner(workloads.operator_for(wl), cfg)
     y_d = runner.dop.upload_y(wl.y)
     trace, cap = [], {}

@@ -41,7 +41,7 @@ def main(name="C1"):
            "cores": os.cpu_count(), "numpy": np.__version__}
     # 1. the reference, unmodified
     op = glr.cacti_operator(wl.masks) if wl.kind == "cacti" else glr.msfa_operator(wl.masks)
-    cfg = glr.SolverConfig(regularizer="glr", max_iters=wl.max_iters,
+    cfg = glr.SolverConfig(regularizer="glr", max_iters=wl.max_iters, init=wl.init,
                            match=glr.MatchConfig(patch_size=mc.patch_size,
                                                  group_size=mc.group_size,
                                                  max_corners=mc.max_corners,
@@ -55,7 +55,7 @@ def main(name="C1"):
     t0 = time.perf_counter()
     O.gap_solve(O.Operator(wl.kind, masks=wl.masks), wl.y, wl.max_iters,
                 patch_size=mc.patch_size, group_size=mc.group_size,
-                max_corners=mc.max_corners, exemplar_stride=mc.exemplar_stride)
+                max_corners=mc.max_corners, exemplar_stride=mc.exemplar_stride, init=wl.init)
     t_port = time.perf_counter() - t0
     out["port_full_s"] = t_port
     out["port_full_iters_per_s"] = wl.max_iters / t_port

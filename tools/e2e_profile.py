@@ -11,7 +11,7 @@ from paper_2301_03047_b200 import _device as D, workloads  # noqa: E402
 from paper_2301_03047_b200.solvers import GapRunner  # noqa: E402
 
 wl = workloads.make(sys.argv[1] if len(sys.argv) > 1 else 'C2')
-cfg = G.SolverConfig(max_iters=wl.max_iters, match=wl.match)
+cfg = wl.solver_config()
 pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
 op = workloads.operator_for(wl)
 op.meta["masks"] = pin(op.meta["masks"])

@@ -6,7 +6,7 @@ import paper_2301_03047_b200 as G  # noqa: E402
 from paper_2301_03047_b200 import workloads  # noqa: E402
 from paper_2301_03047_b200.solvers import GapRunner  # noqa: E402
 wl = workloads.make(sys.argv[1] if len(sys.argv) > 1 else 'C2')
-cfg = G.SolverConfig(max_iters=wl.max_iters, match=wl.match)
+cfg = wl.solver_config()
 r = GapRunner(workloads.operator_for(wl), cfg)
 y = r.dop.upload_y(wl.y)
 x = r.xa

@@ -8,7 +8,7 @@ from paper_2301_03047_b200.solvers import GapRunner
 
 cfgname = sys.argv[1] if len(sys.argv) > 1 else 'C2'
 wl = workloads.make(cfgname)
-cfg = G.SolverConfig(max_iters=wl.max_iters, match=wl.match)
+cfg = wl.solver_config()
 r = GapRunner(workloads.operator_for(wl), cfg)
 y = r.dop.upload_y(wl.y)
 x = r.xa

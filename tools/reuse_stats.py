@@ -7,7 +7,7 @@ from paper_2301_03047_b200 import workloads
 from paper_2301_03047_b200.solvers import GapRunner
 for name in sys.argv[1:]:
     wl = workloads.make(name)
-    cfg = G.SolverConfig(max_iters=wl.max_iters, match=wl.match)
+    cfg = wl.solver_config()
     r = GapRunner(workloads.operator_for(wl), cfg)
     y = r.dop.upload_y(wl.y)
     trace = []

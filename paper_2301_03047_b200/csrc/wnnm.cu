@@ -27,7 +27,7 @@ namespace glr {
 namespace wn {
 constexpr int KMAX = 64;
 constexpr int LD = KMAX + 4;      // row stride of Wm in the apply kernel (== 4 mod 16)
-constexpr int GLD = KMAX + 2;     // row stride of G in the eigen kernel (pair reads: distinct banks)
+constexpr int GLD = KMAX + 1;     // row stride of G in the eigen kernel (odd, see eig_mm64)
 constexpr int VLD = KMAX + 1;     // row stride of V^T in the eigen kernel
 constexpr int GROWS = 32;         // rows of M per Gram tile
 constexpr int GRS = GROWS + 4;    // column stride of the Gram tiles (== 4 mod 16)
@@ -334,7 +334,13 @@ __device__ __forceinline__ void jrot(double c, double s, double& u, double& v) {
 // 64 x 64 x 64 fp64 product on DMMA for the eigen kernel: warp w owns tile
 // row w (rows 8w..8w+7) and all eight 8x8 tile columns; A(i, k) and B(k, j)
 // are read through the accessors. D element (8w + lane/4, 8tj + 2(lane%4) + e)
-// lands in d[tj][e].
+// lands in d[tj][e]. The four k of one MMA are 8 apart (k = kb + 8 (lane%4),
+// kb = 0..7, 32..39): with the ODD row strides of G and V^T a fragment load
+// then touches every bank exactly twice whether k indexes the row or the
+// column of the operand ((lane/4) S + 8 (lane%4) or 8 (lane%4) S + lane/4
+// mod 16 with S odd) -- consecutive k gave 4-way conflicts on the V^T reads
+// (ncu: 4x the ideal wavefronts, the products were ~45 % of the kernel's
+// shared-memory traffic on a one-sweep iteration).
 template <class FA, class FB>
 __device__ __forceinline__ void eig_mm64(FA A, FB B, double (&d)[8][2]) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -342,10 +348,11 @@ __device__ __forceinline__ void eig_mm64(FA A, FB B, double (&d)[8][2]) {
 #pragma unroll
   for (int t = 0; t < 8; ++t) d[t][0] = d[t][1] = 0.0;
 #pragma unroll 4
-  for (int k0 = 0; k0 < wn::KMAX; k0 += 4) {
-    const double fa = A(8 * w + ar, k0 + ak);
+  for (int kk = 0; kk < wn::KMAX / 4; ++kk) {
+    const int k = (kk & 7) + 32 * (kk >> 3) + 8 * ak;
+    const double fa = A(8 * w + ar, k);
 #pragma unroll
-    for (int t = 0; t < 8; ++t) dmma(d[t][0], d[t][1], fa, B(k0 + ak, 8 * t + ar));
+    for (int t = 0; t < 8; ++t) dmma(d[t][0], d[t][1], fa, B(k, 8 * t + ar));
   }
 }
 
@@ -485,7 +492,9 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
   } else {
     for (int t = tid; t < GSZ / 2; t += EIG_THREADS) {
       const int i = (2 * t) >> 6, j = (2 * t) & 63;
-      *reinterpret_cast<double2*>(&G[i * GLD + j]) = reinterpret_cast<const double2*>(Gg)[t];
+      const double2 v = reinterpret_cast<const double2*>(Gg)[t];
+      G[i * GLD + j] = v.x;
+      G[i * GLD + j + 1] = v.y;
     }
   }
   for (int t = tid; t < GSZ; t += EIG_THREADS) {
@@ -493,10 +502,11 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
     Vt[j * VLD + i] = warm ? vc[t] : (i == j ? 1.0 : 0.0);
   }
   __syncthreads();
-  if (tid == 0) {
-    double tr = 0.0;
-    for (int i = 0; i < K; ++i) tr += fabs(G[i * GLD + i]);
-    s_tiny = 1e-17 * tr;
+  if (warp == 0) {  // trace (entries beyond K are zero)
+    double tr = fabs(G[lane * GLD + lane]) + fabs(G[(lane + 32) * GLD + lane + 32]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    if (lane == 0) s_tiny = 1e-17 * tr;
   }
   if (warm) {
     // Warm start from this group's eigenvectors of a previous iteration:

@@ -836,7 +836,7 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
   if (tid == 0) atomicAdd(&g_eig_hist[warm ? 32 + sweep : sweep], 1u);
   if (tid == 0 && warm) atomicAdd(&g_res_hist[0], 1ull);
 #endif
-  if (vc) {
+  if (vc && !(warm && sweep == 0)) {  // no sweep from a warm start: the cached V is unchanged
     for (int t = tid; t < GSZ; t += EIG_THREADS) vc[t] = Vt[(t >> 6) * VLD + (t & 63)];
   }
   // ---- shrinkage weights (lowrank.py:58-64) ----
@@ -874,7 +874,7 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
         if (e * e > kRotTol * kRotTol * fabs(li * lj)) {
           const double d = li - lj;
           const double D = fabs(d) > 1e-4 * fmax(fabs(li), fabs(lj))
-                               ? (ratio[i] - ratio[j]) / d
+                               ? (ratio[i] - ratio[j]) * rcp_nr<2>(d)
                                : shrink_ratio_deriv(a, 0.5 * (li + lj));
           v = e * D;
         }

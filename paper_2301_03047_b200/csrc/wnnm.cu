@@ -294,6 +294,12 @@ __constant__ unsigned char kJacobiSched[21][6] = {
     {15, 54, 1, 2, 4, 24},  {30, 47, 1, 2, 4, 8},   {60, 29, 1, 2, 4, 8},
 };
 
+// round r = i ^ j of pair (i, j) -> its line (super-round) in kJacobiSched
+__constant__ unsigned char kRoundLine[64] = {
+    255, 0,  1,  6,  2,  12, 7,  5,  3,  11, 13, 14, 8,  6,  6,  18, 4,  3,  12, 16, 14, 10,
+    15,  12, 9,  3,  7,  17, 7,  20, 19, 14, 5,  20, 4,  11, 13, 10, 17, 5,  15, 2,  11, 9,
+    16,  2,  13, 19, 10, 19, 4,  9,  8,  1,  18, 1,  8,  18, 0,  0,  20, 17, 15, 16};
+
 // the four indices of quad B in super-round sr: t, t^a, t^b, t^a^b
 __device__ __forceinline__ void jacobi_quad(int sr, int B, int e[4]) {
   const int a = kJacobiSched[sr][0], b = kJacobiSched[sr][1];
@@ -561,6 +567,8 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
   __shared__ unsigned s_qrot[2];
   __shared__ unsigned char s_zb[8];  // per warp: zero-shrinkage flags of its 8 rows
   __shared__ unsigned char s_ub[8];  // per warp: rows too close to the shrinkage kink
+  __shared__ unsigned s_lines;       // super-rounds holding a pair the finish cannot absorb
+  __shared__ unsigned char s_rline[64];  // kRoundLine (lane-indexed reads: shared, not constant)
   __shared__ double s_kd[8];         // per warp: smallest kept diagonal entry
   __shared__ double s_rz[8];         // per warp: largest off-diagonal row sum of an exempt row
   __shared__ double lamv[KMAX];      // final diagonal (first-order finish)
@@ -592,6 +600,7 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
       }
     }
   };
+  if (tid < 64) s_rline[tid] = kRoundLine[tid];
   int sweep = 0;
   uint64_t zmask = 0;  // indices whose whole Gershgorin disc shrinks to zero
   bool early = false;  // stopped by the first-order finish (residue above kRotTol)
@@ -625,6 +634,7 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
         kd = fmin(kd, __shfl_xor_sync(0xffffffffu, kd, o));
         rz = fmax(rz, __shfl_xor_sync(0xffffffffu, rz, o));
       }
+      if (tid == 0) s_lines = 0u;
       if (lane == 0) {
         s_kd[warp] = kd;
         s_rz[warp] = rz;
@@ -656,6 +666,7 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
     // row near the kink, kept-kept pairs below kFinishTol, and every
     // kept-exempt pair below its own finish bound (see the pair test).
     bool need = false, block_finish = false;
+    unsigned lines = 0u;
     const double rot_over_rz2 = (kRotTol / RZ) * (kRotTol / RZ);  // +inf without exempt rows (unused then)
     for (int t = tid; t < GSZ; t += EIG_THREADS) {
       const int i = t >> 6, j = t & 63;
@@ -689,16 +700,32 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
 #endif
         need |= g2 > st2;
         block_finish |= g2 > fmax(st2, fin2);
+        // lines the sweep has to visit: pairs above half their finish bound
+        if (g2 > fmax(st2, 0.25 * fin2)) lines |= 1u << s_rline[i ^ j];
       }
     }
+    lines = __reduce_or_sync(0xffffffffu, lines);
+    if (lane == 0 && lines) atomicOr(&s_lines, lines);
     const bool any_need = __syncthreads_or(need);
     const bool any_block = __syncthreads_or(block_finish) || unsafe;
     if (!any_need || !any_block) {
       early = any_need;
       break;
     }
-    for (int sr = 0; sr < 21; ++sr, ++gsr) {
+    // Partial sweep: only the lines holding a pair above half its finish bound
+    // (rotations stay strict, so a visited quad is cleaned completely and the
+    // rest is left to the first-order finish); every line where the finish
+    // is ruled out (a kept row near the kink). From ~iteration 15 of C2 a
+    // group has 1-3 pairs above the finish tolerance -- a full 21-line sweep
+    // for them rotated all ~2000 pairs above the strict test.
+    const unsigned run_lines = unsafe ? 0x1FFFFFu : s_lines;
+    for (int sr = 0; sr < 21; ++sr) {
+      if (!((run_lines >> sr) & 1u)) continue;
       const int buf = gsr & 1;
+      ++gsr;
+#ifdef GLR_EIG_STATS
+      if (tid == 0 && warm) atomicAdd(&g_res_hist[7], 1ull);
+#endif
       if (warp == 0) {
         bool any = false;
         if (lane < 16) {

@@ -36,7 +36,7 @@ def on_iter(it, x):
     res = np.frombuffer(bytes(buf), dtype=np.uint64, count=8, offset=130 * 4)
     ng = max(int(res[0]), 1)
     rs = ' '.join(f'{int(v) / ng:.1f}' for v in res[1:7])
-    print(f"it {it:2d} pairs/group above 1e-4..1e-9: {rs}")
+    print(f"it {it:2d} pairs/group above 1e-4..1e-9: {rs}  lines/warm group {int(res[7]) / ng:.1f}")
     print(f"it {it:2d} mean sweeps {tot / max(h.sum(), 1):.2f} cold {cold} warm {warm} "
           f"kept-rank mean {rk @ np.arange(65) / max(rk.sum(), 1):.1f} p10/50/90/99 {q}")
 

@@ -719,6 +719,14 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
     // group has 1-3 pairs above the finish tolerance -- a full 21-line sweep
     // for them rotated all ~2000 pairs above the strict test.
     const unsigned run_lines = unsafe ? 0x1FFFFFu : s_lines;
+#ifdef GLR_EIG_QUADTOL  // dev A/B: rotate only pairs above GLR_EIG_QUADTOL x the finish tolerance
+                        // (measured on C2: 0.5 -> 175.7, 0.1 -> 179.6, strict -> 180.1 iters/s: the
+                        // unrotated residues pile up below the threshold and more lines get marked)
+    const double rtol2 = unsafe ? kRotTol * kRotTol
+                                : (GLR_EIG_QUADTOL * kFinishTol) * (GLR_EIG_QUADTOL * kFinishTol);
+#else
+    const double rtol2 = kRotTol * kRotTol;
+#endif
     for (int sr = 0; sr < 21; ++sr) {
       if (!((run_lines >> sr) & 1u)) continue;
       const int buf = gsr & 1;
@@ -763,9 +771,10 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
               // pairs only under the gap rule (kZGapTol)
               const double a2 = apq[h] * apq[h], dpq = app[h] - aqq[h];
               const double sc2 = fabs(app[h] * aqq[h]);
-              const double thr2 = (zp ^ zq) ? fmax(sc2, dpq * dpq) : sc2;
+              const double thr2 = (zp ^ zq) ? kRotTol * kRotTol * fmax(sc2, dpq * dpq)
+                                            : rtol2 * sc2;
               const bool rot =
-                  a2 > fmax(kRotTol * kRotTol * thr2, tiny2) &&
+                  a2 > fmax(thr2, tiny2) &&
                   !((zp & zq) && fabs(apq[h]) <= kZGapTol * (KD - fmax(app[h], aqq[h])));
               any |= rot;
               rotd[h] = rot;

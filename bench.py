@@ -320,6 +320,7 @@ def run_b200(args, rank, world, local_rank):
     if clocks:
         clocks.start()
     launches0 = N.launch_count
+    N.call("glr_eig_work", None, 1)  # clear the eigen step's work counters
     flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device="cuda") \
         if _needs_flush(wl, n_ex) else None
     ev = []
@@ -335,6 +336,10 @@ def run_b200(args, rank, world, local_rank):
     torch.cuda.synchronize()
     barrier()
     launches = N.launch_count - launches0  # fill_ is a torch kernel, not counted
+    import ctypes as _C
+    _ew = (_C.c_uint64 * 3)()
+    N.call("glr_eig_work", _C.addressof(_ew), 0)
+    eig_work = [int(v) for v in _ew]  # this rank's groups, super-rounds, first-order finishes
     ck = clocks.stop(local_rank) if clocks else None
     ms = sum(a.elapsed_time(b) for a, b in ev)
     if world > 1:
@@ -422,12 +427,34 @@ def run_b200(args, rank, world, local_rank):
             avg_s = d["ms"] / d["launches"] / 1e3
             ach = flops / avg_s / 1e12
             byts = 2.0 * m * k * 8 * d["units"] / d["launches"]
-            roof["wnnm_scatter"] = {"bound": "tensor", "achieved": ach, "peak": FP64_DMMA_PEAK,
-                                    "unit": "TFLOP/s", "frac": ach / FP64_DMMA_PEAK,
-                                    "peak_kind": "fp64-equivalent work vs the measured fp64 DMMA peak "
-                                                 "(Gram on DMMA, apply on int8 tcgen05 as an "
-                                                 "exact split-integer product)",
+            # The eigen step's work is data dependent and counted by the library
+            # (glr_eig_work): per group the warm-start products G' = Vp^T G Vp
+            # (2 x 2*64^3) and Wm = V diag V^T (one product, two with the
+            # first-order finish); per 4x4 block super-round the G update
+            # (256 blocks x 2 x 4^3 FMA) and the V update (16 quads x 64 rows x
+            # 16 FMA) = 98.3 kflop, nominal (blocks of unrotated quads are skipped).
+            eg = max(eig_work[0], 1)
+            sr_per_group = eig_work[1] / eg
+            fin_frac = eig_work[2] / eg
+            eig_flops_group = (3.0 + fin_frac) * 2.0 * 64 ** 3 + sr_per_group * 98304.0
+            eig_flops = eig_flops_group * d["units"] / d["launches"]
+            ach_all = (flops + eig_flops) / avg_s / 1e12
+            roof["wnnm_scatter"] = {"bound": "tensor", "achieved": ach_all,
+                                    "peak": FP64_DMMA_PEAK,
+                                    "unit": "TFLOP/s", "frac": ach_all / FP64_DMMA_PEAK,
+                                    "peak_kind": "fp64-equivalent work (Gram + eigen step + apply) vs "
+                                                 "the measured fp64 DMMA peak (Gram and the eigen "
+                                                 "step's products on DMMA, rotations on the fp64 "
+                                                 "pipe, apply on int8 tcgen05 as an exact "
+                                                 "split-integer product)",
                                     "avg_ms": d["ms"] / d["launches"],
+                                    "achieved_gram_apply_only": ach,
+                                    "frac_gram_apply_only": ach / FP64_DMMA_PEAK,
+                                    "eig": {"super_rounds_per_group": sr_per_group,
+                                            "sweeps_per_group": sr_per_group / 21.0,
+                                            "first_order_finish_frac": fin_frac,
+                                            "gflop_per_launch": eig_flops / 1e9,
+                                            "gram_apply_gflop_per_launch": flops / 1e9},
                                     "hbm_gbs": byts / avg_s / 1e9}
         if "topk" in kern:
             d = kern["topk"]
@@ -441,7 +468,7 @@ def run_b200(args, rank, world, local_rank):
         roofline = dict(roof.get(dominant, {})) if dominant else {}
         traffic = None
         prof = ROOT / "profiles" / "ncu_traffic.json"
-        if prof.exists() and dominant:
+        if prof.exists() and dominant and args.config == "C2":  # the capture is C2's
             traffic = json.loads(prof.read_text()).get(dominant)
         roofline["traffic"] = traffic
         roofline["kernel"] = dominant

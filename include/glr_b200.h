@@ -214,6 +214,15 @@ int glr_wnnm_scatter(const double* x_d, int H, int W, int C, int P, const int32_
                      double eps, int frac_bits, int64_t* acc_d, double* vcache_d, int warm,
                      const uint8_t* warm_flags_d, void* ws_d, size_t ws_bytes, void* stream);
 
+/* glr_eig_work: measurement aid (no reference counterpart). The eigen step of
+ * glr_wnnm_scatter / glr_wnnm (K <= 64) is iterative, so its work is data
+ * dependent; the library counts, per device, [0] groups processed, [1] 4x4
+ * block super-rounds run (one line of the Jacobi schedule = 1/21 of a sweep),
+ * [2] groups finished by the first-order correction. Copies the three
+ * counters to out3_host (host memory, may be NULL) after a device
+ * synchronisation and clears them when reset != 0.                          */
+int glr_eig_work(uint64_t* out3_host, int reset);
+
 /* glr_vcache_remap: carry cached eigenvectors across a matching refresh —
  * new group g in [new_lo, new_hi) whose anchor was old group i in
  * [old_lo, old_hi) gets vc_new[g] = vc_old[i] and flags[g] = 1 (else 0), for

@@ -41,6 +41,7 @@ SIGNATURES: dict[str, tuple] = {
     "glr_last_error": (C.c_char_p, []),
     "glr_version": (i32, []),
     "glr_device_info": (i32, [vp, vp, vp]),
+    "glr_eig_work": (i32, [vp, i32]),
     "glr_sobel": (i32, [vp, i32, i32, i32, vp, vp, vp]),
     "glr_edge_stack": (i32, [vp, vp, i32, i32, i32, f64, i32, i32, vp, vp, vp, vp]),
     "glr_stack_from_maps": (i32, [vp, i32, i32, i32, i32, vp, vp]),

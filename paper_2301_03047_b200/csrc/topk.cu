@@ -69,6 +69,80 @@ struct TopkParams {
   int32_t* stageN;
 };
 
+// Ascending bitonic sort of sz (a power of two >= 64) 64-bit keys in shared
+// memory with the keys held in registers: thread t owns a[EPT t .. EPT t + EPT),
+// so partner distances below EPT are register exchanges, those below 32 EPT
+// warp shuffles, and only the rest go through shared memory (sz = 2048,
+// EPT = 4: 10 of the 66 stages -- the plain version paid a block barrier for
+// every stage and was ~27 % of the dense top-K kernel on C4).
+template <class T, int EPT>
+__device__ __forceinline__ void bitonic_regs(T* a, int sz) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const bool act = tid < sz / EPT;  // whole warps: sz / EPT is a multiple of 32
+  const int i0 = tid * EPT;
+  T x[EPT];
+  if (act) {
+#pragma unroll
+    for (int q = 0; q < EPT; ++q) x[q] = a[i0 + q];
+  }
+  for (int k = 2; k <= sz; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < EPT) {
+        if (act) {
+#pragma unroll
+          for (int jc = 1; jc < EPT; jc <<= 1) {  // compile-time distances: x[] stays in registers
+            if (j != jc) continue;
+#pragma unroll
+            for (int q = 0; q < EPT; ++q) {
+              if ((q & jc) == 0) {
+                const int pq = q | jc;
+                const bool up = ((i0 + q) & k) == 0;
+                const T lo = x[q] < x[pq] ? x[q] : x[pq], hi = x[q] < x[pq] ? x[pq] : x[q];
+                x[q] = up ? lo : hi;
+                x[pq] = up ? hi : lo;
+              }
+            }
+          }
+        }
+      } else if (j < 32 * EPT) {
+        if (act) {
+          const int lm = j / EPT;
+          const bool lower = (lane & lm) == 0;
+#pragma unroll
+          for (int q = 0; q < EPT; ++q) {
+            const T y = __shfl_xor_sync(0xffffffffu, x[q], lm);
+            const bool up = ((i0 + q) & k) == 0;
+            const bool keep_min = lower == up;
+            x[q] = (x[q] < y) == keep_min ? x[q] : y;
+          }
+        }
+      } else {
+        if (act) {
+#pragma unroll
+          for (int q = 0; q < EPT; ++q) a[i0 + q] = x[q];
+        }
+        __syncthreads();
+        if (act) {
+#pragma unroll
+          for (int q = 0; q < EPT; ++q) {
+            const int i = i0 + q;
+            const T y = a[i ^ j];
+            const bool up = (i & k) == 0;
+            const bool keep_min = ((i & j) == 0) == up;
+            x[q] = (x[q] < y) == keep_min ? x[q] : y;
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+  if (act) {
+#pragma unroll
+    for (int q = 0; q < EPT; ++q) a[i0 + q] = x[q];
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ int cheb(int r0, int c0, int r1, int c1) {
   return max(abs(r0 - r1), abs(c0 - c1));
 }
@@ -85,6 +159,17 @@ __device__ __forceinline__ void topk_finish(const TopkParams& p, int n, int64_t 
   while (sz < cntA) sz <<= 1;
   for (int i = cntA + tid; i < sz; i += THREADS) sA[i] = ~0ull;
   __syncthreads();
+  // keys are distinct (the position is part of the key; the padding sorts last
+  // in any order), so every sorting network gives the same result
+  const int ept = sz / THREADS;
+  if (sz >= 64 && ept <= 8) {
+    switch (ept) {
+      case 0: case 1: bitonic_regs<uint64_t, 1>(sA, sz); break;
+      case 2: bitonic_regs<uint64_t, 2>(sA, sz); break;
+      case 4: bitonic_regs<uint64_t, 4>(sA, sz); break;
+      default: bitonic_regs<uint64_t, 8>(sA, sz); break;
+    }
+  } else
   for (int k = 2; k <= sz; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int i = tid; i < sz; i += THREADS) {
@@ -181,12 +266,73 @@ __device__ __forceinline__ void topk_cut(const int32_t* hist, int bins, int lo, 
   }
 }
 
+// The same cut found by the whole CTA: every warp sums 32-bin chunks of the
+// histogram (from the top down) into csum, warp 0 scans the chunk sums for
+// the chunk where the running count reaches `need` and finishes inside it
+// with topk_cut -- a handful of dependent steps instead of one per 32 bins
+// (C4: 4097 bins, the cut ~50-100 chunks from the top, two searches per row).
+// Called by all threads; res = {T, cntA, found} in shared memory, valid after
+// the closing barrier.
+__device__ __forceinline__ void topk_cut_block(const int32_t* hist, int bins, int lo, int need,
+                                               int* csum, int* res) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nchunks = (bins - lo + 31) / 32;
+  for (int c = warp; c < nchunks; c += nw) {
+    const int b = bins - 1 - 32 * c - lane;
+    const int v = __reduce_add_sync(0xffffffffu, b >= lo ? hist[b] : 0);
+    if (lane == 0) csum[c] = v;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    int running = 0, cstar = -1;
+    for (int c0 = 0; c0 < nchunks && cstar < 0; c0 += 32) {
+      const int v = c0 + lane < nchunks ? csum[c0 + lane] : 0;
+      int incl = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const unsigned hit = __ballot_sync(0xffffffffu, running + incl >= need);
+      if (hit) {
+        const int l = __ffs(hit) - 1;
+        cstar = c0 + l;
+        running += __shfl_sync(0xffffffffu, incl - v, l);
+      } else {
+        running += __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+    int T = 0, cntA = 0;
+    bool found = false;
+    if (cstar >= 0) {  // the cut lies inside chunk cstar: `need - running` more from its top
+      const int top = bins - 1 - 32 * cstar;
+      topk_cut(hist, top + 1, max(lo, top - 31), need - running, T, cntA, found);
+      cntA += running;
+    }
+    if (lane == 0) {
+      res[0] = T;
+      res[1] = cntA;
+      res[2] = found ? 1 : 0;
+    }
+  }
+  __syncthreads();
+}
+
 // ascending bitonic sort of n int32 in shared memory (padded with INT_MAX)
 __device__ __forceinline__ void bitonic_i32(int32_t* a, int n) {
   int sz = 1;
   while (sz < n) sz <<= 1;
   for (int i = n + threadIdx.x; i < sz; i += blockDim.x) a[i] = 0x7fffffff;
   __syncthreads();
+  const int ept = sz / (int)blockDim.x;
+  if (sz >= 64 && ept <= 8 && blockDim.x == topk::THREADS) {
+    switch (ept) {
+      case 0: case 1: bitonic_regs<int32_t, 1>(a, sz); break;
+      case 2: bitonic_regs<int32_t, 2>(a, sz); break;
+      case 4: bitonic_regs<int32_t, 4>(a, sz); break;
+      default: bitonic_regs<int32_t, 8>(a, sz); break;
+    }
+    return;
+  }
   for (int k = 2; k <= sz; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int i = threadIdx.x; i < sz; i += blockDim.x) {
@@ -215,6 +361,7 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
       smem + max(p.a_cap * 8 + p.b_cap * 4, topk::RING_STAGES * topk::RING_BYTES));  // bins
   int32_t* chosen = hist + p.bins;                                     // 2*K
   __shared__ int warp_tot[32];
+  __shared__ int s_csum[topk::MAX_BINS / 32], s_cut[3];
   __shared__ int s_total, s_T, s_cntA, s_baseA, s_baseB, s_na, s_nb, s_found, s_nl, s_next;
   const int BCAP = p.b_cap;
 
@@ -262,12 +409,10 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
         }
       }
       __syncthreads();
-      if (warp == 0) {
+      {
         const int64_t want = ((int64_t)kFloorSafety * need * ns * VEC + M - 1) / M;
-        int T, cntA;
-        bool found;
-        topk_cut(hist, p.bins, L0, want > 1 ? (int)want : 1, T, cntA, found);
-        if (lane == 0 && found) s_T = max(T, L0);
+        topk_cut_block(hist, p.bins, L0, want > 1 ? (int)want : 1, s_csum, s_cut);
+        if (tid == 0 && s_cut[2]) s_T = max(s_cut[0], L0);
       }
       __syncthreads();
       for (int b = L0 + tid; b < p.bins; b += THREADS) hist[b] = 0;
@@ -415,18 +560,16 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   __syncthreads();
 
   // 2. cut score T: walk bins from the top down to `lo`, 32 at a time
-  auto cut_search = [&](int lo) {
-    int T, cntA;
-    bool found;
-    topk_cut(hist, p.bins, lo, need, T, cntA, found);
-    if (lane == 0) {
-      s_T = T;
-      s_cntA = cntA;
-      s_found = found ? 1 : 0;
+  auto cut_search = [&](int lo) {  // block-wide
+    topk_cut_block(hist, p.bins, lo, need, s_csum, s_cut);
+    if (tid == 0) {
+      s_T = s_cut[0];
+      s_cntA = s_cut[1];
+      s_found = s_cut[2];
     }
+    __syncthreads();
   };
-  if (warp == 0) cut_search(L);
-  __syncthreads();
+  cut_search(L);
 #ifdef GLR_TOPK_STATS
   if (tid == 0) {
     atomicAdd(&g_topk_stats[0], 1u);
@@ -445,8 +588,7 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
     __syncthreads();
     hist_pass(0, L, false);
     __syncthreads();
-    if (warp == 0) cut_search(0);
-    __syncthreads();
+    cut_search(0);
   }
   const int T = s_T, cntA = s_cntA, capB = need - cntA;
 
@@ -657,15 +799,12 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_cand_kernel(TopkCandPar
   for (int i = tid; i < c; i += THREADS)
     atomicAdd(&hist[min((int)(list[i] >> 32), p.bins - 1)], 1);
   __syncthreads();
-  if (warp == 0) {
-    int T, cntA;
-    bool found;
-    topk_cut(hist, p.bins, L, need, T, cntA, found);
-    if ((tid & 31) == 0) {
-      s_T = T;
-      s_cntA = cntA;
-      s_found = found ? 1 : 0;
-    }
+  __shared__ int s_csum[topk::MAX_BINS / 32], s_cut[3];
+  topk_cut_block(hist, p.bins, L, need, s_csum, s_cut);
+  if (tid == 0) {
+    s_T = s_cut[0];
+    s_cntA = s_cut[1];
+    s_found = s_cut[2];
   }
   __syncthreads();
   const int T = s_T, cntA = s_cntA;

@@ -252,6 +252,13 @@ __global__ void __launch_bounds__(wn::GRAM_THREADS)
 // ---------------------------------------------------------------------------
 // K2: eigen-decomposition + shrinkage -> Wm (in place over G)
 
+// Work done by the eigen step since the last reset: [0] groups, [1] 4x4
+// block super-rounds (one line of the schedule: 16 quads x three rotation
+// rounds, the G and V updates), [2] groups finished by the first-order
+// correction (two extra 64^3 products). Read by glr_eig_work for the bench's
+// roofline (the O(K^3) eigen work is data dependent).
+__device__ unsigned long long g_eig_work[3];
+
 #ifdef GLR_EIG_STATS
 // dev statistics: groups per sweep count (cold [0, 32), warm [32, 64))
 __device__ unsigned int g_eig_hist[64];
@@ -868,6 +875,11 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
     __syncthreads();
   }
 
+  if (tid == 0) {
+    atomicAdd(&g_eig_work[0], 1ull);
+    if (gsr) atomicAdd(&g_eig_work[1], (unsigned long long)gsr);
+    if (early) atomicAdd(&g_eig_work[2], 1ull);
+  }
 #ifdef GLR_EIG_STATS
   if (tid == 0) atomicAdd(&g_eig_hist[warm ? 32 + sweep : sweep], 1u);
   if (tid == 0 && warm) atomicAdd(&g_res_hist[0], 1ull);
@@ -1835,6 +1847,19 @@ extern "C" int glr_debug_eig_hist(unsigned int* out, int reset) {
   return 0;
 }
 #endif
+
+extern "C" int glr_eig_work(uint64_t* out3_host, int reset) {
+  unsigned long long v[3] = {0, 0, 0};
+  if (out3_host) {
+    GLR_CUDA(cudaMemcpyFromSymbol(v, g_eig_work, sizeof(v)));
+    for (int i = 0; i < 3; ++i) out3_host[i] = v[i];
+  }
+  if (reset) {
+    const unsigned long long z[3] = {0, 0, 0};
+    GLR_CUDA(cudaMemcpyToSymbol(g_eig_work, z, sizeof(z)));
+  }
+  return GLR_OK;
+}
 
 extern "C" size_t glr_wnnm_workspace(int G, int K) {
   // K > 64 (generic path): G and V, K x K each, per group

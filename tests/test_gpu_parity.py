@@ -441,3 +441,49 @@ def test_wnnm_scatter_image_groups_vs_oracle(p, c, k, amp, rng):
     tol = cnt[..., None] * (2.0 ** -frac + 1e-9 * amp)
     err = np.abs(got - ref)
     assert (err <= tol + 1e-15).all(), float((err - tol).max())
+
+
+@pytest.mark.parametrize("sigmas", [(0.5, 0.45, 0.4), (0.1, 0.08, 0.06), (0.02, 0.015, 0.01),
+                                    (0.002, 0.0015, 0.001)])
+def test_wnnm_scatter_warm_start_across_kept_ranks(sigmas, rng):
+    """The warm path of glr_wnnm_scatter (cached eigenvectors, zero-shrinkage
+    exemption with its gap rule, partial sweeps, first-order finish) against
+    the SVD oracle on a smooth image + noise, at noise levels that keep from
+    3 to all 64 of the components (oracle ranks: ~3, ~8, ~44, ~63), with the
+    iterate perturbed between calls as in a solve (lowrank.py:46-65 per group, :68-87 aggregated)."""
+    from paper_2301_03047_b200 import _device as D, _native as N
+    from paper_2301_03047_b200.lowrank import frac_bits_for
+    t = D.torch()
+    h, w, c, p, k, n = 48, 52, 2, 8, 64, 24
+    yy, xx = np.mgrid[0:h, 0:w]
+    base = 0.5 + 0.3 * np.sin(yy / 5.0)[..., None] * np.cos(xx / 7.0)[..., None] \
+        + 0.1 * np.stack([np.sin(xx / 3.0), np.cos(yy / 4.0)], axis=2)
+    x = base + 0.02 * rng.standard_normal((h, w, c))
+    pos = np.stack([rng.integers(0, h - p + 1, (n, k)), rng.integers(0, w - p + 1, (n, k))],
+                   axis=2).astype(np.int32)
+    frac = frac_bits_for(1.5)
+    pos_d = D.i32(pos)
+    vc = D.zeros((n, 64, 64), t.float64)
+    ws = D.empty((N.query("glr_wnnm_workspace", n, k),), t.uint8)
+    cnt = np.zeros((h, w))
+    for g in range(n):
+        for r, q in pos[g]:
+            cnt[r:r + p, q:q + p] += 1
+    for step, sigma in enumerate(sigmas):
+        if step:
+            x = x + 2e-3 * rng.standard_normal((h, w, c))  # the iterate moves between calls
+        acc = D.zeros((h, w, c), t.int64)
+        x_d = D.f64(x)
+        N.call("glr_wnnm_scatter", x_d.data_ptr(), h, w, c, p, pos_d.data_ptr(), n, None, k,
+               float(sigma), 2.0 * np.sqrt(2.0), 1e-16, frac, acc.data_ptr(), vc.data_ptr(),
+               1 if step else 0, None, ws.data_ptr(), ws.numel(), D.stream())
+        got = D.host(acc).astype(np.float64) * 2.0 ** -frac
+        ref = np.zeros((h, w, c))
+        for g in range(n):
+            m = np.stack([x[r:r + p, q:q + p, :].ravel() for r, q in pos[g]], axis=1)
+            den = O.wnnm_prox(m, sigma)
+            for j, (r, q) in enumerate(pos[g]):
+                ref[r:r + p, q:q + p, :] += den[:, j].reshape(p, p, c)
+        tol = cnt[..., None] * (2.0 ** -frac + 1e-9)
+        err = np.abs(got - ref)
+        assert (err <= tol + 1e-15).all(), (step, sigma, float((err - tol).max()))

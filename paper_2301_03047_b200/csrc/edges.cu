@@ -584,22 +584,31 @@ constexpr uint8_t DEAD = 0, UNDEC = 1, PICKED = 2, REJECTED = 3;
 constexpr size_t kBatchBytes = (size_t)B * (2 * 4 + NBR * 2 + 1);
 }  // namespace nmsb
 
+// GBM: the bitmap of blocked pixels lives in global memory (zeroed by the
+// launcher; L2-resident, read with ld.cg and written with atomics, ordered by
+// the block barriers) for images whose bitmap exceeds shared memory (C5:
+// 2048^2 = 512 KB) -- those used to take the one-warp walk (19.4 ms per C5
+// pass with 16 K corners).
+template <bool GBM>
 __global__ void __launch_bounds__(nmsb::B) nms_batch_kernel(const int32_t* __restrict__ idx,
                                                            const int* __restrict__ n_cand, int H,
                                                            int W, int max_n, int R,
                                                            int32_t* __restrict__ out_rc,
-                                                           int32_t* __restrict__ out_n) {
+                                                           int32_t* __restrict__ out_n,
+                                                           uint32_t* gbm) {
   using namespace nmsb;
-  extern __shared__ uint32_t bm[];
+  extern __shared__ uint32_t bm_s[];
   const int nw = (int)(((int64_t)H * W + 31) / 32);
-  int32_t* br = reinterpret_cast<int32_t*>(bm + ((nw + 3) & ~3));
+  uint32_t* bm = GBM ? gbm : bm_s;
+  int32_t* br = reinterpret_cast<int32_t*>(bm_s + (GBM ? 0 : ((nw + 3) & ~3)));
   int32_t* bc = br + B;
   int16_t* nbr = reinterpret_cast<int16_t*>(bc + B);
   uint8_t* st = reinterpret_cast<uint8_t*>(nbr + B * NBR);
   __shared__ int warp_tot[32];
   __shared__ int s_total, s_picked, s_nb, s_pos;
   const int t = threadIdx.x;
-  for (int i = t; i < nw; i += B) bm[i] = 0u;
+  if constexpr (!GBM)
+    for (int i = t; i < nw; i += B) bm[i] = 0u;
   if (t == 0) {
     s_picked = 0;
     s_pos = 0;
@@ -618,7 +627,8 @@ __global__ void __launch_bounds__(nmsb::B) nms_batch_kernel(const int32_t* __res
       bool alive = false;
       if (i < total) {
         cand = idx[i];
-        alive = !((bm[cand >> 5] >> (cand & 31)) & 1u);
+        const uint32_t word = GBM ? __ldcg(bm + (cand >> 5)) : bm[cand >> 5];
+        alive = !((word >> (cand & 31)) & 1u);
       }
       const int e = block_excl_scan_1024(alive ? 1 : 0, warp_tot, &s_total);
       if (alive && nb0 + e < B) {
@@ -949,12 +959,20 @@ extern "C" int glr_corners(const double* resp_d, int H, int W, int max_n, int nm
   constexpr int kBatchSmemMax = 226 * 1024;  // 227 KB less the kernel's static shared memory
   if (batch_bytes <= (size_t)kBatchSmemMax && nms_radius <= 64) {
     {
-      const int s = ensure_smem_attr((const void*)nms_batch_kernel, kBatchSmemMax);
+      const int s = ensure_smem_attr((const void*)nms_batch_kernel<false>, kBatchSmemMax);
       if (s) return s;
     }
-    nms_batch_kernel<<<1, nmsb::B, batch_bytes, st>>>(v_out, n_cand, H, W, max_n, nms_radius,
-                                                      out_rc_d, out_n_d);
+    nms_batch_kernel<false><<<1, nmsb::B, batch_bytes, st>>>(v_out, n_cand, H, W, max_n,
+                                                             nms_radius, out_rc_d, out_n_d, nullptr);
     return check_launch("nms_batch_kernel");
+  }
+  if (nms_radius <= 64 && n >= 32) {
+    // bitmap in global memory (the `blocked` byte map's storage: n >= n / 8 bytes)
+    uint32_t* gbm = reinterpret_cast<uint32_t*>(blocked);
+    GLR_CUDA(cudaMemsetAsync(gbm, 0, bm_bytes, st));
+    nms_batch_kernel<true><<<1, nmsb::B, nmsb::kBatchBytes + 16, st>>>(
+        v_out, n_cand, H, W, max_n, nms_radius, out_rc_d, out_n_d, gbm);
+    return check_launch("nms_batch_kernel (global bitmap)");
   }
   if (bm_bytes <= (size_t)kNmsBitmapMaxBytes && nms_radius <= 15) {
     {

@@ -42,10 +42,12 @@ def test_edges_corners_anchors_bitwise_vs_golden():
 
 
 @pytest.mark.parametrize("shape,max_n,radius", [((300, 280, 3), 500, 4), ((1300, 1300, 1), 60, 4),
-                                              ((97, 131, 2), 5000, 2), ((64, 64, 1), 10, 17)])
+                                              ((97, 131, 2), 5000, 2), ((64, 64, 1), 10, 17),
+                                              ((2048, 1100, 1), 3000, 4)])
 def test_detect_corners_vs_oracle(shape, max_n, radius, rng):
-    """Greedy NMS (edges.py:100-128): the shared-memory bitmap walk, and the
-    global-memory fallback (over 1.6 MPixel or radius > 15), vs the oracle."""
+    """Greedy NMS (edges.py:100-128): the batched kernel with its bitmap in
+    shared memory, and in global memory for images beyond ~1.8 MPixel (the
+    2048 x 1100 case, C5's path), vs the oracle."""
     h, w, c = shape
     base = rng.random((h // 4 + 2, w // 4 + 2, c))
     x = np.kron(base, np.ones((4, 4, 1)))[:h, :w] + 0.05 * rng.random((h, w, c))

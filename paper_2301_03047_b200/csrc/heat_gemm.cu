@@ -28,19 +28,20 @@
 //     reference's row-major slice index, matching.py:177-178), rows padded
 //     to a multiple of 8 entries (glr_heat_stride) for 16-byte loads.
 //
-// Persistent, warp-specialised kernel (256 threads, one CTA per SM), launched
-// as clusters of CL CTAs that work on adjacent position tiles of the same
-// exemplar tile: each CTA loads its own A box and 1/CL of the B box,
-// multicast into every CTA's shared memory, so the L2 -> SM operand stream
-// (the bound) carries 16 + 28/CL KB per stage instead of 16 + 28 KB.
-//   warp 0 (one lane)  TMA producer, 5-stage smem ring (full/empty mbarriers;
-//                      a stage is refilled once ALL CTAs' MMAs released it);
-//   warp 1 (one lane)  tcgen05.mma issuer into one of two TMEM accumulators;
+// Persistent, warp-specialised kernel (one CTA per SM), launched as CTA pairs
+// (cta_group::2): the pair works on two adjacent 128-position tiles of the
+// same 224-exemplar tile, each CTA loads its own A box and half of the B box.
+//   warp 0 (one lane)  TMA producer, 7-stage smem ring (full/empty mbarriers;
+//                      a stage is refilled once the pair's MMAs released it);
+//   warp 1 (one lane)  pair leader: tcgen05.mma.cta_group::2 into one of two
+//                      TMEM accumulators;
 //   warp 2             owns the 512-column TMEM allocation;
-//   warps 4-7          also write the constant scale factors at start-up;
-//   warps 4-7          epilogue: tcgen05.ld -> u16 stores, then release the
-//                      accumulator, so tile i's epilogue overlaps tile i+1's
-//                      MMAs (accumulator handoff via tmem_full/tmem_empty).
+//   warps 4..          epilogue, 4 lane quadrants x EG column groups (EG = 4,
+//                      or 7 for tiles of one or two k-blocks): also write the
+//                      constant scale factors at start-up; tcgen05.ld -> u16
+//                      stores (dense map) or candidate-list appends (fused
+//                      top-K), then release the accumulator, so tile i's
+//                      epilogue overlaps tile i+1's MMAs (tmem_full/tmem_empty).
 #include <cstdio>
 #include <cudaTypedefs.h>
 
@@ -57,9 +58,13 @@ constexpr int BK = 128;      // bytes of K per stage (one 128B swizzle row = 256
 constexpr int UK = 32;       // bytes of K per tcgen05.mma kind::mxf4 (64 fp4)
 constexpr int STAGES = 7;
 constexpr int ACC = 2;       // TMEM accumulators (2 x 224 columns)
-constexpr int EPI_GROUPS = 3;  // column groups of the epilogue (chunks 0-2 | 3-4 | 5-6)
-constexpr int EPI_WARPS = 4 * EPI_GROUPS;
-constexpr int THREADS = 128 + 32 * EPI_WARPS;  // warps 4..: epilogue (lane quadrant w%4, group)
+// Epilogue warps: 4 lane quadrants x EG column groups (warps 4 ..), the kernel
+// is a template on EG. Four groups (chunks 0-1 | 2-3 | 4-5 | 6, 96 registers
+// per thread) by default; seven (one 32-column chunk per warp, 64 registers)
+// where a tile is one or two k-blocks and the epilogue IS the kernel (C5:
+// fused heat + top-K 42.8 / 36.7 / 34.3 ms with 3 / 4 / 7 groups; C2: 93.3 /
+// 92.6 / 93.8 ms per solve).
+constexpr int threads_for(int eg) { return 128 + 128 * eg; }
 constexpr int A_BYTES = BM * BK;
 constexpr int B_BYTES = BNH * BK;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -105,10 +110,12 @@ struct HeatParams {
   int cap;
 };
 
-__global__ void __launch_bounds__(heat::THREADS, 1)
+template <int EPI_GROUPS>
+__global__ void __launch_bounds__(heat::threads_for(EPI_GROUPS), 1)
     heat_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB, HeatParams p) {
   using namespace heat;
+  constexpr int EPI_WARPS = 4 * EPI_GROUPS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -247,68 +254,90 @@ __global__ void __launch_bounds__(heat::THREADS, 1)
       const bool v_ok = v < p.ow;
       GLR_DCHECK(ui < p.oh && u < p.oh * p.u_step + p.u0 && (int64_t)ui * p.ow < p.Mpad);
       uint16_t* out = p.heat + (size_t)ui * p.ow + v;
-#pragma unroll 1
-      for (int c = c_lo; c < c_hi; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * BN + c * 32), r);
-        tmem_ld_wait();
-        const int nb = n0 + c * 32;
-        if (p.cand) {
-          // candidate lists: a lane-local pre-test of the 32 scores against
-          // their exemplars' floors (float compares, floors broadcast from
-          // registers of the lane that owns the column); only a chunk in
-          // which some lane has a hit takes the per-column ballot and the
-          // warp-aggregated list appends
-          int tl = 0x10000;
+      if (p.cand) {
+        // Candidate lists, two sweeps over this warp's chunks so the slot
+        // reservations (one returning atomic per chunk, ~700 cycles) overlap
+        // the next chunks' work instead of sitting on each chunk's critical
+        // path (C5: ~3 hits per 32 x 32 chunk, the epilogue is the kernel).
+        // Sweep A per chunk: lane-local hit bits (float compares, the floors
+        // broadcast from the lane that owns the column), col_mask = their
+        // 32 x 32 bit transpose across the warp (five butterfly stages instead
+        // of a ballot per column; lane j: the lanes that hit column j), and
+        // ONE warp-wide atomic reserving every hit column's slots (lane j for
+        // column j). Sweep B re-reads the chunk from TMEM and appends.
+        const uint32_t pos = (uint32_t)(u * p.ow + v);
+        const unsigned lt = (1u << lane) - 1u;
+        const uint32_t trow = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * BN);
+        unsigned hits_c[MAXC], cmask_c[MAXC];
+        uint32_t base_c[MAXC];
 #pragma unroll
-          for (int k = 0; k < MAXC; ++k)
-            if (c == c_lo + k) tl = tl_c[k];
-          const uint32_t pos = (uint32_t)(u * p.ow + v);
-          const unsigned lt = (1u << lane) - 1u;
-          const float tlf = (float)tl;
-          bool any = false;
+        for (int k = 0; k < MAXC; ++k) {
+          hits_c[k] = 0;
+          cmask_c[k] = 0;
+          base_c[k] = 0;
+          const int c = c_lo + k;
+          if (c >= c_hi) continue;  // warp-uniform
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(trow + (uint32_t)(c * 32), r);
+          tmem_ld_wait();
+          const float tlf = (float)tl_c[k];
+          unsigned my_hits = 0;
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            any |= __uint_as_float(r[j]) >= __shfl_sync(0xffffffffu, tlf, j);
-          if (!__any_sync(0xffffffffu, any && v_ok)) continue;
-          // pass 1: per column j the warp's hit mask (lane j keeps it) and
-          // this lane's hit bits; then ONE warp-wide atomic reserves every
-          // column's slots at once (lane j for column j), so a chunk pays one
-          // atomic round trip instead of one per hit column
-          unsigned col_mask = 0, my_hits = 0;
+            my_hits |= (unsigned)(__uint_as_float(r[j]) >= __shfl_sync(0xffffffffu, tlf, j)) << j;
+          if (!v_ok) my_hits = 0;
+          if (!__any_sync(0xffffffffu, my_hits != 0)) continue;
+          unsigned col_mask = my_hits;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int sc = (int)__float2uint_rn(__uint_as_float(r[j]));
-            const int tj = __shfl_sync(0xffffffffu, tl, j);  // all lanes (no short-circuit)
-            const bool hit = v_ok && sc >= tj;
-            const unsigned m = __ballot_sync(0xffffffffu, hit);
-            if (lane == j) col_mask = m;
-            my_hits |= (unsigned)hit << j;
+          for (int sft = 16; sft >= 1; sft >>= 1) {
+            const unsigned M = sft == 16 ? 0x0000FFFFu : sft == 8 ? 0x00FF00FFu
+                             : sft == 4 ? 0x0F0F0F0Fu : sft == 2 ? 0x33333333u : 0x55555555u;
+            const unsigned y = __shfl_xor_sync(0xffffffffu, col_mask, sft);
+            col_mask = (lane & sft) ? ((col_mask & ~M) | ((y & ~M) >> sft))
+                                    : ((col_mask & M) | ((y & M) << sft));
           }
-          uint32_t base = 0;
-          if (col_mask) base = atomicAdd(&p.cnt[nb + lane], (uint32_t)__popc(col_mask));
-          const unsigned any_cols = __ballot_sync(0xffffffffu, col_mask != 0);
-          // pass 2: the appends of every hit column
+          hits_c[k] = my_hits;
+          cmask_c[k] = col_mask;
+          if (col_mask)
+            base_c[k] = atomicAdd(&p.cnt[n0 + c * 32 + lane], (uint32_t)__popc(col_mask));
+        }
+#pragma unroll
+        for (int k = 0; k < MAXC; ++k) {
+          const int c = c_lo + k;
+          if (c >= c_hi) continue;  // warp-uniform
+          const unsigned any_cols = __ballot_sync(0xffffffffu, cmask_c[k] != 0);
+          if (!any_cols) continue;
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(trow + (uint32_t)(c * 32), r);
+          tmem_ld_wait();
+          const int nb = n0 + c * 32;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             if (!((any_cols >> j) & 1u)) continue;  // warp-uniform
-            const unsigned m = __shfl_sync(0xffffffffu, col_mask, j);
-            const uint32_t b = __shfl_sync(0xffffffffu, base, j) + __popc(m & lt);
-            if (((my_hits >> j) & 1u) && b < (uint32_t)p.cap) {
+            const unsigned m = __shfl_sync(0xffffffffu, cmask_c[k], j);
+            const uint32_t b = __shfl_sync(0xffffffffu, base_c[k], j) + __popc(m & lt);
+            if (((hits_c[k] >> j) & 1u) && b < (uint32_t)p.cap) {
               const int sc = (int)__float2uint_rn(__uint_as_float(r[j]));
               p.cand[(size_t)(nb + j) * p.cap + b] = ((uint64_t)sc << 32) | pos;
             }
           }
-          continue;
         }
+      } else {
+#pragma unroll 1
+        for (int c = c_lo; c < c_hi; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * BN + c * 32), r);
+          tmem_ld_wait();
+          const int nb = n0 + c * 32;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int n = nb + j;
-          // streaming (evict-first) stores: the 8.5 GB map must not push the
-          // reused A/B operand tiles out of L2
-          if (v_ok && n < N)
-            __stcs(reinterpret_cast<unsigned short*>(out + (size_t)n * p.Mpad),
-                   (unsigned short)__float2uint_rn(__uint_as_float(r[j])));
+          for (int j = 0; j < 32; ++j) {
+            const int n = nb + j;
+            // streaming (evict-first) stores: the 8.5 GB map must not push the
+            // reused A/B operand tiles out of L2
+            if (v_ok && n < N)
+              __stcs(reinterpret_cast<unsigned short*>(out + (size_t)n * p.Mpad),
+                     (unsigned short)__float2uint_rn(__uint_as_float(r[j])));
+          }
         }
       }
       tc_fence_before();
@@ -485,6 +514,50 @@ struct HeatRows {
   bool pack = true;
 };
 
+template <int EG>
+static int launch_heat(const CUtensorMap& tmA, const CUtensorMap& tmB, const HeatParams& hp,
+                       int64_t pairs, cudaStream_t st) {
+  {
+    const int s = ensure_smem_attr((const void*)heat_gemm_kernel<EG>, heat::SMEM_BYTES);
+    if (s) return s;
+  }
+  const int sms = device_sms();
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(heat::threads_for(EG));
+  cfg.dynamicSmemBytes = heat::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // persistent: one CTA per SM, in clusters of two -- as many clusters as can
+  // be co-resident (the GPCs need not split into pairs evenly)
+  // (per device: the occupancy query depends on the device's GPC layout)
+  struct Q {
+    cudaLaunchConfig_t* cfg;
+    int sms;
+  } q{&cfg, sms};
+  const int max_clusters = cached_per_device(
+      (const void*)heat_gemm_kernel<EG>,
+      [](void* ctx) -> int {
+        Q* qq = static_cast<Q*>(ctx);
+        qq->cfg->gridDim = dim3(2 * (qq->sms / 2));
+        int mc = 0;
+        if (cudaOccupancyMaxActiveClusters(&mc, heat_gemm_kernel<EG>, qq->cfg) != cudaSuccess ||
+            mc < 1)
+          mc = qq->sms / 2;
+        cudaGetLastError();
+        return mc;
+      },
+      &q);
+  cfg.gridDim = dim3(2 * (unsigned)std::min<int64_t>(pairs, max_clusters));
+  GLR_CUDA(cudaLaunchKernelEx(&cfg, heat_gemm_kernel<EG>, tmA, tmB, hp));
+  return GLR_OK;
+}
+
 static int run_heat(const uint8_t* stack_d, int H, int W, int P, const HeatGeom& g,
                     const int32_t* anchors_d, int n_max, const int32_t* n_dev_d,
                     uint16_t* heat_d, uint8_t* bmat, uint16_t* thr_d, uint32_t* cnt_d,
@@ -540,48 +613,11 @@ static int run_heat(const uint8_t* stack_d, int H, int W, int P, const HeatGeom&
   hp.cnt = cnt_d;
   hp.cand = cand_d;
   hp.cap = cap;
-  {
-    const int s = ensure_smem_attr((const void*)heat_gemm_kernel, heat::SMEM_BYTES);
-    if (s) return s;
-  }
   const int64_t pairs = (int64_t)hp.oh * (hp.m_tiles_per_row / 2) * (n_pad / heat::BN);
   if (pairs == 0) return GLR_OK;  // pack only
   GLR_REQUIRE(pairs < (1ll << 31), GLR_ERR_UNSUPPORTED, "heat_map: too many tiles");
-  const int sms = device_sms();
-  cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(heat::THREADS);
-  cfg.dynamicSmemBytes = heat::SMEM_BYTES;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  // persistent: one CTA per SM, in clusters of two -- as many clusters as can
-  // be co-resident (the GPCs need not split into pairs evenly)
-  // (per device: the occupancy query depends on the device's GPC layout)
-  struct Q {
-    cudaLaunchConfig_t* cfg;
-    int sms;
-  } q{&cfg, sms};
-  const int max_clusters = cached_per_device(
-      (const void*)heat_gemm_kernel,
-      [](void* ctx) -> int {
-        Q* qq = static_cast<Q*>(ctx);
-        qq->cfg->gridDim = dim3(2 * (qq->sms / 2));
-        int mc = 0;
-        if (cudaOccupancyMaxActiveClusters(&mc, heat_gemm_kernel, qq->cfg) != cudaSuccess ||
-            mc < 1)
-          mc = qq->sms / 2;
-        cudaGetLastError();
-        return mc;
-      },
-      &q);
-  cfg.gridDim = dim3(2 * (unsigned)std::min<int64_t>(pairs, max_clusters));
-  GLR_CUDA(cudaLaunchKernelEx(&cfg, heat_gemm_kernel, tmA, tmB, hp));
-  return GLR_OK;
+  if (g.S * g.kchunks <= 2) return launch_heat<7>(tmA, tmB, hp, pairs, st);
+  return launch_heat<4>(tmA, tmB, hp, pairs, st);
 }
 
 extern "C" int glr_heat_map(const uint8_t* stack_d, int H, int W, int C, int P, int expand,

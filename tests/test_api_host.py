@@ -157,3 +157,46 @@ def test_divergence_guard():
     with pytest.raises(G.SolverDivergenceError, match="10x"):
         _check_divergence([1.0] + [20.0] * 20, y_norm=1.0)
     _check_divergence([1e-15] + [1e-9] * 20, y_norm=1.0)
+
+
+def test_workload_solver_configs():
+    """BASELINE configurations: iteration counts, group sizes and the MSFA
+    configuration's init (the reference's own MSFA runs start from "interp",
+    scripts/run_msfa_demo.py:38; from the adjoint the iterate is a fixed point)."""
+    from paper_2301_03047_b200 import workloads
+    expect = {"C1": (30, 64, "adjoint"), "C4": (30, 64, "interp")}
+    for name, (iters, k, init) in expect.items():
+        wl = workloads.make(name)
+        cfg = wl.solver_config()
+        assert (cfg.max_iters, cfg.match.group_size, cfg.init) == (iters, k, init)
+        assert wl.solver_config(max_iters=3).max_iters == 3
+
+
+def test_msfa_adjoint_start_is_a_fixed_point_of_the_reference_algorithm():
+    """Why C4 runs from init="interp": from the adjoint start the edge maps of
+    a (smooth) mosaic image repeat with the 4x4 pattern, every patch of a group
+    shares the anchor's mosaic phase, so a row of the group matrix is sampled
+    in all of its columns or in none: GAP-GLR iterations of the oracle
+    (solvers.py:284-308) leave the unsampled entries at zero (to rounding) and
+    return the sampled ones to the measurement."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "oracle"))
+    import glr_oracle as O
+    rng = np.random.default_rng(0)
+    h = w = 48
+    bands = 16
+    yy, xx = np.mgrid[0:h, 0:w]
+    scene = np.clip(0.5 + 0.2 * np.sin(yy / 9.0)[..., None] * np.cos(xx / 11.0)[..., None]
+                    + 0.1 * np.linspace(0, 1, bands)[None, None, :]
+                    + 0.01 * rng.standard_normal((h, w, bands)), 0, 1)
+    masks = O.msfa_pattern_periodic(4, h, w)
+    op = O.Operator("msfa", masks=masks)
+    y = O.masksum_forward(scene, masks)
+    x0 = np.clip(op.adjoint(y), 0.0, 1.0)
+    x2, _, _ = O.gap_solve(op, y, 2, patch_size=8, group_size=8, max_corners=16,
+                           exemplar_stride=4)
+    assert np.abs(x2[masks == 0]).max() < 1e-12  # (exactly 0 on the device path: M Wm of a zero row)
+    assert np.abs(x2 - x0).max() < 1e-12
+    # the normalised-convolution start fills every band
+    assert np.all(O.init_x(op, y, "interp") > 0.0)

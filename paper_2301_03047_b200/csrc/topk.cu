@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   int32_t* chosen = hist + p.bins;                                     // 2*K
   __shared__ int warp_tot[32];
   __shared__ int s_csum[topk::MAX_BINS / 32], s_cut[3];
-  __shared__ int s_total, s_T, s_cntA, s_baseA, s_baseB, s_na, s_nb, s_found, s_nl, s_next;
+  __shared__ int s_total, s_T, s_cntA, s_baseB, s_na, s_nb, s_found, s_nl, s_next, s_floor_est;
   const int BCAP = p.b_cap;
 
   const int n = blockIdx.x;
@@ -388,7 +388,10 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   // self-score). If the row has fewer than `need` positions >= L after all,
   // the exact fallback below adds the lower bins (second read).
   for (int b = L0 + tid; b < p.bins; b += THREADS) hist[b] = 0;
-  if (tid == 0) s_T = L0;
+  if (tid == 0) {
+    s_T = L0;
+    s_floor_est = 0;
+  }
   __syncthreads();
   {
     constexpr int SPT = 4, kFloorSafety = 4;
@@ -412,7 +415,12 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
       {
         const int64_t want = ((int64_t)kFloorSafety * need * ns * VEC + M - 1) / M;
         topk_cut_block(hist, p.bins, L0, want > 1 ? (int)want : 1, s_csum, s_cut);
-        if (tid == 0 && s_cut[2]) s_T = max(s_cut[0], L0);
+        if (tid == 0) {
+          if (s_cut[2]) s_T = max(s_cut[0], L0);
+          // the sample's estimate of how many positions share the floor's score
+          s_floor_est = (int)min((int64_t)hist[s_T] * (M / ((int64_t)ns * VEC) + 1),
+                                 (int64_t)0x7fffffff);
+        }
       }
       __syncthreads();
       for (int b = L0 + tid; b < p.bins; b += THREADS) hist[b] = 0;
@@ -420,6 +428,10 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   }
   __syncthreads();
   const int L = s_T;
+  // floor-level scores: recorded like the rest while they are few (the cut can
+  // then be served from the list even when it lands on the floor), counted
+  // only when the sample says thousands of positions share that score
+  const bool count_floor = s_floor_est > 8192;
   __shared__ __align__(8) uint64_t s_full[topk::RING_STAGES], s_empty[topk::RING_STAGES];
   if (tid == 0) {
     for (int r = 0; r < RING_STAGES; ++r) {
@@ -514,6 +526,14 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
     };
     if (tid == 0)
       for (int j = 0; j < min(RING_STAGES, nst); ++j) issue(j);
+    // Scores equal to the floor are only COUNTED (in a register, one shared
+    // atomic per warp at the end): on few-channel images tens of thousands of
+    // positions share the floor's score, and taking each through the shared
+    // histogram atomic, the list slot reservation and an 8-byte global store
+    // was most of the kernel (C3: ~207 K of 255 K entries per row). The list
+    // then holds the scores ABOVE the floor; if the cut lands on the floor
+    // itself, the ties are collected in index order with early exit below.
+    int floor_cnt = 0;
     for (int i = 0; i < nst; ++i) {
       const int sl = i % RING_STAGES;
       mbar_wait(&s_full[sl], (uint32_t)(i / RING_STAGES) & 1u);
@@ -532,7 +552,9 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
           val[j] = min((int)((j & 1) ? wv[j >> 1] >> 16 : wv[j >> 1] & 0xFFFFu), p.bins - 1);
-          if (base + j < Mi && val[j] >= lo) hit |= 1u << j;
+          const bool in = base + j < Mi;
+          if (in && val[j] >= lo + (count_floor ? 1 : 0)) hit |= 1u << j;
+          floor_cnt += count_floor && in && val[j] == lo;
         }
         if (!hit) continue;
         int off = atomicAdd(&s_nl, __popc(hit));
@@ -551,6 +573,9 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
         issue(i + RING_STAGES);
       }
     }
+    __syncwarp();
+    floor_cnt = __reduce_add_sync(0xffffffffu, floor_cnt);
+    if (lane == 0 && floor_cnt) atomicAdd(&hist[lo], floor_cnt);
   };
   if (list) {
     ring_pass(L);  // bulk-TMA-fed first pass (records the list)
@@ -582,11 +607,24 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
 #endif
   const bool first_pass_cut = s_found;
   if (!s_found) {
+    // The bins below L. Score 0 is not histogrammed: on sparse edge maps most
+    // of a row is zero (C3's phantom: ~200 K of 255 K positions, one shared
+    // bin = serialised atomics); its count is M minus everything else.
     for (int b = tid; b < L; b += THREADS) hist[b] = 0;
     __syncthreads();
-    if (tid == 0) s_next = 0;
+    if (tid == 0) {
+      s_next = 0;
+      s_total = 0;
+    }
     __syncthreads();
-    hist_pass(0, L, false);
+    if (L > 1) hist_pass(1, L, false);
+    __syncthreads();
+    int part = 0;
+    for (int b = 1 + tid; b < p.bins; b += THREADS) part += hist[b];
+    part = __reduce_add_sync(0xffffffffu, part);
+    if (lane == 0 && part) atomicAdd(&s_total, part);
+    __syncthreads();
+    if (tid == 0) hist[0] = (int)(M - (int64_t)s_total);
     __syncthreads();
     cut_search(0);
   }
@@ -595,8 +633,22 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   // 3. collect A = {score > T} (cntA < need entries) and the ties {score == T};
   //    unordered warp-aggregated appends when the ties fit the buffer (they are
   //    then sorted by index), else an ordered block-scan compaction.
-  if (list && first_pass_cut && s_nl <= p.scap && hist[T] <= BCAP) {
-    // the recorded list holds every score >= L >= ... >= T: no second row read
+  const bool list_ok = list && first_pass_cut && s_nl <= p.scap;
+  bool ties_done = false;  // false: the split path at the end collects the ties (and A if needed)
+  bool a_done = false;
+  if (list_ok && T == L && count_floor) {
+    // the cut is the floor: the list holds exactly A = {score > T}; the ties
+    // come from the ordered prefix scan below
+    const int c = s_nl;
+    for (int i = tid; i < c; i += THREADS) {
+      const uint64_t e = list[i];
+      sA[atomicAdd(&s_na, 1)] = ((uint64_t)(65535 - (int)(e >> 32)) << 32) | (uint32_t)e;
+    }
+    a_done = true;
+  } else if (list_ok && hist[T] <= BCAP) {
+    ties_done = a_done = true;
+    // the recorded list holds every score >= T (the floor's level too unless
+    // it was only counted, and then T > L): no second row read
     const int c = s_nl;
     for (int i = tid; i < c; i += THREADS) {
       const uint64_t e = list[i];
@@ -610,6 +662,7 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
     __syncthreads();
     if (!p.stageA) bitonic_i32(sB, s_nb);
   } else if (hist[T] <= BCAP) {
+    ties_done = a_done = true;
     constexpr int U = 4;  // 16-byte loads in flight per thread
     const unsigned lt = (1u << lane) - 1u;
     for (int64_t tile = 0; tile < M; tile += (int64_t)THREADS * VEC * U) {
@@ -654,48 +707,87 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
     __syncthreads();
     // ties in index order
     if (!p.stageA) bitonic_i32(sB, s_nb);
-  } else {
+  }
+  if (!ties_done) {
+    // The cut is the floor, or more ties than the buffer holds (few channels: tens of thousands of
+    // positions share the cut score). Only the ties need index order, and
+    // only the first capB of them: (a) A = {score > T} is collected unordered
+    // (it is sorted below anyway) in one streaming pass with the SWAR pre-test
+    // -- A is rare, so almost every 16-byte chunk is skipped; (b) the ties by
+    // an ordered block-scan compaction that stops as soon as capB are found,
+    // typically within the first tiles. (One ordered compaction of both used
+    // to walk the whole row with two block barriers per 4096 scores: ~125 us
+    // per C3 row.)
+    __syncthreads();
     if (tid == 0) {
-      s_baseA = 0;
       s_baseB = 0;
+      s_next = 0;
+      if (!a_done) s_na = 0;
     }
     __syncthreads();
+    if (cntA > 0 && !a_done) {
+      constexpr int U = 4;
+      const uint32_t kadd = (0x8000u - (uint32_t)(T + 1)) * 0x10001u;
+      const int Mi = (int)M;
+      const int nch = (Mi + VEC - 1) / VEC;
+      const uint4* rv = reinterpret_cast<const uint4*>(row);
+      const int ntl = (nch + 32 * U - 1) / (32 * U);
+      int wt = 0;
+      if (lane == 0) wt = atomicAdd(&s_next, 1);
+      wt = __shfl_sync(0xffffffffu, wt, 0);
+      while (wt < ntl) {
+        const int c0 = wt * 32 * U;
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int ci = c0 + u * 32 + lane;
+          v[u] = ci < nch ? rv[ci] : make_uint4(0, 0, 0, 0);
+        }
+        int wn = 0;
+        if (lane == 0) wn = atomicAdd(&s_next, 1);
+        wt = __shfl_sync(0xffffffffu, wn, 0);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t any = ((v[u].x + kadd) | (v[u].y + kadd) | (v[u].z + kadd) |
+                                (v[u].w + kadd)) & 0x80008000u;
+          if (!any) continue;
+          const int base = (c0 + u * 32 + lane) * VEC;
+          const uint32_t wv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) {
+            const int val = (int)((j & 1) ? wv[j >> 1] >> 16 : wv[j >> 1] & 0xFFFFu);
+            if (base + j < Mi && val > T)
+              sA[atomicAdd(&s_na, 1)] = ((uint64_t)(65535 - val) << 32) | (uint32_t)(base + j);
+          }
+        }
+      }
+    }
     for (int64_t tile = 0; tile < M; tile += (int64_t)THREADS * VEC) {
-      if (s_baseA >= cntA && s_baseB >= capB) break;  // block-uniform
+      if (s_baseB >= capB) break;  // block-uniform
       const int64_t base = tile + (int64_t)tid * VEC;
-      uint16_t s[VEC];
-      int a = 0, b = 0;
+      uint16_t sc[VEC];
+      int b = 0;
       if (base < M) {
         const uint4 v = *reinterpret_cast<const uint4*>(row + base);
         const uint16_t* sv = reinterpret_cast<const uint16_t*>(&v);
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
-          s[j] = (base + j < M) ? sv[j] : 0;
-          const bool valid = base + j < M;
-          a += valid && s[j] > T;
-          b += valid && s[j] == T;
+          sc[j] = (base + j < M) ? sv[j] : 0xFFFF;
+          b += sc[j] == T;
         }
       }
-      const int pre = block_excl_scan_1024(a | (b << 16), warp_tot, &s_total);
-      int ia = s_baseA + (pre & 0xFFFF);
-      int ib = s_baseB + (pre >> 16);
-      if (a | b) {
+      int ib = s_baseB + block_excl_scan_1024(b, warp_tot, &s_total);
+      if (b) {
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
-          if (base + j >= M) break;
-          if (s[j] > T) {
-            sA[ia++] = ((uint64_t)(65535 - s[j]) << 32) | (uint32_t)(base + j);
-          } else if (s[j] == T) {
+          if (sc[j] == T) {
             if (ib < capB) sB[ib] = (int32_t)(base + j);
             ++ib;
           }
         }
       }
       __syncthreads();
-      if (tid == 0) {
-        s_baseA += s_total & 0xFFFF;
-        s_baseB += s_total >> 16;
-      }
+      if (tid == 0) s_baseB += s_total;
       __syncthreads();
     }
   }
@@ -703,7 +795,7 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   if (p.stageA) {
     // hand A and the ties over to topk_select_kernel (ordered-compaction
     // path: the first capB ties in index order; otherwise all, unsorted)
-    const int nb = hist[T] <= BCAP ? s_nb : min(s_baseB, capB);
+    const int nb = ties_done ? s_nb : min(s_baseB, capB);
     uint64_t* ga = p.stageA + (size_t)n * p.a_cap;
     int32_t* gb = p.stageB + (size_t)n * BCAP;
     for (int i = tid; i < cntA; i += THREADS) ga[i] = sA[i];

@@ -50,6 +50,15 @@
 
 namespace glr {
 
+// Candidate floor of the fused path: the sampled pre-pass aims at this many
+// pool-sizes of positions above the floor (measured 8 / 4 / 2: C2 92.2 / 91.0 /
+// 90.4 ms of fused matching per solve, C5 34.4 / 33.4 / 33.0 ms per pass, no
+// exemplar handed to the dense path at any of them; 4 keeps a 4x margin
+// against a sample that overestimates the count).
+#ifndef GLR_HEAT_WANT_POOLS
+#define GLR_HEAT_WANT_POOLS 4
+#endif
+
 namespace heat {
 constexpr int BM = 128;      // positions per CTA tile (the pair's UMMA M = 256)
 constexpr int BN = 224;      // exemplars per pair tile (UMMA N)
@@ -719,10 +728,10 @@ extern "C" int glr_heat_topk(const uint8_t* stack_d, int H, int W, int C, int P,
       const int ns = oh_eff * g.ow;
       const int64_t M = (int64_t)g.oh * g.ow;
       const int pool = K * (2 * sep + 1) * (2 * sep + 1) + 1;
-      // aim at ~8 pool-sizes above the floor: the integer scores tie heavily
+      // aim at a few pool-sizes above the floor: the integer scores tie heavily
       // at the cut, and a floor estimated too high sends the exemplar to the
       // dense fallback
-      const int want = (int)std::max<int64_t>(1, (8 * (int64_t)pool * ns + M - 1) / M);
+      const int want = (int)std::max<int64_t>(1, (GLR_HEAT_WANT_POOLS * (int64_t)pool * ns + M - 1) / M);
       const int smem = bins * (int)sizeof(int);
       {
         const int s_ = ensure_smem_attr((const void*)sample_thr_kernel, smem);

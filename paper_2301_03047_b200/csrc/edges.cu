@@ -627,6 +627,7 @@ __global__ void __launch_bounds__(nmsb::B) nms_batch_kernel(const int32_t* __res
       bool alive = false;
       if (i < total) {
         cand = idx[i];
+        GLR_DCHECK(cand >= 0 && (int64_t)cand < (int64_t)H * W);
         const uint32_t word = GBM ? __ldcg(bm + (cand >> 5)) : bm[cand >> 5];
         alive = !((word >> (cand & 31)) & 1u);
       }

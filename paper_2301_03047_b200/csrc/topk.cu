@@ -642,7 +642,9 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
     const int c = s_nl;
     for (int i = tid; i < c; i += THREADS) {
       const uint64_t e = list[i];
-      sA[atomicAdd(&s_na, 1)] = ((uint64_t)(65535 - (int)(e >> 32)) << 32) | (uint32_t)e;
+      const int ia = atomicAdd(&s_na, 1);
+      GLR_DCHECK(ia < p.a_cap && (int)(e >> 32) > T);
+      sA[ia] = ((uint64_t)(65535 - (int)(e >> 32)) << 32) | (uint32_t)e;
     }
     a_done = true;
   } else if (list_ok && hist[T] <= BCAP) {
@@ -756,8 +758,11 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
 #pragma unroll
           for (int j = 0; j < VEC; ++j) {
             const int val = (int)((j & 1) ? wv[j >> 1] >> 16 : wv[j >> 1] & 0xFFFFu);
-            if (base + j < Mi && val > T)
-              sA[atomicAdd(&s_na, 1)] = ((uint64_t)(65535 - val) << 32) | (uint32_t)(base + j);
+            if (base + j < Mi && val > T) {
+              const int ia = atomicAdd(&s_na, 1);
+              GLR_DCHECK(ia < p.a_cap && ia < cntA);
+              sA[ia] = ((uint64_t)(65535 - val) << 32) | (uint32_t)(base + j);
+            }
           }
         }
       }
@@ -781,6 +786,7 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
           if (sc[j] == T) {
+            GLR_DCHECK(capB <= BCAP);
             if (ib < capB) sB[ib] = (int32_t)(base + j);
             ++ib;
           }

@@ -93,6 +93,10 @@ struct GroupSrc {
   int H;               // image groups: image rows (bounds checks of the checked build)
   int64_t rs;
   int m, K;
+  // rows 2q, 2q+1 of every column are 16 contiguous, 16-byte aligned bytes
+  // (image groups: even C; explicit groups: even m): the tile fills then
+  // move two rows per cp.async
+  int vec2;
 };
 
 template <bool IMG>
@@ -113,6 +117,26 @@ template <int NWARPS>
 __device__ __forceinline__ void fill_tile(double* Tt, const GroupSrc& s, const long long* cbase,
                                           int r0, int R, int RS) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (s.vec2 && R == 32) {
+    // 16 lanes x 2 rows down the tile, the two half-warps on alternating
+    // columns: half the cp.async instructions and shared-memory wavefronts of
+    // the 8-byte fill (ncu: the fill was a third of the Gram kernel's stall
+    // samples beside an 80 % busy DMMA pipe)
+    const int rr = 2 * (lane & 15), r = r0 + rr;
+    const bool rok = r < s.m;  // m even: the pair is in or out together
+    const int64_t off = rok ? (int64_t)(r / s.PC) * s.rs + (r % s.PC) : 0;
+#pragma unroll 4
+    for (int j = 2 * warp + (lane >> 4); j < wn::KMAX; j += 2 * NWARPS) {
+      if (rok && j < s.K) {
+        cp_async16(&Tt[j * RS + rr], s.src + cbase[j] + off);
+      } else {
+        Tt[j * RS + rr] = 0.0;
+        Tt[j * RS + rr + 1] = 0.0;
+      }
+    }
+    cp_async_commit();
+    return;
+  }
   for (int rr = lane; rr < R; rr += 32) {
     const int r = r0 + rr;
     const bool rok = r < s.m;
@@ -1885,6 +1909,7 @@ extern "C" int glr_wnnm(const double* groups_d, int G, int m, int K, double sigm
   s.rs = 0;
   s.m = m;
   s.K = K;
+  s.vec2 = (m % 2 == 0) && (reinterpret_cast<uintptr_t>(groups_d) % 16 == 0);
   EigArgs ea{};
   ea.K = K;
   ea.sigma = sigma;
@@ -1922,6 +1947,7 @@ extern "C" int glr_wnnm_scatter(const double* x_d, int H, int W, int C, int P,
   s.rs = (int64_t)W * C;
   s.m = P * P * C;
   s.K = K;
+  s.vec2 = (C % 2 == 0) && (reinterpret_cast<uintptr_t>(x_d) % 16 == 0);
   EigArgs ea{};
   ea.K = K;
   ea.sigma = sigma;

@@ -373,28 +373,42 @@ __device__ __forceinline__ void jrot(double c, double s, double& u, double& v) {
   v = nv;
 }
 
-// 64 x 64 x 64 fp64 product on DMMA for the eigen kernel: warp w owns tile
-// row w (rows 8w..8w+7) and all eight 8x8 tile columns; A(i, k) and B(k, j)
-// are read through the accessors. D element (8w + lane/4, 8tj + 2(lane%4) + e)
-// lands in d[tj][e]. The four k of one MMA are 8 apart (k = kb + 8 (lane%4),
+// 64 x 64 x 64 fp64 product on DMMA for the eigen kernel; A(i, k) and B(k, j)
+// are read through the accessors. The four k of one MMA are 8 apart (k = kb + 8 (lane%4),
 // kb = 0..7, 32..39): with the ODD row strides of G and V^T a fragment load
 // then touches every bank exactly twice whether k indexes the row or the
 // column of the operand ((lane/4) S + 8 (lane%4) or 8 (lane%4) S + lane/4
 // mod 16 with S odd) -- consecutive k gave 4-way conflicts on the V^T reads
 // (ncu: 4x the ideal wavefronts, the products were ~45 % of the kernel's
 // shared-memory traffic on a one-sweep iteration).
+// Warp w owns a 16 x 32 block of D: row tiles 2 (w / 2), 2 (w / 2) + 1 and
+// column tiles 4 (w % 2) .. + 3, so a k-step loads 2 A and 4 B fragments for
+// its 8 DMMAs (one A and 8 B fragments with a 8 x 64 strip per warp: a third
+// more shared-memory wavefronts for the same math). Slot t of d = (row tile
+// t / 4, column tile t % 4); mm64_row / mm64_col give an element's indices.
+__device__ __forceinline__ int mm64_row(int warp, int t, int ar) {
+  return 16 * (warp >> 1) + 8 * (t >> 2) + ar;
+}
+__device__ __forceinline__ int mm64_col(int warp, int t, int ak) {  // + e for the second value
+  return 8 * (4 * (warp & 1) + (t & 3)) + 2 * ak;
+}
 template <class FA, class FB>
 __device__ __forceinline__ void eig_mm64(FA A, FB B, double (&d)[8][2]) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int ar = lane >> 2, ak = lane & 3;
+  const int r0 = 16 * (w >> 1), c0 = 32 * (w & 1);
 #pragma unroll
   for (int t = 0; t < 8; ++t) d[t][0] = d[t][1] = 0.0;
 #pragma unroll 4
   for (int kk = 0; kk < wn::KMAX / 4; ++kk) {
     const int k = (kk & 7) + 32 * (kk >> 3) + 8 * ak;
-    const double fa = A(8 * w + ar, k);
+    const double fa0 = A(r0 + ar, k), fa1 = A(r0 + 8 + ar, k);
 #pragma unroll
-    for (int t = 0; t < 8; ++t) dmma(d[t][0], d[t][1], fa, B(k, 8 * t + ar));
+    for (int c = 0; c < 4; ++c) {
+      const double fb = B(k, c0 + 8 * c + ar);
+      dmma(d[c][0], d[c][1], fa0, fb);
+      dmma(d[4 + c][0], d[4 + c][1], fa1, fb);
+    }
   }
 }
 
@@ -563,7 +577,8 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
 #pragma unroll
     for (int t = 0; t < 8; ++t)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) G[(8 * warp + ar) * GLD + 8 * t + 2 * ak + e] = d[t][e];
+      for (int e = 0; e < 2; ++e)
+        G[mm64_row(warp, t, ar) * GLD + mm64_col(warp, t, ak) + e] = d[t][e];
     __syncthreads();
     eig_mm64([&](int i, int k) { return Vt[i * VLD + k]; },
              [&](int k, int j) { return G[k * GLD + j]; }, d);
@@ -571,7 +586,8 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
 #pragma unroll
     for (int t = 0; t < 8; ++t)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) G[(8 * warp + ar) * GLD + 8 * t + 2 * ak + e] = d[t][e];
+      for (int e = 0; e < 2; ++e)
+        G[mm64_row(warp, t, ar) * GLD + mm64_col(warp, t, ak) + e] = d[t][e];
     __syncthreads();
     // symmetrise (the product is symmetric up to rounding)
     for (int t = tid; t < GSZ; t += EIG_THREADS) {
@@ -962,7 +978,8 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
 #pragma unroll
       for (int t = 0; t < 8; ++t)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) G[(8 * warp + ar) * GLD + 8 * t + 2 * ak + e] = o[t][e];
+        for (int e = 0; e < 2; ++e)
+          G[mm64_row(warp, t, ar) * GLD + mm64_col(warp, t, ak) + e] = o[t][e];
     }
     __syncthreads();
     eig_mm64([&](int i, int k) { return G[i * GLD + k]; },
@@ -972,7 +989,7 @@ __device__ __forceinline__ void eig_group(const EigArgs& a, const int g, double*
     const int ar = lane >> 2, ak = lane & 3;
 #pragma unroll
     for (int t = 0; t < 8; ++t)
-      *reinterpret_cast<double2*>(&Gg[(8 * warp + ar) * KMAX + 8 * t + 2 * ak]) =
+      *reinterpret_cast<double2*>(&Gg[mm64_row(warp, t, ar) * KMAX + mm64_col(warp, t, ak)]) =
           make_double2(o[t][0], o[t][1]);
   }
   if (a.wmax) {

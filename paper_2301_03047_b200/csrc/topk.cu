@@ -36,6 +36,27 @@ constexpr int RING_STAGES = 3;
 constexpr int RING_BYTES = 16384;  // 32 bytes per thread per slice
 }  // namespace topk
 
+#ifdef GLR_TOPK_PHASES  // dev: per-phase cycles of topk_kernel (thread 0 of every CTA)
+__device__ unsigned long long g_topk_phase[8];
+#define TK_MARK(i)                                                        \
+  do {                                                                    \
+    if (threadIdx.x == 0) {                                               \
+      const long long now_ = clock64();                                   \
+      atomicAdd(&g_topk_phase[i], (unsigned long long)(now_ - tk_t0_));   \
+      tk_t0_ = now_;                                                      \
+    }                                                                     \
+  } while (0)
+extern "C" int glr_debug_topk_phases(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_topk_phase, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_topk_phase, z, sizeof(z));
+  }
+  return 0;
+}
+#else
+#define TK_MARK(i)
+#endif
 #ifdef GLR_TOPK_STATS
 __device__ unsigned int g_topk_stats[4];  // rows, fallbacks below L, sum / max of count(>= L)
 __device__ unsigned int g_cand_stats[6];  // list path: rows, overflow, short, ties, sum / max count
@@ -154,6 +175,9 @@ __device__ __forceinline__ void topk_finish(const TopkParams& p, int n, int64_t 
                                             int32_t* chosen) {
   using namespace topk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef GLR_TOPK_PHASES
+  long long tk_t0_ = clock64();
+#endif
   // 4. bitonic sort of A (padded to the next power of two >= cntA)
   int sz = 1;
   while (sz < cntA) sz <<= 1;
@@ -187,6 +211,7 @@ __device__ __forceinline__ void topk_finish(const TopkParams& p, int n, int64_t 
     }
   }
 
+  TK_MARK(4);
   // 5. greedy walk (warp 0)
   if (warp == 0) {
     const int ar = p.anchors[2 * n], ac = p.anchors[2 * n + 1];
@@ -235,6 +260,7 @@ __device__ __forceinline__ void topk_finish(const TopkParams& p, int n, int64_t 
       out[2 * t + 1] = t < nch ? chosen[2 * t + 1] : ac;
     }
     if (lane == 0) p.padded[n] = p.K - nch;
+    TK_MARK(5);
   }
 }
 
@@ -372,6 +398,9 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   const uint16_t* row = p.heat + (size_t)n * p.stride;
   const int64_t M = p.M;
   const int need = (int)(M < (int64_t)p.pool ? M : (int64_t)p.pool);
+#ifdef GLR_TOPK_PHASES
+  long long tk_t0_ = clock64();
+#endif
 
   // 1. histogram of the scores >= L, L = a quarter of the anchor's own score
   //    (for a heat map the row maximum: |E_u ∩ E_n| <= |E_n|), so the bulk of
@@ -432,6 +461,7 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   // then be served from the list even when it lands on the floor), counted
   // only when the sample says thousands of positions share that score
   const bool count_floor = s_floor_est > 8192;
+  TK_MARK(0);
   __shared__ __align__(8) uint64_t s_full[topk::RING_STAGES], s_empty[topk::RING_STAGES];
   if (tid == 0) {
     for (int r = 0; r < RING_STAGES; ++r) {
@@ -584,6 +614,7 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
   }
   __syncthreads();
 
+  TK_MARK(1);
   // 2. cut score T: walk bins from the top down to `lo`, 32 at a time
   auto cut_search = [&](int lo) {  // block-wide
     topk_cut_block(hist, p.bins, lo, need, s_csum, s_cut);
@@ -629,6 +660,7 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
     cut_search(0);
   }
   const int T = s_T, cntA = s_cntA, capB = need - cntA;
+  TK_MARK(2);
 
   // 3. collect A = {score > T} (cntA < need entries) and the ties {score == T};
   //    unordered warp-aggregated appends when the ties fit the buffer (they are
@@ -812,6 +844,8 @@ __global__ void __launch_bounds__(topk::THREADS, 3) topk_kernel(TopkParams p) {
     }
     return;
   }
+  __syncthreads();
+  TK_MARK(3);
   topk_finish(p, n, M, need, cntA, sA, sB, chosen);
 }
 

@@ -259,7 +259,7 @@ def _config(args, wl, n_exemplars):
                         f"exemplar_stride={wl.match.exemplar_stride}, init={wl.init}",
             "exemplars": n_exemplars, "iters_per_step": wl.max_iters,
             "parallelism": f"exemplar-shard x{args.gpus}",
-            "l2": _l2_note(wl, n_exemplars),
+            "l2": _l2_note(wl, n_exemplars, _fused_auto(wl)),
             "seed": 0}
 
 
@@ -278,8 +278,21 @@ def _needs_flush(wl, n_exemplars):
     return hb + 4 * xb < 2 * L2_BYTES
 
 
-def _l2_note(wl, n_exemplars):
+def _fused_auto(wl) -> bool:
+    """GlrEngine's automatic choice of the fused heat map + top-K (engine.py:
+    the dense u16 map would exceed 4 GB)."""
+    mc = wl.match
+    h, w, _ = wl.shape
+    p, g = mc.patch_size, 3 * mc.exemplar_stride
+    n_est = mc.max_corners + ((h - p) // g + 1) * ((w - p) // g + 1)
+    return n_est * (h - p + 1) * (w - p + 1) * 2 > (4 << 30)
+
+
+def _l2_note(wl, n_exemplars, fused=False):
     xb, hb = _working_set(wl, n_exemplars)
+    if fused:  # no dense heat map: candidate lists (glr_heat_topk)
+        return (f"inputs > L2 (x {xb / 1e6:.0f} MB per array; fused matching: candidate lists "
+                f"instead of a {hb / 1e9:.2f} GB dense heat map per refresh)")
     if _needs_flush(wl, n_exemplars):
         return (f"L2 flushed between timed steps (256 MB write outside the per-step events); "
                 f"x {xb / 1e6:.0f} MB, heat map {hb / 1e6:.0f} MB per refresh")

@@ -152,7 +152,7 @@ KERNELS_PER_CALL = {
     "glr_scatter_add_f64": 1, "glr_normalize": 1, "glr_masksum_forward": 1,
     "glr_masksum_adjoint": 1, "glr_gap_masksum": 2, "glr_fourier_forward": 4,
     "glr_fourier_adjoint": 4, "glr_gap_fourier": 11, "glr_sq_err": 2, "glr_vcache_remap": 3,
-    "glr_lincomb": 1, "glr_interp_msfa": 3, "glr_interp_cacti": 1, "glr_heat_topk": 4, "glr_ssim": 3,
+    "glr_lincomb": 1, "glr_interp_msfa": 3, "glr_interp_cacti": 1, "glr_heat_topk": 6, "glr_ssim": 3,
     "glr_block_match": 1, "glr_rerank_pixel": 1, "glr_xcorr_valid": 1,
 }
 launch_count = 0
